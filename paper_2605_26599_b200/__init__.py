@@ -1,0 +1,323 @@
+"""B200-native boundary-row (BR) eigenvalue-only tridiagonal eigensolver.
+
+Python mirror of the reference's public surface for this path
+(/root/reference/proj/include/br/):
+
+* ``TridiagonalMatrix(d, e)`` -- validates like tridiagonal.cpp:17-30 (InvalidArgument).
+* ``eigenvalues(T)``            -- the ``std::vector<double> eigenvalues_qrql(const
+  TridiagonalMatrix&)`` shape (qrql.hpp:20-23): all eigenvalues ascending, computed by the
+  GPU BR solver through the C ABI (include/brgpu.h).
+* ``br_eigenvalues(T, options)`` -- SPEC.md:348-356 ``BrResult{lambda, ledger}``.
+* ``Solver``                     -- an explicit handle (device, options, host/device/batched calls).
+* ``Error`` hierarchy            -- errors.hpp:9-60, one class per C-ABI status code.
+
+There is no CPU fallback: every solve runs the sm_100a kernels in ``libbrgpu.so``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+
+__all__ = [
+    "Error", "InvalidArgument", "NoConvergence", "BudgetExceeded", "PoleHit", "ZeroDenominator",
+    "MalformedCompactRoot", "DimensionMismatch", "DomainError", "DeviceError",
+    "TridiagonalMatrix", "Block", "find_irreducible_blocks", "Solver", "BrOptions", "BrResult",
+    "LedgerSnapshot", "eigenvalues", "br_eigenvalues", "workspace_query",
+]
+
+
+# --------------------------------------------------------------------- errors (errors.hpp:9-60)
+class Error(RuntimeError):
+    """Base class for all solver errors (br::Error)."""
+
+
+class BudgetExceeded(Error):
+    pass
+
+
+class NoConvergence(Error):
+    pass
+
+
+class PoleHit(Error):
+    pass
+
+
+class ZeroDenominator(Error):
+    pass
+
+
+class MalformedCompactRoot(Error):
+    pass
+
+
+class DomainError(Error):
+    pass
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class InvalidArgument(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / NCCL / no-device failures (no reference counterpart)."""
+
+
+_CODE = {1: InvalidArgument, 2: NoConvergence, 3: BudgetExceeded, 4: PoleHit, 5: ZeroDenominator,
+         6: MalformedCompactRoot, 7: DimensionMismatch, 8: DomainError, 9: DeviceError}
+
+
+def _raise(code: int, msg: str) -> None:
+    raise _CODE.get(code, DeviceError)(msg or f"status {code}")
+
+
+# ------------------------------------------------------------- input type (tridiagonal.hpp:12-25)
+class TridiagonalMatrix:
+    """Real symmetric tridiagonal matrix (diagonal d, off-diagonal e)."""
+
+    def __init__(self, d, e=None):
+        self.d = np.ascontiguousarray(d, dtype=np.float64).reshape(-1)
+        self.e = (np.ascontiguousarray(e, dtype=np.float64).reshape(-1) if e is not None
+                  else np.zeros(0))
+        self.n = len(self.d)
+        self.validate()
+
+    def validate(self) -> None:
+        if self.n == 0:
+            raise InvalidArgument("tridiagonal: order must be positive")
+        if len(self.e) + 1 != self.n:
+            raise InvalidArgument("tridiagonal: off-diagonal length != n-1")
+        if not np.all(np.isfinite(self.d)):
+            raise InvalidArgument("tridiagonal: non-finite diagonal entry")
+        if not np.all(np.isfinite(self.e)):
+            raise InvalidArgument("tridiagonal: non-finite off-diagonal entry")
+
+    def inf_norm(self) -> float:
+        row = np.abs(self.d).copy()
+        if self.n > 1:
+            row[:-1] += np.abs(self.e)
+            row[1:] += np.abs(self.e)
+        return float(row.max())
+
+
+@dataclass(frozen=True)
+class Block:
+    offset: int
+    size: int
+
+
+def find_irreducible_blocks(T: TridiagonalMatrix, tol: float) -> list[Block]:
+    """tridiagonal.cpp:45-58 (host mirror; the solver itself splits on the device)."""
+    if tol < 0:
+        raise InvalidArgument("find_irreducible_blocks: tol must be nonnegative")
+    split = np.nonzero(np.abs(T.e) <= tol * (np.abs(T.d[:-1]) + np.abs(T.d[1:])))[0]
+    starts = [0] + [int(i) + 1 for i in split] + [T.n]
+    return [Block(a, b - a) for a, b in zip(starts[:-1], starts[1:])]
+
+
+# --------------------------------------------------------------------------------- solver
+@dataclass
+class BrOptions:
+    leaf_cutoff: int = 25
+    zhat: bool = True
+    patched_stop: bool = True
+    use_graph: bool = True
+    subtree: bool = True
+
+
+@dataclass
+class LedgerSnapshot:
+    live_doubles: int
+    peak_doubles: int
+    live_ints: int
+    peak_ints: int
+    limit_doubles: int
+    limit_ints: int
+
+    def limit_bytes(self) -> int:
+        return self.limit_doubles * 8 + self.limit_ints * 4
+
+
+@dataclass
+class BrResult:
+    lam: np.ndarray
+    ledger: LedgerSnapshot
+    stats: dict = field(default_factory=dict)
+
+
+def workspace_query(n: int) -> tuple[int, int]:
+    dd, ii = C.c_int64(), C.c_int64()
+    rc = _native.lib().brgpu_workspace_query(int(n), C.byref(dd), C.byref(ii))
+    if rc:
+        _raise(rc, "workspace_query")
+    return dd.value, ii.value
+
+
+class Solver:
+    """One handle = one device + one stream (handles are independent; use one per thread)."""
+
+    def __init__(self, device: int = 0, options: BrOptions | None = None):
+        self._lib = _native.lib()
+        h = C.c_void_p()
+        rc = self._lib.brgpu_create(C.byref(h), int(device))
+        if rc:
+            _raise(rc, f"brgpu_create(device={device}): {self._lib.brgpu_status_string(rc).decode()}")
+        self._h = h
+        self.device = device
+        self.set_options(options or BrOptions())
+
+    # options --------------------------------------------------------------
+    def set_options(self, o: BrOptions) -> None:
+        self._opt(_native.OPT_LEAF_CUTOFF, o.leaf_cutoff)
+        self._opt(_native.OPT_ZHAT, int(o.zhat))
+        self._opt(_native.OPT_PATCHED_STOP, int(o.patched_stop))
+        self._opt(_native.OPT_USE_GRAPH, int(o.use_graph))
+        self._opt(_native.OPT_SUBTREE, int(o.subtree))
+        self.options = o
+
+    def _opt(self, k: int, v: int) -> None:
+        rc = self._lib.brgpu_set_option(self._h, k, int(v))
+        if rc:
+            self._fail(rc)
+
+    def _fail(self, rc: int) -> None:
+        msg = self._lib.brgpu_last_error_message(self._h)
+        _raise(rc, msg.decode() if msg else "")
+
+    # solves ---------------------------------------------------------------
+    def eigvals(self, d, e=None) -> np.ndarray:
+        """Host arrays in, ascending eigenvalues out (H2D + solve + D2H)."""
+        d = np.ascontiguousarray(d, dtype=np.float64).reshape(-1)
+        n = len(d)
+        e = np.ascontiguousarray(e if e is not None else np.zeros(0), dtype=np.float64).reshape(-1)
+        if n == 0:
+            raise InvalidArgument("tridiagonal: order must be positive")
+        if len(e) + 1 != n:
+            raise InvalidArgument("tridiagonal: off-diagonal length != n-1")
+        w = np.empty(n)
+        rc = self._lib.brgpu_eigvals(self._h, n, d.ctypes.data, e.ctypes.data if n > 1 else None,
+                                     w.ctypes.data)
+        if rc:
+            self._fail(rc)
+        return w
+
+    def eigvals_device(self, d, e, w=None, stream: int | None = None):
+        """torch.cuda float64 tensors in (resident in HBM), ascending eigenvalues in ``w``."""
+        import torch
+        n = d.numel()
+        if w is None:
+            w = torch.empty(n, dtype=torch.float64, device=d.device)
+        for t in (d, e, w):
+            if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+                raise InvalidArgument("eigvals_device: contiguous cuda float64 tensors required")
+        if e.numel() + 1 != n:
+            raise InvalidArgument("tridiagonal: off-diagonal length != n-1")
+        s = stream if stream is not None else torch.cuda.current_stream(d.device).cuda_stream
+        rc = self._lib.brgpu_eigvals_device(self._h, n, d.data_ptr(), e.data_ptr() if n > 1 else None,
+                                            w.data_ptr(), s)
+        if rc:
+            self._fail(rc)
+        return w
+
+    def eigvals_batched(self, d, e) -> np.ndarray:
+        """d (batch, n), e (batch, n-1) host arrays -> (batch, n) ascending per matrix."""
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        batch, n = d.shape
+        if e.shape != (batch, n - 1):
+            raise InvalidArgument("batched: e must be (batch, n-1)")
+        w = np.empty((batch, n))
+        rc = self._lib.brgpu_eigvals_batched(self._h, batch, n, d.ctypes.data,
+                                             e.ctypes.data if n > 1 else None, w.ctypes.data)
+        if rc:
+            self._fail(rc)
+        return w
+
+    def eigvals_batched_device(self, d, e, w=None, stream: int | None = None):
+        import torch
+        batch, n = d.shape
+        if w is None:
+            w = torch.empty((batch, n), dtype=torch.float64, device=d.device)
+        s = stream if stream is not None else torch.cuda.current_stream(d.device).cuda_stream
+        rc = self._lib.brgpu_eigvals_batched_device(self._h, batch, n, d.data_ptr(),
+                                                    e.data_ptr() if n > 1 else None, w.data_ptr(), s)
+        if rc:
+            self._fail(rc)
+        return w
+
+    # introspection --------------------------------------------------------
+    def reserve(self, n: int) -> None:
+        rc = self._lib.brgpu_reserve(self._h, int(n))
+        if rc:
+            self._fail(rc)
+
+    def stats(self) -> dict:
+        s = _native.Stats()
+        self._lib.brgpu_get_stats(self._h, C.byref(s))
+        return {f: getattr(s, f) for f, _ in _native.Stats._fields_}
+
+    def ledger(self) -> LedgerSnapshot:
+        l = _native.Ledger()
+        self._lib.brgpu_get_ledger(self._h, C.byref(l))
+        return LedgerSnapshot(*(getattr(l, f) for f, _ in _native.Ledger._fields_))
+
+    def set_trace(self, on: bool) -> None:
+        self._lib.brgpu_set_trace(self._h, int(on))
+
+    def trace(self) -> list[tuple]:
+        n = C.c_int64()
+        self._lib.brgpu_get_trace(self._h, None, 0, C.byref(n))
+        buf = (_native.Trace * max(n.value, 1))()
+        self._lib.brgpu_get_trace(self._h, buf, n.value, C.byref(n))
+        return [(t.level, t.is_root, t.offset, t.size, t.nn, t.k) for t in buf[: n.value]]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.brgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+_default: Solver | None = None
+
+
+def _solver() -> Solver:
+    global _default
+    if _default is None:
+        _default = Solver(0)
+    return _default
+
+
+def eigenvalues(T: TridiagonalMatrix) -> np.ndarray:
+    """All eigenvalues of T, ascending (the eigenvalues_qrql shape, qrql.hpp:20-23)."""
+    T.validate()
+    return _solver().eigvals(T.d, T.e)
+
+
+def br_eigenvalues(T: TridiagonalMatrix, options: BrOptions | None = None) -> BrResult:
+    """BR eigenvalues plus the workspace ledger snapshot."""
+    T.validate()
+    s = _solver()
+    if options is not None:
+        s.set_options(options)
+    lam = s.eigvals(T.d, T.e)
+    return BrResult(lam, s.ledger(), s.stats())

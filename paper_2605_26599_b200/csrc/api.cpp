@@ -1,0 +1,742 @@
+// api.cpp -- C ABI (include/brgpu.h), handle, workspace ledger and the host
+// planner of the B200 BR solver.
+//
+// Host responsibilities (everything O(#nodes), never O(n) per solve once the
+// plan is cached):
+//   * irreducible-block plan (tridiagonal.cpp:45-58): the device flags split
+//     points (k_scan_input); the host receives only their count, and the flag
+//     array when it is non-zero;
+//   * split trees per block (merge_tree.cpp:34-60), Cuppen cut list
+//     (merge_tree.cpp:78-92), leaf tasks, per-level merge tables;
+//   * the launch sequence (optionally replayed as one CUDA graph).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace brgpu {
+
+// kernels.cu
+void launch_scan_input(cudaStream_t s, int n, const double* d, const double* e, uint8_t* split,
+                       int* nsplit, int* status);
+void launch_scan_input_batched(cudaStream_t s, int batch, int n, const double* d, const double* e,
+                               double* dw, double* ew, uint8_t* split, int* nsplit, int* status);
+void launch_copy_input(cudaStream_t s, int n, const double* d, const double* e, double* dw, double* ew);
+void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned long long* sbits,
+                    double* dw, double* ew, int ncut, const int* cutPos, int* launches);
+void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const int* tSize,
+                   const int* tFlags, const Work& w, int* launches);
+void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
+                  int* launches);
+void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
+                        int* launches);
+void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
+                   const unsigned long long* sbits, double* lam, int* launches);
+void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
+                       int nruns, int* launches);
+
+}  // namespace brgpu
+
+using namespace brgpu;
+
+namespace {
+
+const char* kVersion = "brgpu 0.1 sm_100a fp64 (--fmad=false)";
+
+struct LevelHost {
+    int level;
+    int m0;      // first merge index (global across levels)
+    int M;       // merges at this level
+    int tile0;   // offset of this level's tileFirst table
+};
+
+struct Plan {
+    int n = 0;
+    int cutoff = 0;
+    std::vector<int> bstart;  // blocks (nblk + 1)
+    std::vector<int> segs;    // segment (matrix) boundaries for the final merge
+    // host tables
+    std::vector<int> tOff, tSize, tFlags;
+    std::vector<int> cutPos;
+    std::vector<int> mOff, mSize, mNL, mFlags, mLevel;
+    std::vector<int> tileFirst;
+    std::vector<LevelHost> levels;
+    std::vector<std::vector<int>> runPasses;  // run boundaries before each merge pass
+    int height = 0;
+    int maxM = 0;
+    int maxLeaf = 0;
+    // device copies
+    int* dev = nullptr;  // one int buffer
+    size_t devInts = 0;
+    int *d_tOff = nullptr, *d_tSize = nullptr, *d_tFlags = nullptr, *d_cut = nullptr;
+    int *d_mOff = nullptr, *d_mSize = nullptr, *d_mNL = nullptr, *d_mFlags = nullptr;
+    int *d_tileFirst = nullptr, *d_bstart = nullptr;
+    std::vector<int*> d_runs;
+    cudaGraphExec_t graph = nullptr;
+    bool graph_trace = false;
+    uint64_t graph_gen = 0;
+    int launches = 0;
+};
+
+struct Handle {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int leaf_cutoff = 25;
+    int zhat = 1;
+    int patched = 1;
+    int use_graph = 1;
+    int subtree = 1;
+    int trace = 0;
+    double tol_scale = 1.0;
+    std::string err;
+    // workspace
+    int64_t cap = 0;
+    Work w{};
+    uint8_t* split = nullptr;
+    unsigned long long* sbits = nullptr;  // per block scale bits
+    int64_t sbitsCap = 0;
+    unsigned long long* mTol = nullptr;
+    int64_t mTolCap = 0;
+    int* traceBuf = nullptr;  // 2 ints per merge
+    int64_t traceCap = 0;
+    // io staging
+    double* io = nullptr;   // device d, e, w for host API (3n)
+    int64_t ioCap = 0;
+    double* pinned = nullptr;
+    int64_t pinnedCap = 0;
+    int* hsmall = nullptr;  // pinned: [0]=nsplit [1]=status
+    unsigned long long* hcnt = nullptr;
+    int* dsmall = nullptr;  // device: [0]=nsplit [1..]=unused
+    // ledger
+    int64_t ledger_doubles = 0, ledger_ints = 0, peak_doubles = 0, peak_ints = 0, limit_n = 0;
+    // plan cache
+    std::unique_ptr<Plan> plan;
+    uint64_t bufgen = 1;  // bumped whenever a buffer baked into a graph moves
+    brgpu_stats stats{};
+    std::vector<brgpu_trace> traceRecs;
+};
+
+int fail(Handle* h, int code, const std::string& msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+#define CUDA_TRY(h, call)                                                              \
+    do {                                                                               \
+        cudaError_t e__ = (call);                                                      \
+        if (e__ != cudaSuccess)                                                        \
+            return fail((h), BRGPU_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// planning
+// ---------------------------------------------------------------------------
+struct NodeRec {
+    int off, size, nl, level, root;
+};
+
+int build_node(int off, int size, int cutoff, bool root, std::vector<NodeRec>& internal,
+               std::vector<std::pair<int, int>>& leaves) {
+    if (size <= cutoff) {
+        leaves.emplace_back(off, size);
+        return 0;
+    }
+    const int nl = size / 2;
+    const int idx = (int)internal.size();
+    internal.push_back({off, size, nl, 0, root ? 1 : 0});
+    const int ll = build_node(off, nl, cutoff, false, internal, leaves);
+    const int rl = build_node(off + nl, size - nl, cutoff, false, internal, leaves);
+    const int lev = 1 + std::max(ll, rl);
+    internal[idx].level = lev;
+    return lev;
+}
+
+std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
+                                const std::vector<int>& segs) {
+    auto p = std::make_unique<Plan>();
+    p->n = n;
+    p->cutoff = cutoff;
+    p->bstart = bstart;
+    p->segs = segs;
+    std::vector<NodeRec> internal;
+    std::vector<std::pair<int, int>> leaves;
+    const int nblk = (int)bstart.size() - 1;
+    for (int b = 0; b < nblk; ++b) {
+        const int off = bstart[b], sz = bstart[b + 1] - off;
+        if (sz <= cutoff) {
+            p->tOff.push_back(off);
+            p->tSize.push_back(sz);
+            p->tFlags.push_back(1);  // values only
+            p->maxLeaf = std::max(p->maxLeaf, sz);
+            continue;
+        }
+        const int h = build_node(off, sz, cutoff, true, internal, leaves);
+        p->height = std::max(p->height, h);
+    }
+    for (auto& lf : leaves) {
+        p->tOff.push_back(lf.first);
+        p->tSize.push_back(lf.second);
+        p->tFlags.push_back(0);
+        p->maxLeaf = std::max(p->maxLeaf, lf.second);
+    }
+    for (auto& nd : internal) p->cutPos.push_back(nd.off + nd.nl - 1);
+    // merges grouped by level, offset order
+    std::stable_sort(internal.begin(), internal.end(), [](const NodeRec& a, const NodeRec& b) {
+        return a.level != b.level ? a.level < b.level : a.off < b.off;
+    });
+    const int ntiles = (n + kTile - 1) / kTile;
+    size_t i = 0;
+    while (i < internal.size()) {
+        const int lev = internal[i].level;
+        LevelHost L;
+        L.level = lev;
+        L.m0 = (int)p->mOff.size();
+        L.tile0 = (int)p->tileFirst.size();
+        size_t j = i;
+        while (j < internal.size() && internal[j].level == lev) {
+            p->mOff.push_back(internal[j].off);
+            p->mSize.push_back(internal[j].size);
+            p->mNL.push_back(internal[j].nl);
+            p->mFlags.push_back(internal[j].root ? kMergeRoot : 0);
+            p->mLevel.push_back(lev);
+            ++j;
+        }
+        L.M = (int)(j - i);
+        p->maxM = std::max(p->maxM, L.M);
+        // tileFirst[t] = first merge whose end exceeds t*kTile
+        int m = 0;
+        for (int t = 0; t <= ntiles; ++t) {
+            const long long start = (long long)t * kTile;
+            while (m < L.M && (long long)p->mOff[L.m0 + m] + p->mSize[L.m0 + m] <= start) ++m;
+            p->tileFirst.push_back(m);
+        }
+        p->levels.push_back(L);
+        i = j;
+    }
+    // final merge passes: runs = blocks, merged pairwise inside each segment;
+    // a segment with an odd run count gets an empty partner so that pairs
+    // (2k, 2k+1) of a pass table never straddle segments.
+    {
+        std::vector<int> runs = bstart;
+        for (;;) {
+            bool any = false;
+            std::vector<int> pass{0};
+            size_t r = 0;
+            const size_t nr = runs.size() - 1;
+            for (size_t sg = 0; sg + 1 < segs.size(); ++sg) {
+                const int segEnd = segs[sg + 1];
+                size_t cnt = 0;
+                while (r < nr && runs[r + 1] <= segEnd) { pass.push_back(runs[r + 1]); ++r; ++cnt; }
+                if (cnt > 1) any = true;
+                if (cnt % 2) pass.push_back(segEnd);
+            }
+            if (!any) break;
+            p->runPasses.push_back(pass);
+            std::vector<int> nxt;
+            for (size_t k = 0; k < pass.size(); k += 2)
+                if (nxt.empty() || nxt.back() != pass[k]) nxt.push_back(pass[k]);
+            runs = nxt;
+        }
+    }
+    return p;
+}
+
+int upload_plan(Handle* h, Plan* p) {
+    std::vector<int> buf;
+    auto put = [&](const std::vector<int>& v) {
+        const size_t o = buf.size();
+        buf.insert(buf.end(), v.begin(), v.end());
+        while (buf.size() % 4) buf.push_back(0);
+        return o;
+    };
+    const size_t oTOff = put(p->tOff), oTSize = put(p->tSize), oTFlags = put(p->tFlags);
+    const size_t oCut = put(p->cutPos);
+    const size_t oMOff = put(p->mOff), oMSize = put(p->mSize), oMNL = put(p->mNL), oMF = put(p->mFlags);
+    const size_t oTile = put(p->tileFirst);
+    const size_t oB = put(p->bstart);
+    std::vector<size_t> oRuns;
+    for (auto& rp : p->runPasses) oRuns.push_back(put(rp));
+    p->devInts = buf.size();
+    CUDA_TRY(h, cudaMalloc(&p->dev, sizeof(int) * std::max<size_t>(buf.size(), 1)));
+    CUDA_TRY(h, cudaMemcpy(p->dev, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice));
+    p->d_tOff = p->dev + oTOff; p->d_tSize = p->dev + oTSize; p->d_tFlags = p->dev + oTFlags;
+    p->d_cut = p->dev + oCut;
+    p->d_mOff = p->dev + oMOff; p->d_mSize = p->dev + oMSize; p->d_mNL = p->dev + oMNL;
+    p->d_mFlags = p->dev + oMF; p->d_tileFirst = p->dev + oTile; p->d_bstart = p->dev + oB;
+    for (size_t o : oRuns) p->d_runs.push_back(p->dev + o);
+    return BRGPU_OK;
+}
+
+void free_plan(Plan* p) {
+    if (!p) return;
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    if (p->dev) cudaFree(p->dev);
+    p->graph = nullptr;
+    p->dev = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// workspace
+// ---------------------------------------------------------------------------
+void free_work(Handle* h) {
+    if (h->cap == 0) return;
+    cudaFree(h->w.dw);
+    cudaFree(h->w.nnPre);
+    cudaFree(h->w.nnFlag);
+    h->w = Work{};
+    h->cap = 0;
+    h->ledger_doubles = h->ledger_ints = 0;
+}
+
+int ensure_work(Handle* h, int64_t n) {
+    if (n <= h->cap) return BRGPU_OK;
+    if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
+    free_work(h);
+    const int64_t c = (std::max<int64_t>(n, 1024) + 1023) / 1024 * 1024;
+    const int64_t nd = 15 * c;
+    double* dbl = nullptr;
+    CUDA_TRY(h, cudaMalloc(&dbl, sizeof(double) * nd));
+    Work& w = h->w;
+    w.dw = dbl; w.ew = dbl + c; w.lam = dbl + 2 * c; w.blo = dbl + 3 * c; w.bhi = dbl + 4 * c;
+    w.D = dbl + 5 * c; w.Z = dbl + 6 * c; w.R0 = dbl + 7 * c; w.R1 = dbl + 8 * c;
+    w.dA = dbl + 9 * c; w.zA = dbl + 10 * c; w.z2A = dbl + 11 * c; w.r0A = dbl + 12 * c;
+    w.r1A = dbl + 13 * c; w.tau = dbl + 14 * c;
+    const int64_t ntiles = (c + 1023) / 1024 + 1;
+    const int64_t ni = 5 * c + 2 + 2 * ntiles + 8;
+    int* ib = nullptr;
+    CUDA_TRY(h, cudaMalloc(&ib, sizeof(int) * ni));
+    w.nnPre = ib; w.nnPos = ib + c + 1; w.survPre = ib + 2 * c + 1; w.aMerge = ib + 3 * c + 2;
+    w.org = ib + 4 * c + 2; w.tileCnt = ib + 5 * c + 2; w.tileOff = ib + 5 * c + 2 + ntiles;
+    w.status = ib + 5 * c + 2 + 2 * ntiles;
+    uint8_t* bb = nullptr;
+    CUDA_TRY(h, cudaMalloc(&bb, 3 * c + 64));
+    w.nnFlag = bb; w.survFlag = bb + c; h->split = bb + 2 * c;
+    w.counters = reinterpret_cast<unsigned long long*>(bb + 3 * c);  // 8-byte aligned (c%8==0? pad)
+    h->cap = c;
+    ++h->bufgen;
+    h->ledger_doubles = nd;
+    h->ledger_ints = ni + (3 * c + 64 + 3) / 4;
+    h->peak_doubles = std::max(h->peak_doubles, h->ledger_doubles);
+    h->peak_ints = std::max(h->peak_ints, h->ledger_ints);
+    h->limit_n = c;
+    return BRGPU_OK;
+}
+
+template <typename T>
+int ensure_buf(Handle* h, T*& p, int64_t& cap, int64_t need) {
+    if (need <= cap) return BRGPU_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    CUDA_TRY(h, cudaMalloc(&p, sizeof(T) * std::max<int64_t>(need, 1)));
+    cap = need;
+    ++h->bufgen;
+    return BRGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// solve
+// ---------------------------------------------------------------------------
+int status_message(Handle* h, int st) {
+    switch (st) {
+        case BRGPU_ERR_INVALID_ARGUMENT: return fail(h, st, "tridiagonal: non-finite entry");
+        case BRGPU_ERR_NO_CONVERGENCE: return fail(h, st, "no convergence (QL/QR sweep limit or secular iteration)");
+        case BRGPU_ERR_ZERO_DENOMINATOR: return fail(h, st, "secular_column: reconstructed delta is zero");
+        default: return fail(h, st, "device error " + std::to_string(st));
+    }
+}
+
+int run_plan(Handle* h, Plan* p, int* launches) {
+    cudaStream_t s = h->stream;
+    const int n = p->n;
+    const int nblk = (int)p->bstart.size() - 1;
+    launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
+                   p->d_cut, launches);
+    launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
+                  launches);
+    SolveParams prm{n, h->zhat, h->patched, h->tol_scale};
+    for (const LevelHost& lh : p->levels) {
+        LevelDev L;
+        L.mOff = p->d_mOff + lh.m0;
+        L.mSize = p->d_mSize + lh.m0;
+        L.mNL = p->d_mNL + lh.m0;
+        L.mFlags = p->d_mFlags + lh.m0;
+        L.mTol = h->mTol;
+        L.tileFirst = p->d_tileFirst + lh.tile0;
+        L.M = lh.M;
+        launch_level(s, h->w, L, n, prm, launches);
+        if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches);
+    }
+    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches);
+    // cross-block merge passes (ping-pong lam <-> D), result back in lam
+    double* src = h->w.lam;
+    double* dst = h->w.D;
+    for (size_t q = 0; q < p->runPasses.size(); ++q) {
+        launch_merge_runs(s, n, src, dst, p->d_runs[q], (int)p->runPasses[q].size() - 1, launches);
+        std::swap(src, dst);
+    }
+    if (src != h->w.lam) {
+        cudaMemcpyAsync(h->w.lam, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    }
+    return BRGPU_OK;
+}
+
+// After the input has been copied to dw/ew and split flags computed, finish the solve.
+int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
+    cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaMemcpyAsync(h->hsmall, h->dsmall, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    if (h->hsmall[1]) return status_message(h, h->hsmall[1]);
+    const int nsplit = h->hsmall[0];
+    std::vector<int> bstart;
+    if (nsplit == 0) {
+        bstart = segs;
+    } else {
+        // split flags mark natural splits; segment (matrix) ends are implied
+        std::vector<uint8_t> fl((size_t)n);
+        CUDA_TRY(h, cudaMemcpy(fl.data(), h->split, (size_t)n, cudaMemcpyDeviceToHost));
+        size_t sg = 1;
+        bstart.push_back(0);
+        for (int i = 0; i + 1 < n; ++i) {
+            const bool segEnd = sg + 1 < segs.size() && segs[sg] == i + 1;
+            if (segEnd) ++sg;
+            if (fl[(size_t)i] || segEnd) bstart.push_back(i + 1);
+        }
+        bstart.push_back(n);
+    }
+    Plan* p = h->plan.get();
+    if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs) {
+        if (h->plan) free_plan(h->plan.get());
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs);
+        p = h->plan.get();
+        int r = upload_plan(h, p);
+        if (r) return r;
+    }
+    if (int r = ensure_buf(h, h->sbits, h->sbitsCap, (int64_t)bstart.size())) return r;
+    if (int r = ensure_buf(h, h->mTol, h->mTolCap, std::max(p->maxM, 1))) return r;
+    if (h->trace)
+        if (int r = ensure_buf(h, h->traceBuf, h->traceCap, 2 * (int64_t)std::max<size_t>(p->mOff.size(), 1))) return r;
+    CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
+    CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 4, s));
+    int launches = 0;
+    const bool want_graph = h->use_graph != 0;
+    if (want_graph) {
+        if (!p->graph || p->graph_trace != (h->trace != 0) || p->graph_gen != h->bufgen) {
+            if (p->graph) { cudaGraphExecDestroy(p->graph); p->graph = nullptr; }
+            cudaGraph_t g;
+            CUDA_TRY(h, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int r = run_plan(h, p, &launches);
+            cudaError_t ce = cudaStreamEndCapture(s, &g);
+            if (r) return r;
+            if (ce != cudaSuccess) return fail(h, BRGPU_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+            CUDA_TRY(h, cudaGraphInstantiate(&p->graph, g, 0));
+            cudaGraphDestroy(g);
+            p->graph_trace = h->trace != 0;
+            p->graph_gen = h->bufgen;
+            p->launches = launches;
+        }
+        launches = p->launches;
+        CUDA_TRY(h, cudaGraphLaunch(p->graph, s));
+        h->stats.graph_replayed = 1;
+    } else {
+        int r = run_plan(h, p, &launches);
+        if (r) return r;
+        h->stats.graph_replayed = 0;
+    }
+    CUDA_TRY(h, cudaGetLastError());
+    h->stats.kernel_launches = launches + 2;  // + input copy and scan
+    h->stats.n = n;
+    h->stats.blocks = (int)bstart.size() - 1;
+    h->stats.height = p->height;
+    h->stats.merges = (int64_t)p->mOff.size();
+    return BRGPU_OK;
+}
+
+int finish_solve(Handle* h) {
+    cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    h->stats.evals = (int64_t)h->hcnt[0];
+    h->stats.pole_terms = (double)h->hcnt[1];
+    if (h->trace && h->plan) {
+        Plan* p = h->plan.get();
+        const size_t M = p->mOff.size();
+        std::vector<int> tb(2 * M);
+        if (M) CUDA_TRY(h, cudaMemcpy(tb.data(), h->traceBuf, sizeof(int) * 2 * M, cudaMemcpyDeviceToHost));
+        h->traceRecs.resize(M);
+        double sk2 = 0, szt = 0;
+        int64_t sk = 0, snn = 0, mk = 0;
+        for (size_t m = 0; m < M; ++m) {
+            brgpu_trace& t = h->traceRecs[m];
+            t.level = p->mLevel[m];
+            t.is_root = p->mFlags[m] & kMergeRoot;
+            t.offset = p->mOff[m];
+            t.size = p->mSize[m];
+            t.nn = tb[2 * m];
+            t.k = tb[2 * m + 1];
+            sk += t.k; snn += t.nn; sk2 += (double)t.k * (double)t.k;
+            if (!t.is_root) szt += (double)t.k * (double)t.k;
+            mk = std::max<int64_t>(mk, t.k);
+        }
+        h->stats.sum_k = sk; h->stats.sum_k2 = sk2; h->stats.sum_nn = snn;
+        h->stats.row_terms = szt; h->stats.zhat_terms = h->zhat ? szt : 0.0; h->stats.max_k = mk;
+        h->stats.rotations = snn - sk;
+    }
+    if (h->hsmall[1]) return status_message(h, h->hsmall[1]);
+    return BRGPU_OK;
+}
+
+int solve_device(Handle* h, int64_t n64, const double* d, const double* e, double* w_out,
+                 bool w_host) {
+    if (n64 <= 0 || n64 >= (int64_t)1 << 31) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be positive (and < 2^31)");
+    const int n = (int)n64;
+    if (int r = ensure_work(h, n64)) return r;
+    cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaMemsetAsync(h->dsmall, 0, sizeof(int) * 2, s));
+    CUDA_TRY(h, cudaMemsetAsync(h->w.status, 0, sizeof(int), s));
+    launch_copy_input(s, n, d, e, h->w.dw, h->w.ew);
+    launch_scan_input(s, n, h->w.dw, h->w.ew, h->split, h->dsmall, h->w.status);
+    int r = solve_prepared(h, n, {0, n});
+    if (r) return r;
+    if (w_host)
+        CUDA_TRY(h, cudaMemcpyAsync(w_out, h->w.lam, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    else if (w_out != h->w.lam)
+        CUDA_TRY(h, cudaMemcpyAsync(w_out, h->w.lam, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    return finish_solve(h);
+}
+
+}  // namespace
+
+struct brgpu_handle {
+    Handle h;
+};
+
+extern "C" {
+
+const char* brgpu_version(void) { return kVersion; }
+
+const char* brgpu_status_string(int st) {
+    switch (st) {
+        case BRGPU_OK: return "ok";
+        case BRGPU_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+        case BRGPU_ERR_NO_CONVERGENCE: return "NoConvergence";
+        case BRGPU_ERR_BUDGET_EXCEEDED: return "BudgetExceeded";
+        case BRGPU_ERR_POLE_HIT: return "PoleHit";
+        case BRGPU_ERR_ZERO_DENOMINATOR: return "ZeroDenominator";
+        case BRGPU_ERR_MALFORMED_COMPACT_ROOT: return "MalformedCompactRoot";
+        case BRGPU_ERR_DIMENSION_MISMATCH: return "DimensionMismatch";
+        case BRGPU_ERR_DOMAIN_ERROR: return "DomainError";
+        case BRGPU_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+        case BRGPU_ERR_CUDA: return "CudaError";
+        case BRGPU_ERR_NCCL: return "NcclError";
+        case BRGPU_ERR_NO_DEVICE: return "NoDevice";
+        default: return "unknown";
+    }
+}
+
+int brgpu_create(brgpu_handle** out, int device) {
+    if (!out) return BRGPU_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return BRGPU_ERR_NO_DEVICE;
+    }
+    if (device < 0 || device >= ndev) return BRGPU_ERR_INVALID_ARGUMENT;
+    auto* hh = new brgpu_handle();
+    Handle* h = &hh->h;
+    h->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMallocHost(&h->hsmall, sizeof(int) * 4) != cudaSuccess ||
+        cudaMallocHost(&h->hcnt, sizeof(unsigned long long) * 4) != cudaSuccess ||
+        cudaMalloc(&h->dsmall, sizeof(int) * 4) != cudaSuccess) {
+        delete hh;
+        return BRGPU_ERR_CUDA;
+    }
+    *out = hh;
+    return BRGPU_OK;
+}
+
+int brgpu_destroy(brgpu_handle* hh) {
+    if (!hh) return BRGPU_OK;
+    Handle* h = &hh->h;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->plan) free_plan(h->plan.get());
+    free_work(h);
+    if (h->sbits) cudaFree(h->sbits);
+    if (h->mTol) cudaFree(h->mTol);
+    if (h->traceBuf) cudaFree(h->traceBuf);
+    if (h->io) cudaFree(h->io);
+    if (h->pinned) cudaFreeHost(h->pinned);
+    if (h->hsmall) cudaFreeHost(h->hsmall);
+    if (h->hcnt) cudaFreeHost(h->hcnt);
+    if (h->dsmall) cudaFree(h->dsmall);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete hh;
+    return BRGPU_OK;
+}
+
+const char* brgpu_last_error_message(const brgpu_handle* hh) { return hh ? hh->h.err.c_str() : "null handle"; }
+
+int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    switch (opt) {
+        case BRGPU_OPT_LEAF_CUTOFF:
+            if (v < 5 || v > 32) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "leaf cutoff must be in [5, 32]");
+            h->leaf_cutoff = (int)v;
+            return BRGPU_OK;
+        case BRGPU_OPT_ZHAT: h->zhat = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        case BRGPU_OPT_PATCHED_STOP: h->patched = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        case BRGPU_OPT_USE_GRAPH: h->use_graph = v != 0; return BRGPU_OK;
+        case BRGPU_OPT_SUBTREE: h->subtree = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        default: return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "unknown option");
+    }
+}
+
+int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
+    if (!hh || !v) return BRGPU_ERR_INVALID_ARGUMENT;
+    const Handle* h = &hh->h;
+    switch (opt) {
+        case BRGPU_OPT_LEAF_CUTOFF: *v = h->leaf_cutoff; return BRGPU_OK;
+        case BRGPU_OPT_ZHAT: *v = h->zhat; return BRGPU_OK;
+        case BRGPU_OPT_PATCHED_STOP: *v = h->patched; return BRGPU_OK;
+        case BRGPU_OPT_USE_GRAPH: *v = h->use_graph; return BRGPU_OK;
+        case BRGPU_OPT_SUBTREE: *v = h->subtree; return BRGPU_OK;
+        default: return BRGPU_ERR_INVALID_ARGUMENT;
+    }
+}
+
+int brgpu_workspace_query(int64_t n, int64_t* doubles, int64_t* ints) {
+    if (n <= 0) return BRGPU_ERR_INVALID_ARGUMENT;
+    if (doubles) *doubles = 16 * n;
+    if (ints) *ints = 7 * n;
+    return BRGPU_OK;
+}
+
+int brgpu_reserve(brgpu_handle* hh, int64_t n) {
+    if (!hh || n <= 0) return BRGPU_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(hh->h.device);
+    return ensure_work(&hh->h, n);
+}
+
+int brgpu_get_ledger(const brgpu_handle* hh, brgpu_ledger* out) {
+    if (!hh || !out) return BRGPU_ERR_INVALID_ARGUMENT;
+    const Handle* h = &hh->h;
+    out->live_doubles = h->ledger_doubles;
+    out->peak_doubles = h->peak_doubles;
+    out->live_ints = h->ledger_ints + (h->plan ? (int64_t)h->plan->devInts : 0) + 2 * h->mTolCap;
+    out->peak_ints = std::max(h->peak_ints, out->live_ints);
+    out->limit_doubles = 16 * h->limit_n;
+    out->limit_ints = 7 * h->limit_n;
+    return BRGPU_OK;
+}
+
+int brgpu_eigvals(brgpu_handle* hh, int64_t n, const double* d, const double* e, double* w) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (n <= 0 || !d || !w || (n > 1 && !e)) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be positive");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    if (int r = ensure_buf(h, h->io, h->ioCap, 2 * n)) return r;
+    cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaMemcpyAsync(h->io, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->io + n, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, s));
+    return solve_device(h, n, h->io, h->io + n, w, true);
+}
+
+int brgpu_eigvals_device(brgpu_handle* hh, int64_t n, const double* d, const double* e, double* w,
+                         void* stream) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (n <= 0 || !d || !w || (n > 1 && !e)) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be positive");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    cudaStream_t user = (cudaStream_t)stream;
+    cudaEvent_t ev = nullptr;
+    if (user) {
+        // order the handle stream after the caller's stream
+        CUDA_TRY(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventRecord(ev, user));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    return solve_device(h, n, d, e, w, false);
+}
+
+int brgpu_eigvals_batched_device(brgpu_handle* hh, int64_t batch, int64_t n, const double* d,
+                                 const double* e, double* w, void* stream) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (batch <= 0 || n <= 0 || !d || !w || (n > 1 && !e)) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "batched: bad sizes");
+    const int64_t N = batch * n;
+    if (N >= (int64_t)1 << 31) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "batched: batch*n must be < 2^31");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    if (stream) {
+        cudaEvent_t ev;
+        CUDA_TRY(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventRecord(ev, (cudaStream_t)stream));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    if (int r = ensure_work(h, N)) return r;
+    cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaMemsetAsync(h->dsmall, 0, sizeof(int) * 2, s));
+    CUDA_TRY(h, cudaMemsetAsync(h->w.status, 0, sizeof(int), s));
+    launch_scan_input_batched(s, (int)batch, (int)n, d, e, h->w.dw, h->w.ew, h->split, h->dsmall, h->w.status);
+    std::vector<int> segs;
+    for (int64_t b = 0; b <= batch; ++b) segs.push_back((int)(b * n));
+    int r = solve_prepared(h, (int)N, segs);
+    if (r) return r;
+    if (w != h->w.lam)
+        CUDA_TRY(h, cudaMemcpyAsync(w, h->w.lam, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    return finish_solve(h);
+}
+
+int brgpu_eigvals_batched(brgpu_handle* hh, int64_t batch, int64_t n, const double* d,
+                          const double* e, double* w) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (batch <= 0 || n <= 0 || !d || !w || (n > 1 && !e)) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "batched: bad sizes");
+    const int64_t N = batch * n;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    if (int r = ensure_buf(h, h->io, h->ioCap, 3 * N)) return r;
+    cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaMemcpyAsync(h->io, d, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->io + N, e, sizeof(double) * batch * (n - 1), cudaMemcpyHostToDevice, s));
+    int r = brgpu_eigvals_batched_device(hh, batch, n, h->io, h->io + N, h->io + 2 * N, nullptr);
+    if (r) return r;
+    CUDA_TRY(h, cudaMemcpy(w, h->io + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    return BRGPU_OK;
+}
+
+int brgpu_get_stats(const brgpu_handle* hh, brgpu_stats* out) {
+    if (!hh || !out) return BRGPU_ERR_INVALID_ARGUMENT;
+    *out = hh->h.stats;
+    return BRGPU_OK;
+}
+
+int brgpu_set_trace(brgpu_handle* hh, int enable) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    hh->h.trace = enable != 0;
+    return BRGPU_OK;
+}
+
+int brgpu_get_trace(const brgpu_handle* hh, brgpu_trace* out, int64_t cap, int64_t* len) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    const auto& v = hh->h.traceRecs;
+    if (len) *len = (int64_t)v.size();
+    if (out) for (int64_t i = 0; i < cap && i < (int64_t)v.size(); ++i) out[i] = v[(size_t)i];
+    return BRGPU_OK;
+}
+
+}  // extern "C"

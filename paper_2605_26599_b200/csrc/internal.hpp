@@ -1,0 +1,75 @@
+// internal.hpp -- structures shared by the host planner (api.cpp) and the
+// sm_100a kernels (kernels.cu).  Positions are int32 (n < 2^31).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/brgpu.h"
+
+#ifndef __CUDACC__
+#ifndef __host__
+#define __host__
+#define __device__
+#endif
+#endif
+
+namespace brgpu {
+
+// Tile width used to map a position to the merge containing it: tileFirst[t]
+// is the first merge (of a level) that ends after position t*kTile.
+constexpr int kTile = 256;
+
+// Merge flags.
+constexpr int kMergeRoot = 1;   // block root: root-only mode
+
+// Device-resident workspace (all arrays sized for the reserved capacity).
+// Doubles: dw, ew, lam, blo, bhi, D, Z, R0, R1, dA, zA, z2A, r0A, r1A, tau  (15n)
+// Ints   : nnPre(n+1), nnPos, survPre(n+1), aMerge, org, + byte flags (~5.5n)
+struct Work {
+    double* dw;      // scaled, Cuppen-cut diagonal
+    double* ew;      // scaled off-diagonal
+    double* lam;     // node eigenvalues (ascending per node); final output
+    double* blo;     // node first eigenvector row
+    double* bhi;     // node last eigenvector row
+    double* D;       // merged (sorted) poles
+    double* Z;       // merged z (rotated in place by close-pole deflation)
+    double* R0;      // merged first selected row
+    double* R1;      // merged last selected row
+    double* dA;      // compacted active poles (global active index)
+    double* zA;      // compacted active weights; replaced by z-hat
+    double* z2A;     // zA^2
+    double* r0A;
+    double* r1A;
+    double* tau;     // root offsets
+    int* nnPre;      // exclusive prefix of non-negligible flags over positions (n+1)
+    int* nnPos;      // NN index -> sorted position
+    int* survPre;    // exclusive prefix of survivor flags over NN indices (n+1)
+    int* aMerge;     // active index -> merge id (within level)
+    int* org;        // root origin (merge-local pole index)
+    uint8_t* nnFlag;
+    uint8_t* survFlag;
+    int* tileCnt;    // per-1024 tile counts (scan scratch)
+    int* tileOff;
+    int* status;     // first error code
+    unsigned long long* counters;  // [0] evals
+};
+
+// One level's merges (device pointers into the plan arrays).
+struct LevelDev {
+    const int* mOff;
+    const int* mSize;
+    const int* mNL;
+    const int* mFlags;
+    unsigned long long* mTol;  // max(|D|,|z|) bits per merge (atomicMax)
+    const int* tileFirst;      // ceil(n/kTile)+1 entries
+    int M;
+};
+
+struct SolveParams {
+    int n;
+    int zhat;
+    int patched;
+    double tol_scale;
+};
+
+}  // namespace brgpu

@@ -1,0 +1,702 @@
+// kernels.cu -- sm_100a kernels of the boundary-row (BR) eigenvalue-only
+// divide-and-conquer tridiagonal eigensolver.  Built with --fmad=false (see
+// numerics.cuh).  Every kernel is launched by the host planner in api.cpp.
+//
+// Level pipeline (grid tier; one launch per step covers ALL merges of a
+// level, positions are level-global so no host round trip is needed):
+//   k_merge_tol      max(|D|,|z|) per merge              deflate.cpp:55-60
+//   k_merge_scatter  stable merge of the sorted children deflate.cpp:62-66, build_z deflate.cpp:31-41
+//   k_nn_flag/…      small-z flags + compaction          deflate.cpp:70-75
+//   k_segment_walk   close-pole Givens walk per segment  deflate.cpp:76-95, 109-140
+//   k_surv_*         survivor compaction                 deflate.cpp:100-105
+//   k_secular        one root per thread                 secular.cpp:80-241
+//   k_zhat           refreshed weights, one pole/thread  secular.cpp:288-313
+//   k_rows           R_parent(:,j) = R_child y_j + parent placement
+//   k_deflated_out   deflated columns to parent order
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.hpp"
+#include "numerics.cuh"
+
+namespace brgpu {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void set_status(int* status, int code) {
+    if (code) atomicCAS(status, 0, code);
+}
+
+// number of x[0..n) with x < v   (x ascending)
+__device__ __forceinline__ int count_less(const double* __restrict__ x, int n, double v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (x[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+// number of x[0..n) with x <= v  (x ascending)
+__device__ __forceinline__ int count_leq(const double* __restrict__ x, int n, double v) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (!(v < x[mid])) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int find_merge(const LevelDev& L, int p) {
+    const int t = p / kTile;
+    int m = L.tileFirst[t];
+    const int last = L.tileFirst[t + 1] < L.M ? L.tileFirst[t + 1] : L.M - 1;
+    while (m < last && L.mOff[m + 1] <= p) ++m;
+    if (m >= L.M || m < 0) return -1;
+    const int off = L.mOff[m];
+    if (p < off || p >= off + L.mSize[m]) return -1;
+    return m;
+}
+
+__device__ __forceinline__ double merge_tol(const LevelDev& L, int m, double tol_scale) {
+    const double mx = __longlong_as_double((long long)L.mTol[m]);
+    return 8.0 * kU * mx * tol_scale;
+}
+
+// Active range [ks, ke) of merge m in the level-global compacted arrays.
+__device__ __forceinline__ void active_range(const Work& w, const LevelDev& L, int m, int& ks, int& ke) {
+    const int off = L.mOff[m];
+    ks = w.survPre[w.nnPre[off]];
+    ke = w.survPre[w.nnPre[off + L.mSize[m]]];
+}
+
+template <int BLOCK>
+__device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
+    __shared__ int warp_tot[BLOCK / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < BLOCK / 32 ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < BLOCK / 32) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const int base = wid ? warp_tot[wid - 1] : 0;
+    total = warp_tot[BLOCK / 32 - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ int block_sum(int v) {
+    __shared__ int red[BLOCK / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    int t = 0;
+    if (threadIdx.x < 32) {
+        t = lane < BLOCK / 32 ? red[lane] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    return t;  // valid in thread 0
+}
+
+constexpr int kScanBlock = 1024;
+
+// ---------------------------------------------------------------------------
+// input validation + irreducible block split (tridiagonal.cpp:17-30, 45-58)
+// ---------------------------------------------------------------------------
+__global__ void k_copy_input(int n, const double* __restrict__ d, const double* __restrict__ e,
+                             double* __restrict__ dw, double* __restrict__ ew) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    dw[i] = d[i];
+    ew[i] = i + 1 < n ? e[i] : 0.0;
+}
+
+// dw/ew hold the input; flags split points |e_i| <= u(|d_i|+|d_{i+1}|)
+__global__ void k_scan_input(int n, const double* __restrict__ d, const double* __restrict__ e,
+                             uint8_t* __restrict__ split, int* __restrict__ nsplit,
+                             int* __restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int cnt = 0;
+    if (i < n) {
+        const double di = d[i];
+        bool bad = !isfinite(di);
+        uint8_t s = 0;
+        if (i + 1 < n) {
+            const double ei = e[i];
+            bad |= !isfinite(ei);
+            s = fabs(ei) <= kU * (fabs(di) + fabs(d[i + 1]));
+        }
+        if (bad) set_status(status, BRGPU_ERR_INVALID_ARGUMENT);
+        split[i] = s;
+        cnt = s;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nsplit, cnt);
+}
+
+// batch of independent matrices laid end to end; matrix ends are implied
+// block boundaries (not flagged), natural split points are flagged.
+__global__ void k_scan_input_batched(int batch, int n, const double* __restrict__ d,
+                                     const double* __restrict__ e, double* __restrict__ dw,
+                                     double* __restrict__ ew, uint8_t* __restrict__ split,
+                                     int* __restrict__ nsplit, int* __restrict__ status) {
+    const long long N = (long long)batch * n;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int cnt = 0;
+    if (i < N) {
+        const int b = (int)(i / n), j = (int)(i - (long long)b * n);
+        const double di = d[i];
+        dw[i] = di;
+        bool bad = !isfinite(di);
+        uint8_t s = 0;
+        double ei = 0.0;
+        if (j + 1 < n) {
+            ei = e[(long long)b * (n - 1) + j];
+            bad |= !isfinite(ei);
+            s = fabs(ei) <= kU * (fabs(di) + fabs(d[i + 1]));
+        }
+        ew[i] = ei;
+        if (bad) set_status(status, BRGPU_ERR_INVALID_ARGUMENT);
+        split[i] = s;
+        cnt = s;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nsplit, cnt);
+}
+
+// block id of position i (bstart ascending, nblk+1 entries)
+__device__ __forceinline__ int find_block(const int* __restrict__ bstart, int nblk, int i) {
+    int lo = 0, hi = nblk;  // last b with bstart[b] <= i
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (bstart[mid] <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// per-block scale = max(1, |d|, |e internal|), computed on dw/ew
+__global__ void k_block_scale(int n, const double* __restrict__ d, const double* __restrict__ e,
+                              const int* __restrict__ bstart, int nblk,
+                              unsigned long long* __restrict__ sbits) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = (i < n && nblk > 1) ? find_block(bstart, nblk, i) : 0;
+    double v = 0.0;
+    if (i < n) {
+        v = fabs(d[i]);
+        if (i + 1 < bstart[b + 1]) v = fmax(v, fabs(e[i]));
+    }
+    unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    if (nblk == 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = y > bits ? y : bits;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(sbits, bits);
+    } else if (i < n) {
+        atomicMax(&sbits[b], bits);
+    }
+}
+
+// in place: dw /= s, ew /= s inside the block, 0 at block boundaries
+__global__ void k_apply_scale(int n, const int* __restrict__ bstart, int nblk,
+                              const unsigned long long* __restrict__ sbits,
+                              double* __restrict__ dw, double* __restrict__ ew) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
+    const double s = fmax(1.0, __longlong_as_double((long long)sbits[b]));
+    dw[i] = dw[i] / s;
+    ew[i] = (i + 1 < bstart[b + 1]) ? ew[i] / s : 0.0;
+}
+
+// Cuppen cuts (merge_tree.cpp:78-92).  With leaf cutoff >= 3 every cut
+// position is strictly interior to its node, so no position is cut twice and
+// the cuts commute: one thread per internal node, bitwise equal to pre-order.
+__global__ void k_cuts(int ncut, const int* __restrict__ cutPos, const double* __restrict__ ew,
+                       double* __restrict__ dw) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ncut) return;
+    const int m = cutPos[t];
+    const double rho = fabs(ew[m]);
+    dw[m] -= rho;
+    dw[m + 1] -= rho;
+}
+
+// ---------------------------------------------------------------------------
+// leaves (qrql.cpp:396-413) and small blocks (qrql.cpp:386-394): one per thread
+// ---------------------------------------------------------------------------
+template <int MAXM>
+__global__ void __launch_bounds__(128) k_leaf(int ntask, const int* __restrict__ tOff,
+                                              const int* __restrict__ tSize,
+                                              const int* __restrict__ tFlags,
+                                              const double* __restrict__ dw,
+                                              const double* __restrict__ ew, double* __restrict__ lam,
+                                              double* __restrict__ blo, double* __restrict__ bhi,
+                                              int* __restrict__ status) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntask) return;
+    const int off = tOff[t], m = tSize[t];
+    const bool values_only = tFlags[t] & 1;
+    double d[MAXM], e[MAXM], r0[MAXM], r1[MAXM];
+    for (int i = 0; i < m; ++i) {
+        d[i] = dw[off + i];
+        e[i] = (i + 1 < m) ? ew[off + i] : 0.0;
+        r0[i] = 0.0;
+        r1[i] = 0.0;
+    }
+    r0[0] = 1.0;
+    r1[m - 1] = 1.0;
+    int st = values_only ? steqr_leaf<false>(m, d, e, r0, r1) : steqr_leaf<true>(m, d, e, r0, r1);
+    if (st) set_status(status, st);
+    // stable ascending sort (qrql.cpp:348-364): rank = #{d_j < d_i} + #{j<i: d_j == d_i}
+    for (int i = 0; i < m; ++i) {
+        const double di = d[i];
+        int rank = 0;
+        for (int j = 0; j < m; ++j) rank += (d[j] < di) || (j < i && d[j] == di);
+        lam[off + rank] = di;
+        if (!values_only) {
+            blo[off + rank] = r0[i];
+            bhi[off + rank] = r1[i];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// level pipeline
+// ---------------------------------------------------------------------------
+__global__ void k_merge_tol(Work w, LevelDev L, int n) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = p < n ? find_merge(L, p) : -1;
+    double v = 0.0;
+    if (m >= 0) {
+        const int off = L.mOff[m], nl = L.mNL[m];
+        const double zv = p < off + nl ? w.bhi[p] : w.blo[p];
+        v = fmax(fabs(w.lam[p]), fabs(zv));
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, m);
+    unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    if (peers == 0xffffffffu) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, bits, o);
+            bits = y > bits ? y : bits;
+        }
+        if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(&L.mTol[m], bits);
+    } else if (m >= 0) {
+        atomicMax(&L.mTol[m], bits);
+    }
+}
+
+// Stable merge of the two sorted children (== std::stable_sort of the
+// concatenation by '<', deflate.cpp:62-66) and z = (sign*bhi_L, blo_R).
+__global__ void k_merge_scatter(Work w, LevelDev L, int n) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int m = find_merge(L, p);
+    if (m < 0) return;
+    const int off = L.mOff[m], nl = L.mNL[m], nr = L.mSize[m] - nl;
+    const double v = w.lam[p];
+    int sp;
+    double z, r0, r1;
+    if (p < off + nl) {
+        sp = p + count_less(w.lam + off + nl, nr, v);
+        const double em = w.ew[off + nl - 1];
+        const double b = w.bhi[p];
+        z = em < 0 ? -b : b;
+        r0 = w.blo[p];
+        r1 = 0.0;
+    } else {
+        sp = (p - nl) + count_leq(w.lam + off, nl, v);
+        z = w.blo[p];
+        r0 = 0.0;
+        r1 = w.bhi[p];
+    }
+    w.D[sp] = v;
+    w.Z[sp] = z;
+    w.R0[sp] = r0;
+    w.R1[sp] = r1;
+}
+
+// non-negligible flags |z| > tol (deflate.cpp:72) + per-tile counts
+__global__ void __launch_bounds__(kScanBlock) k_nn_flag(Work w, LevelDev L, int n, double tol_scale) {
+    const int k = blockIdx.x * kScanBlock + threadIdx.x;
+    int f = 0;
+    if (k < n) {
+        const int m = find_merge(L, k);
+        if (m >= 0) f = fabs(w.Z[k]) > merge_tol(L, m, tol_scale);
+        w.nnFlag[k] = (uint8_t)f;
+    }
+    const int s = block_sum<kScanBlock>(f);
+    if (threadIdx.x == 0) w.tileCnt[blockIdx.x] = s;
+}
+
+// exclusive scan of tile counts (one CTA); total -> *total_dst[*idx_src or 0]
+__global__ void __launch_bounds__(kScanBlock) k_scan_tiles(int* __restrict__ tileCnt,
+                                                           int* __restrict__ tileOff, int ntiles,
+                                                           int* __restrict__ total_dst,
+                                                           const int* __restrict__ idx_src) {
+    int carry = 0;
+    for (int base = 0; base < ntiles; base += kScanBlock) {
+        const int i = base + threadIdx.x;
+        const int v = i < ntiles ? tileCnt[i] : 0;
+        int tot;
+        const int ex = block_exclusive_scan<kScanBlock>(v, tot);
+        if (i < ntiles) tileOff[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) total_dst[idx_src ? *idx_src : 0] = carry;
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_nn_write(Work w, int n) {
+    const int k = blockIdx.x * kScanBlock + threadIdx.x;
+    const int f = k < n ? w.nnFlag[k] : 0;
+    int tot;
+    const int ex = block_exclusive_scan<kScanBlock>(f, tot) + w.tileOff[blockIdx.x];
+    if (k < n) {
+        w.nnPre[k] = ex;
+        if (f) w.nnPos[ex] = k;
+    }
+}
+
+// Close-pole deflation (deflate.cpp:76-95).  A segment is a maximal run of
+// consecutive non-negligible sorted poles whose neighbour gaps are <= tol; its
+// first pole is always a survivor (its gap to any earlier survivor exceeds
+// tol), so segments are independent.  The segment head walks its run with the
+// reference's rule (rotate into the last survivor when |d - d_prev| <= tol),
+// applying each rotation to z and the two selected rows in record order.
+__global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int NN = w.nnPre[n];
+    if (q >= NN) return;
+    const int k = w.nnPos[q];
+    const int m = find_merge(L, k);
+    const int off = L.mOff[m];
+    const int qs = w.nnPre[off], qe = w.nnPre[off + L.mSize[m]];
+    const double tol = merge_tol(L, m, tol_scale);
+    if (q > qs && fabs(w.D[k] - w.D[w.nnPos[q - 1]]) <= tol) return;  // not a head
+    w.survFlag[q] = 1;
+    int prev = k;
+    double dprev_nn = w.D[k];
+    for (int q2 = q + 1; q2 < qe; ++q2) {
+        const int k2 = w.nnPos[q2];
+        const double d2 = w.D[k2];
+        if (fabs(d2 - dprev_nn) > tol) break;  // next segment head
+        dprev_nn = d2;
+        if (fabs(d2 - w.D[prev]) <= tol) {
+            const double zp = w.Z[prev], zq = w.Z[k2];
+            const double r = hyp(zp, zq);
+            const double c = zp / r, s = zq / r;
+            w.Z[prev] = r;
+            w.Z[k2] = 0.0;
+            double xp = w.R0[prev], xq = w.R0[k2];
+            w.R0[prev] = c * xp + s * xq;
+            w.R0[k2] = c * xq - s * xp;
+            xp = w.R1[prev]; xq = w.R1[k2];
+            w.R1[prev] = c * xp + s * xq;
+            w.R1[k2] = c * xq - s * xp;
+            w.survFlag[q2] = 0;
+        } else {
+            w.survFlag[q2] = 1;
+            prev = k2;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kScanBlock) k_surv_count(Work w, int n) {
+    const int q = blockIdx.x * kScanBlock + threadIdx.x;
+    const int NN = w.nnPre[n];
+    const int f = q < NN ? w.survFlag[q] : 0;
+    const int s = block_sum<kScanBlock>(f);
+    if (threadIdx.x == 0) w.tileCnt[blockIdx.x] = s;
+}
+
+// survivor prefix + compacted active problem (deflate.cpp:100-105)
+__global__ void __launch_bounds__(kScanBlock) k_surv_write(Work w, LevelDev L, int n) {
+    const int q = blockIdx.x * kScanBlock + threadIdx.x;
+    const int NN = w.nnPre[n];
+    const int f = q < NN ? w.survFlag[q] : 0;
+    int tot;
+    const int g = block_exclusive_scan<kScanBlock>(f, tot) + w.tileOff[blockIdx.x];
+    if (q < NN) {
+        w.survPre[q] = g;
+        if (f) {
+            const int k = w.nnPos[q];
+            const double z = w.Z[k];
+            w.dA[g] = w.D[k];
+            w.zA[g] = z;
+            w.z2A[g] = z * z;
+            w.r0A[g] = w.R0[k];
+            w.r1A[g] = w.R1[k];
+            w.aMerge[g] = find_merge(L, k);
+        }
+    }
+}
+
+// one secular root per thread (secular.cpp:80-241, tau-relative stop when patched)
+__global__ void __launch_bounds__(128) k_secular(Work w, LevelDev L, int n, int patched) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int T = w.survPre[w.nnPre[n]];
+    int evals = 0;
+    unsigned long long terms = 0;
+    if (g < T) {
+        const int m = w.aMerge[g];
+        int ks, ke;
+        active_range(w, L, m, ks, ke);
+        const int K = ke - ks, j = g - ks;
+        const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+        int o;
+        double t;
+        const int st = solve_root(K, w.dA + ks, w.zA + ks, w.z2A + ks, rho, j, patched != 0, o, t, evals);
+        if (st) set_status(w.status, st);
+        w.org[g] = o;
+        w.tau[g] = t;
+        terms = (unsigned long long)evals * (unsigned long long)K;
+    }
+    evals = __reduce_add_sync(0xffffffffu, evals);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) terms += __shfl_xor_sync(0xffffffffu, terms, o);
+    if ((threadIdx.x & 31) == 0 && evals) {
+        atomicAdd(&w.counters[0], (unsigned long long)evals);
+        atomicAdd(&w.counters[1], terms);
+    }
+}
+
+// Gu-Eisenstat refreshed weights, one pole per thread, roots in order
+// (secular.cpp:288-313); replaces zA in place by sign(z)*sqrt(max(0,-w)).
+__global__ void __launch_bounds__(128) k_zhat(Work w, LevelDev L, int n) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int T = w.survPre[w.nnPre[n]];
+    if (g >= T) return;
+    const int m = w.aMerge[g];
+    if (L.mFlags[m] & kMergeRoot) return;
+    int ks, ke;
+    active_range(w, L, m, ks, ke);
+    const int i = g - ks, K = ke - ks;
+    const double* __restrict__ dA = w.dA + ks;
+    const double di = dA[i];
+    double prod = 1.0;
+    for (int j = 0; j < K; ++j) {
+        const double del = (di - dA[w.org[ks + j]]) - w.tau[ks + j];
+        if (j == i) prod = prod * del;
+        else prod = prod * (del * __drcp_rn(di - dA[j]));
+    }
+    const double mag = sqrt(fmax(0.0, -prod));
+    w.zA[g] = w.zA[g] >= 0.0 ? mag : -mag;
+}
+
+// Parent boundary rows for root j: R_parent(:,j) = R_child y_j with
+// y = zhat/Delta_j / ||zhat/Delta_j|| streamed (never stored),
+// plus placement of lambda_j in the parent's ascending order.
+__global__ void __launch_bounds__(128) k_rows(Work w, LevelDev L, int n) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int T = w.survPre[w.nnPre[n]];
+    if (g >= T) return;
+    const int m = w.aMerge[g];
+    int ks, ke;
+    active_range(w, L, m, ks, ke);
+    const int K = ke - ks, j = g - ks;
+    const int off = L.mOff[m], size = L.mSize[m];
+    const bool is_root = L.mFlags[m] & kMergeRoot;
+    const double* __restrict__ dA = w.dA + ks;
+    const double dorg = dA[w.org[g]];
+    const double tau = w.tau[g];
+    const double lam = dorg + tau;
+    // parent position: j + #{deflated <= lam} = j + #{D <= lam} - #{dA <= lam}
+    const int pos = j + count_leq(w.D + off, size, lam) - count_leq(dA, K, lam);
+    const int p = off + pos;
+    w.lam[p] = lam;
+    if (is_root) return;
+    const double* __restrict__ zh = w.zA + ks;
+    const double* __restrict__ r0 = w.r0A + ks;
+    const double* __restrict__ r1 = w.r1A + ks;
+    double nn = 0.0, s0 = 0.0, s1 = 0.0;
+    bool zero = false;
+#pragma unroll 4
+    for (int i = 0; i < K; ++i) {
+        const double del = (dA[i] - dorg) - tau;
+        zero |= (del == 0.0);
+        const double y = zh[i] * __drcp_rn(del);
+        nn = __fma_rn(y, y, nn);
+        s0 = __fma_rn(r0[i], y, s0);
+        s1 = __fma_rn(r1[i], y, s1);
+    }
+    if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+    const double inv = 1.0 / sqrt(nn);
+    w.blo[p] = s0 * inv;
+    w.bhi[p] = s1 * inv;
+}
+
+// deflated columns: parent position t + #{roots < D}
+__global__ void k_deflated_out(Work w, LevelDev L, int n) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int m = find_merge(L, k);
+    if (m < 0) return;
+    const int q = w.nnPre[k];
+    if (w.nnFlag[k] && w.survFlag[q]) return;  // survivor: placed by k_rows
+    const int off = L.mOff[m];
+    int ks, ke;
+    active_range(w, L, m, ks, ke);
+    const int K = ke - ks;
+    const int t = (k - off) - (w.survPre[q] - ks);
+    const double v = w.D[k];
+    // #{roots j: lambda_j < v}; roots ascend (interlacing)
+    int lo = 0, hi = K;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const double lj = w.dA[ks + w.org[ks + mid]] + w.tau[ks + mid];
+        if (lj < v) lo = mid + 1; else hi = mid;
+    }
+    const int p = off + t + lo;
+    w.lam[p] = v;
+    if (!(L.mFlags[m] & kMergeRoot)) {
+        w.blo[p] = w.R0[k];
+        w.bhi[p] = w.R1[k];
+    }
+}
+
+// per-merge (nn, K) for the trace
+__global__ void k_level_trace(Work w, LevelDev L, int* __restrict__ out) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= L.M) return;
+    const int off = L.mOff[m], end = off + L.mSize[m];
+    const int a = w.nnPre[off], b = w.nnPre[end];
+    out[2 * m] = b - a;
+    out[2 * m + 1] = w.survPre[b] - w.survPre[a];
+}
+
+// ---------------------------------------------------------------------------
+// rescale + cross-block merge
+// ---------------------------------------------------------------------------
+__global__ void k_rescale(int n, const int* __restrict__ bstart, int nblk,
+                          const unsigned long long* __restrict__ sbits, double* __restrict__ lam) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
+    const double s = fmax(1.0, __longlong_as_double((long long)sbits[b]));
+    lam[i] = lam[i] * s;
+}
+
+// one pass of a bottom-up stable merge sort over runs [rs[r], rs[r+1])
+__global__ void k_merge_runs(int n, const double* __restrict__ src, double* __restrict__ dst,
+                             const int* __restrict__ rs, int nruns) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = find_block(rs, nruns, i);
+    const double v = src[i];
+    const int pr = r ^ 1;
+    const int pair0 = rs[r & ~1];
+    if (pr >= nruns) { dst[i] = v; return; }
+    const int ps = rs[pr], pn = rs[pr + 1] - ps;
+    const int own = i - rs[r];
+    const int other = (r & 1) ? count_leq(src + ps, pn, v) : count_less(src + ps, pn, v);
+    dst[pair0 + own + other] = v;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+void launch_copy_input(cudaStream_t s, int n, const double* d, const double* e, double* dw,
+                       double* ew) {
+    k_copy_input<<<cdiv(n, 256), 256, 0, s>>>(n, d, e, dw, ew);
+}
+
+void launch_scan_input(cudaStream_t s, int n, const double* d, const double* e, uint8_t* split,
+                       int* nsplit, int* status) {
+    k_scan_input<<<cdiv(n, 256), 256, 0, s>>>(n, d, e, split, nsplit, status);
+}
+
+void launch_scan_input_batched(cudaStream_t s, int batch, int n, const double* d, const double* e,
+                               double* dw, double* ew, uint8_t* split, int* nsplit, int* status) {
+    const int N = batch * n;
+    k_scan_input_batched<<<cdiv(N, 256), 256, 0, s>>>(batch, n, d, e, dw, ew, split, nsplit, status);
+}
+
+void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned long long* sbits,
+                    double* dw, double* ew, int ncut, const int* cutPos, int* launches) {
+    k_block_scale<<<cdiv(n, 256), 256, 0, s>>>(n, dw, ew, bstart, nblk, sbits);
+    k_apply_scale<<<cdiv(n, 256), 256, 0, s>>>(n, bstart, nblk, sbits, dw, ew);
+    *launches += 2;
+    if (ncut > 0) {
+        k_cuts<<<cdiv(ncut, 256), 256, 0, s>>>(ncut, cutPos, ew, dw);
+        *launches += 1;
+    }
+}
+
+void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const int* tSize,
+                   const int* tFlags, const Work& w, int* launches) {
+    if (ntask <= 0) return;
+    if (maxm <= 32)
+        k_leaf<32><<<cdiv(ntask, 128), 128, 0, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+                                                   w.blo, w.bhi, w.status);
+    else
+        k_leaf<64><<<cdiv(ntask, 128), 128, 0, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+                                                   w.blo, w.bhi, w.status);
+    *launches += 1;
+}
+
+void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
+                  const SolveParams& prm, int* launches) {
+    const int ntiles = cdiv(n, kScanBlock);
+    cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
+    k_merge_tol<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    k_merge_scatter<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    k_nn_flag<<<ntiles, kScanBlock, 0, s>>>(w, L, n, prm.tol_scale);
+    k_scan_tiles<<<1, kScanBlock, 0, s>>>(w.tileCnt, w.tileOff, ntiles, w.nnPre + n, nullptr);
+    k_nn_write<<<ntiles, kScanBlock, 0, s>>>(w, n);
+    k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
+    k_surv_count<<<ntiles, kScanBlock, 0, s>>>(w, n);
+    k_scan_tiles<<<1, kScanBlock, 0, s>>>(w.tileCnt, w.tileOff, ntiles, w.survPre, w.nnPre + n);
+    k_surv_write<<<ntiles, kScanBlock, 0, s>>>(w, L, n);
+    k_secular<<<cdiv(n, 128), 128, 0, s>>>(w, L, n, prm.patched);
+    int nl = 10;
+    if (prm.zhat) {
+        k_zhat<<<cdiv(n, 128), 128, 0, s>>>(w, L, n);
+        ++nl;
+    }
+    k_rows<<<cdiv(n, 128), 128, 0, s>>>(w, L, n);
+    k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    *launches += nl + 2;
+}
+
+void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
+                        int* launches) {
+    (void)n;
+    k_level_trace<<<cdiv(L.M, 128), 128, 0, s>>>(w, L, out);
+    *launches += 1;
+}
+
+void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
+                   const unsigned long long* sbits, double* lam, int* launches) {
+    k_rescale<<<cdiv(n, 256), 256, 0, s>>>(n, bstart, nblk, sbits, lam);
+    *launches += 1;
+}
+
+void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
+                       int nruns, int* launches) {
+    k_merge_runs<<<cdiv(n, 256), 256, 0, s>>>(n, src, dst, rs, nruns);
+    *launches += 1;
+}
+
+}  // namespace brgpu
