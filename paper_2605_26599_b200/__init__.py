@@ -269,6 +269,25 @@ class Solver:
         self._lib.brgpu_get_ledger(self._h, C.byref(l))
         return LedgerSnapshot(*(getattr(l, f) for f, _ in _native.Ledger._fields_))
 
+    def timing(self) -> dict:
+        """CUDA-event device time of the last solve (ms), on the handle's stream."""
+        t = _native.Timing()
+        self._lib.brgpu_get_timing(self._h, C.byref(t))
+        return {"device_ms": t.device_ms, "pre_ms": t.pre_ms, "main_ms": t.main_ms}
+
+    def profile_kernels(self, d, e) -> dict:
+        """Kernel-by-kernel profile of one solve of device-resident torch tensors:
+        {class: (total_ms, launches)} from CUDA events on the handle's stream."""
+        n = d.numel()
+        ms = (C.c_double * _native.NCLASS)()
+        cnt = (C.c_int32 * _native.NCLASS)()
+        rc = self._lib.brgpu_profile_kernels(self._h, n, d.data_ptr(), e.data_ptr() if n > 1 else None,
+                                             ms, cnt)
+        if rc:
+            self._fail(rc)
+        return {self._lib.brgpu_kernel_class_name(c).decode(): (ms[c], cnt[c])
+                for c in range(_native.NCLASS) if cnt[c]}
+
     def set_trace(self, on: bool) -> None:
         self._lib.brgpu_set_trace(self._h, int(on))
 

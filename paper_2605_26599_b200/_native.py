@@ -42,8 +42,14 @@ EXPORTS = [
     "brgpu_set_option", "brgpu_get_option", "brgpu_workspace_query", "brgpu_reserve",
     "brgpu_get_ledger", "brgpu_eigvals", "brgpu_eigvals_device", "brgpu_eigvals_batched",
     "brgpu_eigvals_batched_device", "brgpu_get_stats", "brgpu_set_trace", "brgpu_get_trace",
-    "brgpu_version",
+    "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_kernel_class_name", "brgpu_version",
 ]
+
+NCLASS = 17
+
+
+class Timing(C.Structure):
+    _fields_ = [("device_ms", C.c_double), ("pre_ms", C.c_double), ("main_ms", C.c_double)]
 
 _lib = None
 
@@ -75,5 +81,10 @@ def lib() -> C.CDLL:
     L.brgpu_set_trace.argtypes = [hp, C.c_int]
     L.brgpu_get_trace.argtypes = [hp, C.POINTER(Trace), C.c_int64, C.POINTER(C.c_int64)]
     L.brgpu_version.restype = C.c_char_p
+    L.brgpu_get_timing.argtypes = [hp, C.POINTER(Timing)]
+    L.brgpu_profile_kernels.argtypes = [hp, C.c_int64, _dp, _dp, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_int32)]
+    L.brgpu_kernel_class_name.argtypes = [C.c_int]
+    L.brgpu_kernel_class_name.restype = C.c_char_p
     _lib = L
     return L

@@ -78,6 +78,19 @@ def build_product(force: bool = False) -> Path:
     return LIB
 
 
+PROBE = PKG / "libbrprobe.so"
+
+
+def build_probe(force: bool = False) -> Path:
+    """FP64 peak microbenchmark (tooling for the roofline denominator)."""
+    BUILD.mkdir(exist_ok=True)
+    s = CSRC / "probe_fp64.cu"
+    if force or _stale(PROBE, [s]):
+        _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
+              "-shared", str(s), "-o", str(PROBE), "-cudart", "static"])
+    return PROBE
+
+
 def build_oracle() -> None:
     """Test-only checkers: oracle/build/libbro.so and (where /root/reference
     exists) oracle/_ref/libbrref.so.  Never linked into the product."""
@@ -90,6 +103,7 @@ def main() -> None:
     ap.add_argument("--force", action="store_true")
     a = ap.parse_args()
     print(build_product(force=a.force))
+    build_probe(force=a.force)
     if not a.product:
         build_oracle()
 

@@ -30,17 +30,30 @@ void launch_scan_input_batched(cudaStream_t s, int batch, int n, const double* d
                                double* dw, double* ew, uint8_t* split, int* nsplit, int* status);
 void launch_copy_input(cudaStream_t s, int n, const double* d, const double* e, double* dw, double* ew);
 void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned long long* sbits,
-                    double* dw, double* ew, int ncut, const int* cutPos, int* launches);
+                    double* dw, double* ew, int ncut, const int* cutPos, int* launches, Prof* prof);
 void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const int* tSize,
-                   const int* tFlags, const Work& w, int* launches);
+                   const int* tFlags, const Work& w, int* launches, Prof* prof);
 void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
-                  int* launches);
+                  int* launches, Prof* prof);
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
-                        int* launches);
+                        int* launches, Prof* prof);
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
-                   const unsigned long long* sbits, double* lam, int* launches);
+                   const unsigned long long* sbits, double* lam, int* launches, Prof* prof);
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
-                       int nruns, int* launches);
+                       int nruns, int* launches, Prof* prof);
+
+struct Prof {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls;
+};
+
+void prof_mark(Prof* p, void* stream, int cls) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, (cudaStream_t)stream);
+    p->ev.push_back(e);
+    p->cls.push_back(cls);
+}
 
 }  // namespace brgpu
 
@@ -118,6 +131,9 @@ struct Handle {
     int64_t ledger_doubles = 0, ledger_ints = 0, peak_doubles = 0, peak_ints = 0, limit_n = 0;
     // plan cache
     std::unique_ptr<Plan> plan;
+    cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+    brgpu_timing timing{};
+    Prof* prof = nullptr;
     uint64_t bufgen = 1;  // bumped whenever a buffer baked into a graph moves
     brgpu_stats stats{};
     std::vector<brgpu_trace> traceRecs;
@@ -353,14 +369,15 @@ int status_message(Handle* h, int st) {
     }
 }
 
-int run_plan(Handle* h, Plan* p, int* launches) {
+int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
     cudaStream_t s = h->stream;
+    if (prof) prof_mark(prof, (void*)s, -1);
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
     launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
-                   p->d_cut, launches);
+                   p->d_cut, launches, prof);
     launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
-                  launches);
+                  launches, prof);
     SolveParams prm{n, h->zhat, h->patched, h->tol_scale};
     for (const LevelHost& lh : p->levels) {
         LevelDev L;
@@ -371,15 +388,16 @@ int run_plan(Handle* h, Plan* p, int* launches) {
         L.mTol = h->mTol;
         L.tileFirst = p->d_tileFirst + lh.tile0;
         L.M = lh.M;
-        launch_level(s, h->w, L, n, prm, launches);
-        if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches);
+        launch_level(s, h->w, L, n, prm, launches, prof);
+        if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
     }
-    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches);
+    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
     // cross-block merge passes (ping-pong lam <-> D), result back in lam
     double* src = h->w.lam;
     double* dst = h->w.D;
     for (size_t q = 0; q < p->runPasses.size(); ++q) {
-        launch_merge_runs(s, n, src, dst, p->d_runs[q], (int)p->runPasses[q].size() - 1, launches);
+        launch_merge_runs(s, n, src, dst, p->d_runs[q], (int)p->runPasses[q].size() - 1, launches,
+                          prof);
         std::swap(src, dst);
     }
     if (src != h->w.lam) {
@@ -427,7 +445,8 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 4, s));
     int launches = 0;
-    const bool want_graph = h->use_graph != 0;
+    const bool want_graph = h->use_graph != 0 && h->prof == nullptr;
+    CUDA_TRY(h, cudaEventRecord(h->tev[2], s));
     if (want_graph) {
         if (!p->graph || p->graph_trace != (h->trace != 0) || p->graph_gen != h->bufgen) {
             if (p->graph) { cudaGraphExecDestroy(p->graph); p->graph = nullptr; }
@@ -447,10 +466,11 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
         CUDA_TRY(h, cudaGraphLaunch(p->graph, s));
         h->stats.graph_replayed = 1;
     } else {
-        int r = run_plan(h, p, &launches);
+        int r = run_plan(h, p, &launches, h->prof);
         if (r) return r;
         h->stats.graph_replayed = 0;
     }
+    CUDA_TRY(h, cudaEventRecord(h->tev[3], s));
     CUDA_TRY(h, cudaGetLastError());
     h->stats.kernel_launches = launches + 2;  // + input copy and scan
     h->stats.n = n;
@@ -465,6 +485,14 @@ int finish_solve(Handle* h) {
     CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
+    {
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, h->tev[0], h->tev[1]);
+        cudaEventElapsedTime(&b, h->tev[2], h->tev[3]);
+        h->timing.pre_ms = a;
+        h->timing.main_ms = b;
+        h->timing.device_ms = (double)a + (double)b;
+    }
     h->stats.evals = (int64_t)h->hcnt[0];
     h->stats.pole_terms = (double)h->hcnt[1];
     if (h->trace && h->plan) {
@@ -503,8 +531,10 @@ int solve_device(Handle* h, int64_t n64, const double* d, const double* e, doubl
     cudaStream_t s = h->stream;
     CUDA_TRY(h, cudaMemsetAsync(h->dsmall, 0, sizeof(int) * 2, s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.status, 0, sizeof(int), s));
+    CUDA_TRY(h, cudaEventRecord(h->tev[0], s));
     launch_copy_input(s, n, d, e, h->w.dw, h->w.ew);
     launch_scan_input(s, n, h->w.dw, h->w.ew, h->split, h->dsmall, h->w.status);
+    CUDA_TRY(h, cudaEventRecord(h->tev[1], s));
     int r = solve_prepared(h, n, {0, n});
     if (r) return r;
     if (w_host)
@@ -559,7 +589,9 @@ int brgpu_create(brgpu_handle** out, int device) {
         cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&h->hsmall, sizeof(int) * 4) != cudaSuccess ||
         cudaMallocHost(&h->hcnt, sizeof(unsigned long long) * 4) != cudaSuccess ||
-        cudaMalloc(&h->dsmall, sizeof(int) * 4) != cudaSuccess) {
+        cudaMalloc(&h->dsmall, sizeof(int) * 4) != cudaSuccess ||
+        cudaEventCreate(&h->tev[0]) != cudaSuccess || cudaEventCreate(&h->tev[1]) != cudaSuccess ||
+        cudaEventCreate(&h->tev[2]) != cudaSuccess || cudaEventCreate(&h->tev[3]) != cudaSuccess) {
         delete hh;
         return BRGPU_ERR_CUDA;
     }
@@ -582,6 +614,7 @@ int brgpu_destroy(brgpu_handle* hh) {
     if (h->hsmall) cudaFreeHost(h->hsmall);
     if (h->hcnt) cudaFreeHost(h->hcnt);
     if (h->dsmall) cudaFree(h->dsmall);
+    for (auto& e : h->tev) if (e) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete hh;
     return BRGPU_OK;
@@ -692,7 +725,9 @@ int brgpu_eigvals_batched_device(brgpu_handle* hh, int64_t batch, int64_t n, con
     cudaStream_t s = h->stream;
     CUDA_TRY(h, cudaMemsetAsync(h->dsmall, 0, sizeof(int) * 2, s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.status, 0, sizeof(int), s));
+    CUDA_TRY(h, cudaEventRecord(h->tev[0], s));
     launch_scan_input_batched(s, (int)batch, (int)n, d, e, h->w.dw, h->w.ew, h->split, h->dsmall, h->w.status);
+    CUDA_TRY(h, cudaEventRecord(h->tev[1], s));
     std::vector<int> segs;
     for (int64_t b = 0; b <= batch; ++b) segs.push_back((int)(b * n));
     int r = solve_prepared(h, (int)N, segs);
@@ -723,6 +758,43 @@ int brgpu_get_stats(const brgpu_handle* hh, brgpu_stats* out) {
     if (!hh || !out) return BRGPU_ERR_INVALID_ARGUMENT;
     *out = hh->h.stats;
     return BRGPU_OK;
+}
+
+int brgpu_get_timing(const brgpu_handle* hh, brgpu_timing* out) {
+    if (!hh || !out) return BRGPU_ERR_INVALID_ARGUMENT;
+    *out = hh->h.timing;
+    return BRGPU_OK;
+}
+
+const char* brgpu_kernel_class_name(int c) {
+    static const char* names[BRGPU_NCLASS] = {
+        "prepare(scale+cuts)", "leaf", "merge_tol", "merge_scatter", "nn_flag", "scan_tiles",
+        "nn_write", "segment_walk", "surv_count", "surv_write", "secular", "zhat", "rows",
+        "deflated_out", "trace", "finish", "subtree"};
+    return (c >= 0 && c < BRGPU_NCLASS) ? names[c] : "?";
+}
+
+int brgpu_profile_kernels(brgpu_handle* hh, int64_t n, const double* d, const double* e,
+                          double* class_ms, int32_t* class_launches) {
+    if (!hh || !class_ms || !class_launches) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    Prof prof;
+    h->prof = &prof;
+    const int r = solve_device(h, n, d, e, h->w.lam, false);
+    h->prof = nullptr;
+    for (int c = 0; c < BRGPU_NCLASS; ++c) { class_ms[c] = 0.0; class_launches[c] = 0; }
+    if (r == BRGPU_OK) {
+        cudaStreamSynchronize(h->stream);
+        for (size_t i = 1; i < prof.ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, prof.ev[i - 1], prof.ev[i]);
+            const int c = prof.cls[i];
+            if (c >= 0 && c < BRGPU_NCLASS) { class_ms[c] += ms; class_launches[c] += 1; }
+        }
+    }
+    for (auto e2 : prof.ev) cudaEventDestroy(e2);
+    return r;
 }
 
 int brgpu_set_trace(brgpu_handle* hh, int enable) {

@@ -65,6 +65,11 @@ struct LevelDev {
     int M;
 };
 
+// Optional per-kernel profiling (brgpu_profile_kernels): the launchers call
+// prof_mark after every launch; api.cpp records a CUDA event per mark.
+struct Prof;
+void prof_mark(Prof* p, void* stream, int cls);
+
 struct SolveParams {
     int n;
     int zhat;

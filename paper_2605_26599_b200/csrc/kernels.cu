@@ -633,8 +633,10 @@ void launch_scan_input_batched(cudaStream_t s, int batch, int n, const double* d
     k_scan_input_batched<<<cdiv(N, 256), 256, 0, s>>>(batch, n, d, e, dw, ew, split, nsplit, status);
 }
 
+#define PMARK(c) do { if (prof) prof_mark(prof, (void*)s, (c)); } while (0)
+
 void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned long long* sbits,
-                    double* dw, double* ew, int ncut, const int* cutPos, int* launches) {
+                    double* dw, double* ew, int ncut, const int* cutPos, int* launches, Prof* prof) {
     k_block_scale<<<cdiv(n, 256), 256, 0, s>>>(n, dw, ew, bstart, nblk, sbits);
     k_apply_scale<<<cdiv(n, 256), 256, 0, s>>>(n, bstart, nblk, sbits, dw, ew);
     *launches += 2;
@@ -642,10 +644,11 @@ void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned
         k_cuts<<<cdiv(ncut, 256), 256, 0, s>>>(ncut, cutPos, ew, dw);
         *launches += 1;
     }
+    PMARK(BRGPU_K_PREPARE);
 }
 
 void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const int* tSize,
-                   const int* tFlags, const Work& w, int* launches) {
+                   const int* tFlags, const Work& w, int* launches, Prof* prof) {
     if (ntask <= 0) return;
     if (maxm <= 32)
         k_leaf<32><<<cdiv(ntask, 128), 128, 0, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
@@ -654,49 +657,66 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
         k_leaf<64><<<cdiv(ntask, 128), 128, 0, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                    w.blo, w.bhi, w.status);
     *launches += 1;
+    PMARK(BRGPU_K_LEAF);
 }
 
 void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
-                  const SolveParams& prm, int* launches) {
+                  const SolveParams& prm, int* launches, Prof* prof) {
     const int ntiles = cdiv(n, kScanBlock);
     cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
     k_merge_tol<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    PMARK(BRGPU_K_TOL);
     k_merge_scatter<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    PMARK(BRGPU_K_SCATTER);
     k_nn_flag<<<ntiles, kScanBlock, 0, s>>>(w, L, n, prm.tol_scale);
+    PMARK(BRGPU_K_NNFLAG);
     k_scan_tiles<<<1, kScanBlock, 0, s>>>(w.tileCnt, w.tileOff, ntiles, w.nnPre + n, nullptr);
+    PMARK(BRGPU_K_SCAN);
     k_nn_write<<<ntiles, kScanBlock, 0, s>>>(w, n);
+    PMARK(BRGPU_K_NNWRITE);
     k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
+    PMARK(BRGPU_K_WALK);
     k_surv_count<<<ntiles, kScanBlock, 0, s>>>(w, n);
+    PMARK(BRGPU_K_SURVCOUNT);
     k_scan_tiles<<<1, kScanBlock, 0, s>>>(w.tileCnt, w.tileOff, ntiles, w.survPre, w.nnPre + n);
+    PMARK(BRGPU_K_SCAN);
     k_surv_write<<<ntiles, kScanBlock, 0, s>>>(w, L, n);
+    PMARK(BRGPU_K_SURVWRITE);
     k_secular<<<cdiv(n, 128), 128, 0, s>>>(w, L, n, prm.patched);
+    PMARK(BRGPU_K_SECULAR);
     int nl = 10;
     if (prm.zhat) {
         k_zhat<<<cdiv(n, 128), 128, 0, s>>>(w, L, n);
+        PMARK(BRGPU_K_ZHAT);
         ++nl;
     }
     k_rows<<<cdiv(n, 128), 128, 0, s>>>(w, L, n);
+    PMARK(BRGPU_K_ROWS);
     k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    PMARK(BRGPU_K_DEFLATED);
     *launches += nl + 2;
 }
 
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
-                        int* launches) {
+                        int* launches, Prof* prof) {
     (void)n;
     k_level_trace<<<cdiv(L.M, 128), 128, 0, s>>>(w, L, out);
     *launches += 1;
+    PMARK(BRGPU_K_TRACE);
 }
 
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
-                   const unsigned long long* sbits, double* lam, int* launches) {
+                   const unsigned long long* sbits, double* lam, int* launches, Prof* prof) {
     k_rescale<<<cdiv(n, 256), 256, 0, s>>>(n, bstart, nblk, sbits, lam);
     *launches += 1;
+    PMARK(BRGPU_K_FINISH);
 }
 
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
-                       int nruns, int* launches) {
+                       int nruns, int* launches, Prof* prof) {
     k_merge_runs<<<cdiv(n, 256), 256, 0, s>>>(n, src, dst, rs, nruns);
     *launches += 1;
+    PMARK(BRGPU_K_FINISH);
 }
 
 }  // namespace brgpu
