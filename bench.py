@@ -47,8 +47,12 @@ CONFIGS = {
                workload="random symmetric tridiagonal n=2^20, d,e~U(-1,1) (config 5)"),
 }
 
-# FP64 pipe operations per algorithmic unit (verified in SASS):
-OPS_PER_TERM = {"secular": 13, "zhat": 10, "rows": 11}
+# FP64 pipe operations per algorithmic unit (verified in SASS of this
+# build): secular pole term 2 DADD (delta) + 5 DFMA (reciprocal) + 2 DMUL + 3 DADD
+# (sum, |sum|, derivative; psi' is a prefix snapshot of the derivative sum, no add) = 12;
+# refreshed-weight term 3 DADD + 5 DFMA + 2 DMUL = 10; boundary-row term 2 DADD + 5 DFMA
+# + 1 DMUL + 3 DFMA = 11.
+OPS_PER_TERM = {"secular": 12, "zhat": 10, "rows": 11}
 # algorithmic bytes per element per level of the memory-bound classes
 BYTES_PER_ELEM = {"merge_tol": 16, "merge_scatter": 56, "nn_flag": 9, "nn_write": 5,
                   "deflated_out": 53, "segment_walk": 0, "surv_count": 1, "surv_write": 0}

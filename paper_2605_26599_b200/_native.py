@@ -6,9 +6,11 @@ calls raise.  The library is built in-tree by ``paper_2605_26599_b200.build``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libbrgpu.so"
+# BRGPU_LIB overrides the in-tree library (used for A/B builds in experiments).
+LIB_PATH = Path(os.environ.get("BRGPU_LIB", Path(__file__).resolve().parent / "libbrgpu.so"))
 
 _dp = C.c_void_p
 
@@ -42,7 +44,8 @@ EXPORTS = [
     "brgpu_set_option", "brgpu_get_option", "brgpu_workspace_query", "brgpu_reserve",
     "brgpu_get_ledger", "brgpu_eigvals", "brgpu_eigvals_device", "brgpu_eigvals_batched",
     "brgpu_eigvals_batched_device", "brgpu_get_stats", "brgpu_set_trace", "brgpu_get_trace",
-    "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_kernel_class_name", "brgpu_version",
+    "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_kernel_class_name", "brgpu_selftest_rcp",
+    "brgpu_version",
 ]
 
 NCLASS = 17
@@ -86,5 +89,6 @@ def lib() -> C.CDLL:
                                         C.POINTER(C.c_int32)]
     L.brgpu_kernel_class_name.argtypes = [C.c_int]
     L.brgpu_kernel_class_name.restype = C.c_char_p
+    L.brgpu_selftest_rcp.argtypes = [hp, C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]
     _lib = L
     return L

@@ -29,9 +29,10 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-    "--expt-relaxed-constexpr",
+    "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}",
 ]
-CXX_FLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", f"-I{CUDA_HOME / 'include'}"]
+CXX_FLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", f"-I{CUDA_HOME / 'include'}",
+             f"-I{ROOT / 'include'}"]
 
 CU_SOURCES = ["kernels.cu", "subtree.cu"]
 CPP_SOURCES = ["api.cpp"]

@@ -42,6 +42,9 @@ void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
                        int nruns, int* launches, Prof* prof);
 
+void init_kernel_attributes();
+int selftest_rcp(long long count, unsigned long long seed, unsigned long long* host_bad);
+
 struct Prof {
     std::vector<cudaEvent_t> ev;
     std::vector<int> cls;
@@ -100,6 +103,8 @@ struct Plan {
 
 struct Handle {
     int device = 0;
+    int sms = 148;
+    int sec_grid = 148 * 8;
     cudaStream_t stream = nullptr;
     int leaf_cutoff = 25;
     int zhat = 1;
@@ -378,7 +383,7 @@ int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
                    p->d_cut, launches, prof);
     launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
                   launches, prof);
-    SolveParams prm{n, h->zhat, h->patched, h->tol_scale};
+    SolveParams prm{n, h->zhat, h->patched, h->tol_scale, h->sec_grid};
     for (const LevelHost& lh : p->levels) {
         LevelDev L;
         L.mOff = p->d_mOff + lh.m0;
@@ -595,6 +600,9 @@ int brgpu_create(brgpu_handle** out, int device) {
         delete hh;
         return BRGPU_ERR_CUDA;
     }
+    brgpu::init_kernel_attributes();
+    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    h->sec_grid = h->sms * 6;
     *out = hh;
     return BRGPU_OK;
 }
@@ -794,6 +802,15 @@ int brgpu_profile_kernels(brgpu_handle* hh, int64_t n, const double* d, const do
         }
     }
     for (auto e2 : prof.ev) cudaEventDestroy(e2);
+    return r;
+}
+
+int brgpu_selftest_rcp(brgpu_handle* hh, int64_t count, uint64_t seed, uint64_t* mismatches) {
+    if (!hh || !mismatches || count <= 0) return BRGPU_ERR_INVALID_ARGUMENT;
+    cudaSetDevice(hh->h.device);
+    unsigned long long bad = 0;
+    const int r = brgpu::selftest_rcp(count, seed, &bad);
+    *mismatches = bad;
     return r;
 }
 

@@ -4,7 +4,7 @@
 
 #include <cstdint>
 
-#include "../../include/brgpu.h"
+#include "brgpu.h"
 
 #ifndef __CUDACC__
 #ifndef __host__
@@ -75,6 +75,7 @@ struct SolveParams {
     int zhat;
     int patched;
     double tol_scale;
+    int sec_grid;  // CTAs of the secular kernel (fills the GPU; chunks adapt to the root count)
 };
 
 }  // namespace brgpu

@@ -244,19 +244,31 @@ __global__ void k_cuts(int ncut, const int* __restrict__ cutPos, const double* _
 // ---------------------------------------------------------------------------
 // leaves (qrql.cpp:396-413) and small blocks (qrql.cpp:386-394): one per thread
 // ---------------------------------------------------------------------------
+// Per-thread arrays live in shared memory ([i][thread] layout): a leaf's QL
+// sweeps are a serial chain of dependent loads/stores, so they must hit SMEM
+// latency, not L1-thrashing local memory (4 x MAXM doubles per thread).
+constexpr int kLeafThreads = 64;
+
 template <int MAXM>
-__global__ void __launch_bounds__(128) k_leaf(int ntask, const int* __restrict__ tOff,
-                                              const int* __restrict__ tSize,
-                                              const int* __restrict__ tFlags,
-                                              const double* __restrict__ dw,
-                                              const double* __restrict__ ew, double* __restrict__ lam,
-                                              double* __restrict__ blo, double* __restrict__ bhi,
-                                              int* __restrict__ status) {
+__global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __restrict__ tOff,
+                                                       const int* __restrict__ tSize,
+                                                       const int* __restrict__ tFlags,
+                                                       const double* __restrict__ dw,
+                                                       const double* __restrict__ ew,
+                                                       double* __restrict__ lam,
+                                                       double* __restrict__ blo,
+                                                       double* __restrict__ bhi,
+                                                       int* __restrict__ status) {
+    extern __shared__ double leaf_sm[];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntask) return;
     const int off = tOff[t], m = tSize[t];
     const bool values_only = tFlags[t] & 1;
-    double d[MAXM], e[MAXM], r0[MAXM], r1[MAXM];
+    constexpr int S = kLeafThreads;
+    const Strided<S> d{leaf_sm + threadIdx.x};
+    const Strided<S> e{leaf_sm + MAXM * S + threadIdx.x};
+    const Strided<S> r0{leaf_sm + 2 * MAXM * S + threadIdx.x};
+    const Strided<S> r1{leaf_sm + 3 * MAXM * S + threadIdx.x};
     for (int i = 0; i < m; ++i) {
         d[i] = dw[off + i];
         e[i] = (i + 1 < m) ? ew[off + i] : 0.0;
@@ -265,7 +277,7 @@ __global__ void __launch_bounds__(128) k_leaf(int ntask, const int* __restrict__
     }
     r0[0] = 1.0;
     r1[m - 1] = 1.0;
-    int st = values_only ? steqr_leaf<false>(m, d, e, r0, r1) : steqr_leaf<true>(m, d, e, r0, r1);
+    const int st = values_only ? steqr_leaf<false>(m, d, e, r0, r1) : steqr_leaf<true>(m, d, e, r0, r1);
     if (st) set_status(status, st);
     // stable ascending sort (qrql.cpp:348-364): rank = #{d_j < d_i} + #{j<i: d_j == d_i}
     for (int i = 0; i < m; ++i) {
@@ -451,25 +463,175 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_write(Work w, LevelDev L, i
     }
 }
 
-// one secular root per thread (secular.cpp:80-241, tau-relative stop when patched)
-__global__ void __launch_bounds__(128) k_secular(Work w, LevelDev L, int n, int patched) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+// Roots of a CTA are a contiguous range of level-global active indices; the
+// poles they need are the union of their merges' active ranges, itself a
+// contiguous window [P0, P1).  Windows up to kWin entries are staged in shared
+// memory (broadcast reads in the pole loop); larger ones read global memory.
+constexpr int kSecBlock = 128;
+constexpr int kWin = 1024;
+
+struct Window {
+    int P0, P1;
+    bool fits;
+};
+
+__device__ __forceinline__ Window range_window(const Work& w, const LevelDev& L, int c0, int c1,
+                                               int cap) {
+    int a, b, c, d;
+    active_range(w, L, w.aMerge[c0], a, b);
+    active_range(w, L, w.aMerge[c1 - 1], c, d);
+    Window win;
+    win.P0 = a;
+    win.P1 = d;
+    win.fits = (d - a) <= cap;
+    return win;
+}
+
+__device__ __forceinline__ Window cta_window(const Work& w, const LevelDev& L, int T) {
+    const int g0 = blockIdx.x * kSecBlock;
+    return range_window(w, L, g0, min(g0 + kSecBlock, T), kWin);
+}
+
+// Secular roots (secular.cpp:80-241, tau-relative stop when patched).
+// A CTA owns a chunk of roots; each lane runs one root's iteration as a
+// resumable state machine (RootSM) and pulls the next root from a CTA queue
+// as soon as its root converges.  Every evaluation is one warp-uniform loop
+// over the poles (shared-memory broadcast reads), so lanes never wait on
+// a neighbour's slower root and the pole loop has no divergence.
+constexpr int kSecWinQ = 2048;
+
+// One evaluation pass for one lane: f, f', rho*sum|t|, psi' at (dorg, tau) over
+// K poles in pole order (secular.cpp:26-52).  P yields (d_i, z_i^2) pairs.
+// psi' = sum_{i<=j} dt_i is the prefix of the same sequential sum, so it is
+// snapshotted instead of accumulated separately (bitwise identical).
+// Returns false if some |delta| left the fast reciprocal's domain (incl. a
+// pole, delta == 0); the caller then redoes the pass exactly.
+template <typename P>
+__device__ __forceinline__ bool eval_pass(const P& pairs, int K, int jsplit, double dorg, double tau,
+                                          double& sum, double& sum_abs, double& sum_d, double& psi) {
+    sum = 0.0; sum_abs = 0.0; sum_d = 0.0; psi = 0.0;
+    unsigned minexp = 0x7ff00000u;
+#pragma unroll 4
+    for (int i = 0; i < K; ++i) {
+        const double2 dz = pairs(i);
+        const double del = (dz.x - dorg) - tau;
+        minexp = min(minexp, expfield(del));
+        const double r = rcp_nr(del);
+        const double t = dz.y * r;
+        sum += t;
+        sum_abs += fabs(t);
+        sum_d += t * r;
+        if (i == jsplit) psi = sum_d;
+    }
+    if (jsplit >= K) psi = sum_d;
+    return minexp >= kRcpMinExp && minexp != 0x7ff00000u;
+}
+
+// Exact (slow) pass with __drcp_rn and explicit pole detection.
+template <typename P>
+__device__ __noinline__ bool eval_pass_exact(const P& pairs, int K, int jsplit, double dorg, double tau,
+                                             double& sum, double& sum_abs, double& sum_d, double& psi) {
+    sum = 0.0; sum_abs = 0.0; sum_d = 0.0; psi = 0.0;
+    bool pole = false;
+    for (int i = 0; i < K; ++i) {
+        const double2 dz = pairs(i);
+        const double del = (dz.x - dorg) - tau;
+        pole |= (del == 0.0);
+        const double r = __drcp_rn(del);
+        const double t = dz.y * r;
+        sum += t;
+        sum_abs += fabs(t);
+        const double dt = t * r;
+        sum_d += dt;
+        if (i <= jsplit) psi += dt;
+    }
+    return pole;
+}
+
+struct SmemPairs {
+    const double2* p;
+    __device__ __forceinline__ double2 operator()(int i) const { return p[i]; }
+};
+struct GlobalPairs {
+    const double* d;
+    const double* z2;
+    __device__ __forceinline__ double2 operator()(int i) const { return make_double2(d[i], z2[i]); }
+};
+
+// Secular roots (secular.cpp:80-241, tau-relative stop when patched).
+// A CTA owns a chunk of roots; each lane runs one root's iteration as a
+// resumable state machine (RootSM) and pulls the next root from a CTA queue
+// as soon as its root converges.  Evaluations are branch-free pole loops over
+// shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
+__global__ void __launch_bounds__(kSecBlock) k_secular(Work w, LevelDev L, int n, int patched) {
+    __shared__ double2 s_dz[kSecWinQ];
+    __shared__ int s_next;
     const int T = w.survPre[w.nnPre[n]];
+    const int R = max(kSecBlock, (T + (int)gridDim.x - 1) / (int)gridDim.x);
+    const int c0 = blockIdx.x * R;
+    if (c0 >= T) return;  // uniform per CTA
+    const int c1 = min(c0 + R, T);
+    const Window win = range_window(w, L, c0, c1, kSecWinQ);
+    if (win.fits) {
+        for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock)
+            s_dz[i] = make_double2(w.dA[win.P0 + i], w.z2A[win.P0 + i]);
+    }
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+
+    RootSM st;
+    int g = -1, ks = 0;
+    bool exhausted = false;
     int evals = 0;
     unsigned long long terms = 0;
-    if (g < T) {
-        const int m = w.aMerge[g];
-        int ks, ke;
-        active_range(w, L, m, ks, ke);
-        const int K = ke - ks, j = g - ks;
-        const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
-        int o;
-        double t;
-        const int st = solve_root(K, w.dA + ks, w.zA + ks, w.z2A + ks, rho, j, patched != 0, o, t, evals);
-        if (st) set_status(w.status, st);
-        w.org[g] = o;
-        w.tau[g] = t;
-        terms = (unsigned long long)evals * (unsigned long long)K;
+    for (;;) {
+        // refill: take roots from the CTA queue until one needs an evaluation
+        while (g < 0 && !exhausted) {
+            const int q = atomicAdd(&s_next, 1);
+            if (c0 + q >= c1) { exhausted = true; break; }
+            g = c0 + q;
+            const int m = w.aMerge[g];
+            int ke;
+            active_range(w, L, m, ks, ke);
+            const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+            rs_begin(st, ke - ks, g - ks, rho, w.dA + ks, w.zA + ks, w.z2A + ks);
+            if (st.phase == kRsDone) {
+                w.org[g] = st.org;
+                w.tau[g] = st.tau;
+                g = -1;
+            }
+        }
+        if (!__any_sync(0xffffffffu, g >= 0)) break;
+        if (g >= 0) {
+            double sum, sum_abs, sum_d, psi;
+            bool pole = false;
+            const int K = st.K;
+            bool ok;
+            if (win.fits) {
+                const SmemPairs P{s_dz + (ks - win.P0)};
+                ok = eval_pass(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+                if (!ok) pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+            } else {
+                const GlobalPairs P{w.dA + ks, w.z2A + ks};
+                ok = eval_pass(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+                if (!ok) pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+            }
+            Ev ev;
+            ev.f = 1.0 + st.rho * sum;
+            ev.fp = st.rho * sum_d;
+            ev.abs_sum = st.rho * sum_abs;
+            ev.psi = st.rho * psi;
+            ev.pole = pole;
+            ++evals;
+            terms += (unsigned long long)K;
+            rs_consume(st, ev, w.dA + ks, patched != 0);
+            if (st.phase == kRsDone || st.phase == kRsFail) {
+                if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                w.org[g] = st.org;
+                w.tau[g] = st.tau;
+                g = -1;
+            }
+        }
     }
     evals = __reduce_add_sync(0xffffffffu, evals);
 #pragma unroll
@@ -480,24 +642,70 @@ __global__ void __launch_bounds__(128) k_secular(Work w, LevelDev L, int n, int 
     }
 }
 
+// Self-test of rcp_nr against __drcp_rn (bitwise) over x = m * 2^e.
+__global__ void k_selftest_rcp(long long count, unsigned long long seed, unsigned long long* bad) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    unsigned long long s = seed ^ (0x9E3779B97F4A7C15ULL * (unsigned long long)(i + 1));
+    s ^= s >> 12; s ^= s << 25; s ^= s >> 27;
+    s *= 0x2545F4914F6CDD1DULL;
+    const int ex = (int)((s >> 52) % 2001) - 1000;          // exponent in [-1000, 1000]
+    unsigned long long mant = s & 0xFFFFFFFFFFFFFULL;         // random mantissa
+    if (i & 1) {  // low-entropy mantissas: only the top k bits set (powers of two, 1.5, ...)
+        const int k = (int)((s >> 20) % 53);
+        mant &= ~((1ULL << (52 - k)) - 1ULL);
+    }
+    if ((i & 3) == 2) mant |= (1ULL << ((s >> 8) % 52)) - 1ULL;  // trailing ones
+    double x = __longlong_as_double((long long)((1023ULL << 52) | mant));
+    x = ldexp(x, ex);
+    if (s & (1ULL << 63)) x = -x;
+    if (__double_as_longlong(rcp_nr(x)) != __double_as_longlong(__drcp_rn(x))) atomicAdd(bad, 1ULL);
+}
+
 // Gu-Eisenstat refreshed weights, one pole per thread, roots in order
 // (secular.cpp:288-313); replaces zA in place by sign(z)*sqrt(max(0,-w)).
-__global__ void __launch_bounds__(128) k_zhat(Work w, LevelDev L, int n) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
+    __shared__ double s_d[kWin], s_tau[kWin];
+    __shared__ int s_org[kWin];
     const int T = w.survPre[w.nnPre[n]];
+    const int g0 = blockIdx.x * kSecBlock;
+    if (g0 >= T) return;
+    const Window win = cta_window(w, L, T);
+    if (win.fits) {
+        for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock) {
+            s_d[i] = w.dA[win.P0 + i];
+            s_tau[i] = w.tau[win.P0 + i];
+            s_org[i] = w.org[win.P0 + i];
+        }
+        __syncthreads();
+    }
+    const int g = g0 + threadIdx.x;
     if (g >= T) return;
     const int m = w.aMerge[g];
     if (L.mFlags[m] & kMergeRoot) return;
     int ks, ke;
     active_range(w, L, m, ks, ke);
     const int i = g - ks, K = ke - ks;
-    const double* __restrict__ dA = w.dA + ks;
+    const double* __restrict__ dA = win.fits ? s_d + (ks - win.P0) : w.dA + ks;
+    const double* __restrict__ tau = win.fits ? s_tau + (ks - win.P0) : w.tau + ks;
+    const int* __restrict__ org = win.fits ? s_org + (ks - win.P0) : w.org + ks;
     const double di = dA[i];
     double prod = 1.0;
+    unsigned minexp = 0x7ff00000u;
     for (int j = 0; j < K; ++j) {
-        const double del = (di - dA[w.org[ks + j]]) - w.tau[ks + j];
-        if (j == i) prod = prod * del;
-        else prod = prod * (del * __drcp_rn(di - dA[j]));
+        const double del = (di - dA[org[j]]) - tau[j];
+        const double dd = di - dA[j];
+        if (j != i) minexp = min(minexp, expfield(dd));
+        const double f = (j == i) ? del : del * rcp_nr(dd);
+        prod = prod * f;
+    }
+    if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {  // exact redo (never for distinct scaled poles)
+        prod = 1.0;
+        for (int j = 0; j < K; ++j) {
+            const double del = (di - dA[org[j]]) - tau[j];
+            if (j == i) prod = prod * del;
+            else prod = prod * (del * __drcp_rn(di - dA[j]));
+        }
     }
     const double mag = sqrt(fmax(0.0, -prod));
     w.zA[g] = w.zA[g] >= 0.0 ? mag : -mag;
@@ -506,9 +714,22 @@ __global__ void __launch_bounds__(128) k_zhat(Work w, LevelDev L, int n) {
 // Parent boundary rows for root j: R_parent(:,j) = R_child y_j with
 // y = zhat/Delta_j / ||zhat/Delta_j|| streamed (never stored),
 // plus placement of lambda_j in the parent's ascending order.
-__global__ void __launch_bounds__(128) k_rows(Work w, LevelDev L, int n) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
+    __shared__ double s_d[kWin], s_zh[kWin], s_r0[kWin], s_r1[kWin];
     const int T = w.survPre[w.nnPre[n]];
+    const int g0 = blockIdx.x * kSecBlock;
+    if (g0 >= T) return;
+    const Window win = cta_window(w, L, T);
+    if (win.fits) {
+        for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock) {
+            s_d[i] = w.dA[win.P0 + i];
+            s_zh[i] = w.zA[win.P0 + i];
+            s_r0[i] = w.r0A[win.P0 + i];
+            s_r1[i] = w.r1A[win.P0 + i];
+        }
+        __syncthreads();
+    }
+    const int g = g0 + threadIdx.x;
     if (g >= T) return;
     const int m = w.aMerge[g];
     int ks, ke;
@@ -516,7 +737,8 @@ __global__ void __launch_bounds__(128) k_rows(Work w, LevelDev L, int n) {
     const int K = ke - ks, j = g - ks;
     const int off = L.mOff[m], size = L.mSize[m];
     const bool is_root = L.mFlags[m] & kMergeRoot;
-    const double* __restrict__ dA = w.dA + ks;
+    const int sh = ks - win.P0;
+    const double* __restrict__ dA = win.fits ? s_d + sh : w.dA + ks;
     const double dorg = dA[w.org[g]];
     const double tau = w.tau[g];
     const double lam = dorg + tau;
@@ -525,21 +747,33 @@ __global__ void __launch_bounds__(128) k_rows(Work w, LevelDev L, int n) {
     const int p = off + pos;
     w.lam[p] = lam;
     if (is_root) return;
-    const double* __restrict__ zh = w.zA + ks;
-    const double* __restrict__ r0 = w.r0A + ks;
-    const double* __restrict__ r1 = w.r1A + ks;
+    const double* __restrict__ zh = win.fits ? s_zh + sh : w.zA + ks;
+    const double* __restrict__ r0 = win.fits ? s_r0 + sh : w.r0A + ks;
+    const double* __restrict__ r1 = win.fits ? s_r1 + sh : w.r1A + ks;
     double nn = 0.0, s0 = 0.0, s1 = 0.0;
-    bool zero = false;
+    unsigned minexp = 0x7ff00000u;
 #pragma unroll 4
     for (int i = 0; i < K; ++i) {
         const double del = (dA[i] - dorg) - tau;
-        zero |= (del == 0.0);
-        const double y = zh[i] * __drcp_rn(del);
+        minexp = min(minexp, expfield(del));
+        const double y = zh[i] * rcp_nr(del);
         nn = __fma_rn(y, y, nn);
         s0 = __fma_rn(r0[i], y, s0);
         s1 = __fma_rn(r1[i], y, s1);
     }
-    if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+    if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {  // exact redo; a zero delta is an error
+        bool zero = false;
+        nn = 0.0; s0 = 0.0; s1 = 0.0;
+        for (int i = 0; i < K; ++i) {
+            const double del = (dA[i] - dorg) - tau;
+            zero |= (del == 0.0);
+            const double y = zh[i] * __drcp_rn(del);
+            nn = __fma_rn(y, y, nn);
+            s0 = __fma_rn(r0[i], y, s0);
+            s1 = __fma_rn(r1[i], y, s1);
+        }
+        if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+    }
     const double inv = 1.0 / sqrt(nn);
     w.blo[p] = s0 * inv;
     w.bhi[p] = s1 * inv;
@@ -617,6 +851,23 @@ __global__ void k_merge_runs(int n, const double* __restrict__ src, double* __re
 // ---------------------------------------------------------------------------
 static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
+int selftest_rcp(long long count, unsigned long long seed, unsigned long long* host_bad) {
+    unsigned long long* d;
+    if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return BRGPU_ERR_CUDA;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    k_selftest_rcp<<<(int)((count + 255) / 256), 256>>>(count, seed, d);
+    cudaError_t e = cudaMemcpy(host_bad, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? BRGPU_OK : BRGPU_ERR_CUDA;
+}
+
+void init_kernel_attributes() {
+    cudaFuncSetAttribute(k_leaf<26>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4 * 26 * kLeafThreads * (int)sizeof(double));
+    cudaFuncSetAttribute(k_leaf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4 * 32 * kLeafThreads * (int)sizeof(double));
+}
+
 void launch_copy_input(cudaStream_t s, int n, const double* d, const double* e, double* dw,
                        double* ew) {
     k_copy_input<<<cdiv(n, 256), 256, 0, s>>>(n, d, e, dw, ew);
@@ -650,12 +901,16 @@ void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned
 void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const int* tSize,
                    const int* tFlags, const Work& w, int* launches, Prof* prof) {
     if (ntask <= 0) return;
-    if (maxm <= 32)
-        k_leaf<32><<<cdiv(ntask, 128), 128, 0, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
-                                                   w.blo, w.bhi, w.status);
-    else
-        k_leaf<64><<<cdiv(ntask, 128), 128, 0, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
-                                                   w.blo, w.bhi, w.status);
+    const int grid = cdiv(ntask, kLeafThreads);
+    if (maxm <= 26) {
+        const size_t sm = 4 * 26 * kLeafThreads * sizeof(double);
+        k_leaf<26><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+                                                  w.blo, w.bhi, w.status);
+    } else {
+        const size_t sm = 4 * 32 * kLeafThreads * sizeof(double);
+        k_leaf<32><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+                                                  w.blo, w.bhi, w.status);
+    }
     *launches += 1;
     PMARK(BRGPU_K_LEAF);
 }
@@ -682,15 +937,15 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
     PMARK(BRGPU_K_SCAN);
     k_surv_write<<<ntiles, kScanBlock, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_SURVWRITE);
-    k_secular<<<cdiv(n, 128), 128, 0, s>>>(w, L, n, prm.patched);
+    k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
     PMARK(BRGPU_K_SECULAR);
     int nl = 10;
     if (prm.zhat) {
-        k_zhat<<<cdiv(n, 128), 128, 0, s>>>(w, L, n);
+        k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
         PMARK(BRGPU_K_ZHAT);
         ++nl;
     }
-    k_rows<<<cdiv(n, 128), 128, 0, s>>>(w, L, n);
+    k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_ROWS);
     k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_DEFLATED);
