@@ -43,6 +43,7 @@ void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, co
                        int nruns, int* launches, Prof* prof);
 
 void init_kernel_attributes();
+int sec_ctas_per_sm();
 int selftest_rcp(long long count, unsigned long long seed, unsigned long long* host_bad);
 
 struct Prof {
@@ -602,7 +603,7 @@ int brgpu_create(brgpu_handle** out, int device) {
     }
     brgpu::init_kernel_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    h->sec_grid = h->sms * 6;
+    h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
     *out = hh;
     return BRGPU_OK;
 }

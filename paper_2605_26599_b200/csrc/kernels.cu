@@ -498,7 +498,17 @@ __device__ __forceinline__ Window cta_window(const Work& w, const LevelDev& L, i
 // as soon as its root converges.  Every evaluation is one warp-uniform loop
 // over the poles (shared-memory broadcast reads), so lanes never wait on
 // a neighbour's slower root and the pole loop has no divergence.
-constexpr int kSecWinQ = 2048;
+#ifndef BRGPU_SEC_WIN
+#define BRGPU_SEC_WIN 2048
+#endif
+constexpr int kSecWinQ = BRGPU_SEC_WIN;
+#ifndef BRGPU_SEC_MINB
+#define BRGPU_SEC_MINB 6
+#endif
+#ifndef BRGPU_SEC_UNROLL
+#define BRGPU_SEC_UNROLL 4
+#endif
+constexpr int kSecUnroll = BRGPU_SEC_UNROLL;
 
 // One evaluation pass for one lane: f, f', rho*sum|t|, psi' at (dorg, tau) over
 // K poles in pole order (secular.cpp:26-52).  P yields (d_i, z_i^2) pairs.
@@ -511,7 +521,7 @@ __device__ __forceinline__ bool eval_pass(const P& pairs, int K, int jsplit, dou
                                           double& sum, double& sum_abs, double& sum_d, double& psi) {
     sum = 0.0; sum_abs = 0.0; sum_d = 0.0; psi = 0.0;
     unsigned minexp = 0x7ff00000u;
-#pragma unroll 4
+#pragma unroll kSecUnroll
     for (int i = 0; i < K; ++i) {
         const double2 dz = pairs(i);
         const double del = (dz.x - dorg) - tau;
@@ -563,7 +573,7 @@ struct GlobalPairs {
 // resumable state machine (RootSM) and pulls the next root from a CTA queue
 // as soon as its root converges.  Evaluations are branch-free pole loops over
 // shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
-__global__ void __launch_bounds__(kSecBlock) k_secular(Work w, LevelDev L, int n, int patched) {
+__global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, LevelDev L, int n, int patched) {
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ int s_next;
     const int T = w.survPre[w.nnPre[n]];
@@ -861,6 +871,8 @@ int selftest_rcp(long long count, unsigned long long seed, unsigned long long* h
     return e == cudaSuccess ? BRGPU_OK : BRGPU_ERR_CUDA;
 }
 
+int sec_ctas_per_sm() { return BRGPU_SEC_MINB; }
+
 void init_kernel_attributes() {
     cudaFuncSetAttribute(k_leaf<26>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          4 * 26 * kLeafThreads * (int)sizeof(double));
@@ -902,7 +914,11 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
                    const int* tFlags, const Work& w, int* launches, Prof* prof) {
     if (ntask <= 0) return;
     const int grid = cdiv(ntask, kLeafThreads);
-    if (maxm <= 26) {
+    if (maxm <= 16) {
+        const size_t sm = 4 * 16 * kLeafThreads * sizeof(double);
+        k_leaf<16><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+                                                  w.blo, w.bhi, w.status);
+    } else if (maxm <= 26) {
         const size_t sm = 4 * 26 * kLeafThreads * sizeof(double);
         k_leaf<26><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
