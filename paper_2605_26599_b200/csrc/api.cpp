@@ -41,6 +41,12 @@ void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
                    const unsigned long long* sbits, double* lam, int* launches, Prof* prof);
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
                        int nruns, int* launches, Prof* prof);
+void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups,
+                        const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
+                        int* launches, Prof* prof);
+void init_fused_attributes();
+constexpr int kFuseMaxElems = 1024;
+constexpr int kFuseMaxMergesHost = 128;
 
 void init_kernel_attributes();
 int sec_ctas_per_sm();
@@ -72,6 +78,8 @@ struct LevelHost {
     int m0;      // first merge index (global across levels)
     int M;       // merges at this level
     int tile0;   // offset of this level's tileFirst table
+    bool fused;  // all merges <= kFuseMaxElems: one fused SMEM launch (fused.cu)
+    int g0, G;   // groups of the fused launch
 };
 
 struct Plan {
@@ -84,6 +92,7 @@ struct Plan {
     std::vector<int> cutPos;
     std::vector<int> mOff, mSize, mNL, mFlags, mLevel;
     std::vector<int> tileFirst;
+    std::vector<int> gFirst, gCount;  // fused groups (level-local first merge, count)
     std::vector<LevelHost> levels;
     std::vector<std::vector<int>> runPasses;  // run boundaries before each merge pass
     int height = 0;
@@ -94,7 +103,7 @@ struct Plan {
     size_t devInts = 0;
     int *d_tOff = nullptr, *d_tSize = nullptr, *d_tFlags = nullptr, *d_cut = nullptr;
     int *d_mOff = nullptr, *d_mSize = nullptr, *d_mNL = nullptr, *d_mFlags = nullptr;
-    int *d_tileFirst = nullptr, *d_bstart = nullptr;
+    int *d_tileFirst = nullptr, *d_bstart = nullptr, *d_gFirst = nullptr, *d_gCount = nullptr;
     std::vector<int*> d_runs;
     cudaGraphExec_t graph = nullptr;
     bool graph_trace = false;
@@ -181,7 +190,7 @@ int build_node(int off, int size, int cutoff, bool root, std::vector<NodeRec>& i
 }
 
 std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
-                                const std::vector<int>& segs) {
+                                const std::vector<int>& segs, bool fuse) {
     auto p = std::make_unique<Plan>();
     p->n = n;
     p->cutoff = cutoff;
@@ -232,6 +241,28 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
         }
         L.M = (int)(j - i);
         p->maxM = std::max(p->maxM, L.M);
+        // fused SMEM tier when every merge of the level fits a group
+        int maxSize = 0;
+        for (int q = 0; q < L.M; ++q) maxSize = std::max(maxSize, p->mSize[L.m0 + q]);
+        L.fused = fuse && maxSize <= kFuseMaxElems;
+        L.g0 = (int)p->gFirst.size();
+        L.G = 0;
+        if (L.fused) {
+            int q = 0;
+            while (q < L.M) {
+                int c = 1, tot = p->mSize[L.m0 + q];
+                while (q + c < L.M && c < kFuseMaxMergesHost &&
+                       p->mOff[L.m0 + q + c] == p->mOff[L.m0 + q + c - 1] + p->mSize[L.m0 + q + c - 1] &&
+                       tot + p->mSize[L.m0 + q + c] <= kFuseMaxElems) {
+                    tot += p->mSize[L.m0 + q + c];
+                    ++c;
+                }
+                p->gFirst.push_back(q);
+                p->gCount.push_back(c);
+                q += c;
+                ++L.G;
+            }
+        }
         // tileFirst[t] = first merge whose end exceeds t*kTile
         int m = 0;
         for (int t = 0; t <= ntiles; ++t) {
@@ -283,6 +314,7 @@ int upload_plan(Handle* h, Plan* p) {
     const size_t oMOff = put(p->mOff), oMSize = put(p->mSize), oMNL = put(p->mNL), oMF = put(p->mFlags);
     const size_t oTile = put(p->tileFirst);
     const size_t oB = put(p->bstart);
+    const size_t oGF = put(p->gFirst), oGC = put(p->gCount);
     std::vector<size_t> oRuns;
     for (auto& rp : p->runPasses) oRuns.push_back(put(rp));
     p->devInts = buf.size();
@@ -292,6 +324,7 @@ int upload_plan(Handle* h, Plan* p) {
     p->d_cut = p->dev + oCut;
     p->d_mOff = p->dev + oMOff; p->d_mSize = p->dev + oMSize; p->d_mNL = p->dev + oMNL;
     p->d_mFlags = p->dev + oMF; p->d_tileFirst = p->dev + oTile; p->d_bstart = p->dev + oB;
+    p->d_gFirst = p->dev + oGF; p->d_gCount = p->dev + oGC;
     for (size_t o : oRuns) p->d_runs.push_back(p->dev + o);
     return BRGPU_OK;
 }
@@ -394,8 +427,13 @@ int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
         L.mTol = h->mTol;
         L.tileFirst = p->d_tileFirst + lh.tile0;
         L.M = lh.M;
-        launch_level(s, h->w, L, n, prm, launches, prof);
-        if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
+        if (lh.fused) {
+            launch_level_fused(s, h->w, L, lh.G, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
+                               h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
+        } else {
+            launch_level(s, h->w, L, n, prm, launches, prof);
+            if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
+        }
     }
     launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
     // cross-block merge passes (ping-pong lam <-> D), result back in lam
@@ -439,7 +477,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     Plan* p = h->plan.get();
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs) {
         if (h->plan) free_plan(h->plan.get());
-        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs);
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0);
         p = h->plan.get();
         int r = upload_plan(h, p);
         if (r) return r;
@@ -602,6 +640,7 @@ int brgpu_create(brgpu_handle** out, int device) {
         return BRGPU_ERR_CUDA;
     }
     brgpu::init_kernel_attributes();
+    brgpu::init_fused_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
     *out = hh;
@@ -779,7 +818,7 @@ const char* brgpu_kernel_class_name(int c) {
     static const char* names[BRGPU_NCLASS] = {
         "prepare(scale+cuts)", "leaf", "merge_tol", "merge_scatter", "nn_flag", "scan_tiles",
         "nn_write", "segment_walk", "surv_count", "surv_write", "secular", "zhat", "rows",
-        "deflated_out", "trace", "finish", "subtree"};
+        "deflated_out", "trace", "finish", "fused_level"};
     return (c >= 0 && c < BRGPU_NCLASS) ? names[c] : "?";
 }
 

@@ -1,0 +1,437 @@
+// fused.cu -- one-launch-per-level merge kernel for the bottom of the tree.
+//
+// A CTA owns a GROUP of consecutive whole merges of one level (<= kFuseMax
+// elements, <= kFuseMaxMerges merges, contiguous in position).  Everything a
+// merge does happens in shared memory: per-merge tolerance (deflate.cpp:55-60),
+// the stable merge of the sorted children with z = (sign*bhi_L, blo_R)
+// (deflate.cpp:31-41, 62-66), small-z compaction, the close-pole Givens walk
+// with its replay on the two selected rows (deflate.cpp:70-107, 109-140), the
+// survivor compaction, the secular roots (secular.cpp:80-241; resumable
+// per-lane RootSM with a CTA root queue), the Gu-Eisenstat weights
+// (secular.cpp:288-313) and the boundary-row streaming R_parent(:,j) =
+// R_child y_j -- then the parent state is written to HBM
+// once.  Arithmetic and every reduction order are those of the grid-tier
+// kernels in kernels.cu (and of oracle/br_oracle.c): results are bit-identical.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.hpp"
+#include "numerics.cuh"
+
+namespace brgpu {
+
+constexpr int kFuseThreads = 256;
+constexpr int kFuseMax = 1024;        // elements per group
+constexpr int kFuseMaxMerges = 128;   // merges per group
+
+struct FuseSmem {
+    // sorted merge arrays (local positions)
+    double D[kFuseMax];
+    double Z[kFuseMax];
+    double R0[kFuseMax];
+    double R1[kFuseMax];
+    // inputs (lam, blo, bhi); after the scatter: active (d, z^2) pairs + active z / z-hat
+    double in[3 * kFuseMax];
+    double r0A[kFuseMax];
+    double r1A[kFuseMax];
+    double tau[kFuseMax];
+    int org[kFuseMax];
+    int nnPre[kFuseMax + 1];
+    int nnPos[kFuseMax];
+    int survPre[kFuseMax + 1];
+    unsigned char flag[kFuseMax];
+    unsigned char surv[kFuseMax];
+    // per-merge metadata
+    int mo[kFuseMaxMerges + 1];  // local offsets (+ end)
+    int ms[kFuseMaxMerges];
+    int mnl[kFuseMaxMerges];
+    int mf[kFuseMaxMerges];
+    int kS[kFuseMaxMerges + 1];  // active ranges
+    double rho[kFuseMaxMerges];
+    double neg[kFuseMaxMerges];  // -1 when e_m < 0
+    unsigned long long tolb[kFuseMaxMerges];
+    int scan[kFuseThreads / 32];
+    int next;
+    int cnt;
+    unsigned long long evals, terms;
+};
+
+__device__ __forceinline__ int cta_excl_scan(int v, int& total, int* warp_tot) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = kFuseThreads / 32;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < NW ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < NW) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const int base = wid ? warp_tot[wid - 1] : 0;
+    total = warp_tot[NW - 1];
+    __syncthreads();
+    return base + x - v;
+}
+
+// exclusive prefix of flags[0..E) into pre[0..E]; each thread scans a contiguous chunk
+__device__ __forceinline__ int cta_scan_flags(const unsigned char* flags, int E, int* pre, int* warp_tot) {
+    const int per = (E + kFuseThreads - 1) / kFuseThreads;
+    const int i0 = threadIdx.x * per;
+    int local = 0;
+    for (int k = 0; k < per; ++k) {
+        const int i = i0 + k;
+        if (i < E) local += flags[i];
+    }
+    int tot;
+    int run = cta_excl_scan(local, tot, warp_tot);
+    for (int k = 0; k < per; ++k) {
+        const int i = i0 + k;
+        if (i < E) {
+            pre[i] = run;
+            run += flags[i];
+        }
+    }
+    if (threadIdx.x == 0) pre[E] = tot;
+    __syncthreads();
+    return tot;
+}
+
+// largest t in [0, cnt) with a[t] <= x
+__device__ __forceinline__ int upper_index(const int* a, int cnt, int x) {
+    int lo = 0, hi = cnt;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kFuseThreads, 2)
+k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
+              SolveParams prm, int* __restrict__ traceOut) {
+    extern __shared__ __align__(16) unsigned char fuse_raw[];
+    FuseSmem& S = *reinterpret_cast<FuseSmem*>(fuse_raw);
+    const int tid = threadIdx.x;
+    const int m0 = gFirst[blockIdx.x];
+    const int cnt = gCount[blockIdx.x];
+    const int base = L.mOff[m0];
+
+    // ---- metadata + inputs -------------------------------------------------
+    if (tid < cnt) {
+        const int m = m0 + tid;
+        const int off = L.mOff[m] - base, nl = L.mNL[m];
+        S.mo[tid] = off;
+        S.ms[tid] = L.mSize[m];
+        S.mnl[tid] = nl;
+        S.mf[tid] = L.mFlags[m];
+        const double em = w.ew[L.mOff[m] + nl - 1];
+        S.rho[tid] = fabs(em);
+        S.neg[tid] = em < 0 ? -1.0 : 1.0;
+        S.tolb[tid] = 0ULL;
+        if (tid == cnt - 1) S.mo[cnt] = off + L.mSize[m];
+    }
+    if (tid == 0) {
+        S.next = 0;
+        S.evals = 0;
+        S.terms = 0;
+        S.cnt = cnt;
+    }
+    __syncthreads();
+    const int E = S.mo[cnt];
+    double* lamIn = S.in;
+    double* bloIn = S.in + kFuseMax;
+    double* bhiIn = S.in + 2 * kFuseMax;
+    for (int i = tid; i < E; i += kFuseThreads) {
+        lamIn[i] = w.lam[base + i];
+        bloIn[i] = w.blo[base + i];
+        bhiIn[i] = w.bhi[base + i];
+    }
+    __syncthreads();
+
+    // ---- tolerance: max(|D|, |z|) per merge ---------------------------------
+    for (int i = tid; i < E; i += kFuseThreads) {
+        const int t = upper_index(S.mo, cnt, i);
+        const double zv = (i - S.mo[t] < S.mnl[t]) ? bhiIn[i] : bloIn[i];
+        const double v = fmax(fabs(lamIn[i]), fabs(zv));
+        atomicMax(&S.tolb[t], (unsigned long long)__double_as_longlong(v));
+    }
+    __syncthreads();
+
+    // ---- stable merge of the two sorted children + z ------------------------
+    for (int i = tid; i < E; i += kFuseThreads) {
+        const int t = upper_index(S.mo, cnt, i);
+        const int off = S.mo[t], nl = S.mnl[t], nr = S.ms[t] - nl;
+        const double v = lamIn[i];
+        int sp;
+        double z, r0, r1;
+        if (i < off + nl) {
+            sp = i + count_less(lamIn + off + nl, nr, v);
+            const double b = bhiIn[i];
+            z = S.neg[t] < 0 ? -b : b;
+            r0 = bloIn[i];
+            r1 = 0.0;
+        } else {
+            sp = (i - nl) + count_leq(lamIn + off, nl, v);
+            z = bloIn[i];
+            r0 = 0.0;
+            r1 = bhiIn[i];
+        }
+        S.D[sp] = v;
+        S.Z[sp] = z;
+        S.R0[sp] = r0;
+        S.R1[sp] = r1;
+    }
+    __syncthreads();
+
+    // ---- small-z flags + NN compaction --------------------------------------
+    for (int i = tid; i < E; i += kFuseThreads) {
+        const int t = upper_index(S.mo, cnt, i);
+        const double tol = 8.0 * kU * __longlong_as_double((long long)S.tolb[t]) * prm.tol_scale;
+        S.flag[i] = fabs(S.Z[i]) > tol;
+    }
+    __syncthreads();
+    const int NN = cta_scan_flags(S.flag, E, S.nnPre, S.scan);
+    for (int i = tid; i < E; i += kFuseThreads)
+        if (S.flag[i]) S.nnPos[S.nnPre[i]] = i;
+    __syncthreads();
+
+    // ---- close-pole deflation: segment heads walk their runs ----------------
+    for (int q = tid; q < NN; q += kFuseThreads) {
+        const int k = S.nnPos[q];
+        const int t = upper_index(S.mo, cnt, k);
+        const int qs = S.nnPre[S.mo[t]], qe = S.nnPre[S.mo[t] + S.ms[t]];
+        const double tol = 8.0 * kU * __longlong_as_double((long long)S.tolb[t]) * prm.tol_scale;
+        if (q > qs && fabs(S.D[k] - S.D[S.nnPos[q - 1]]) <= tol) continue;  // not a head
+        S.surv[q] = 1;
+        int prev = k;
+        double dprev_nn = S.D[k];
+        for (int q2 = q + 1; q2 < qe; ++q2) {
+            const int k2 = S.nnPos[q2];
+            const double d2 = S.D[k2];
+            if (fabs(d2 - dprev_nn) > tol) break;
+            dprev_nn = d2;
+            if (fabs(d2 - S.D[prev]) <= tol) {
+                const double zp = S.Z[prev], zq = S.Z[k2];
+                const double r = hyp(zp, zq);
+                const double c = zp / r, s = zq / r;
+                S.Z[prev] = r;
+                S.Z[k2] = 0.0;
+                double xp = S.R0[prev], xq = S.R0[k2];
+                S.R0[prev] = c * xp + s * xq;
+                S.R0[k2] = c * xq - s * xp;
+                xp = S.R1[prev]; xq = S.R1[k2];
+                S.R1[prev] = c * xp + s * xq;
+                S.R1[k2] = c * xq - s * xp;
+                S.surv[q2] = 0;
+            } else {
+                S.surv[q2] = 1;
+                prev = k2;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- survivor compaction: active (d, z^2) pairs, z, rows ----------------
+    const int T = cta_scan_flags(S.surv, NN, S.survPre, S.scan);
+    double2* pairs = reinterpret_cast<double2*>(S.in);   // aliases lam/blo inputs (dead)
+    double* zA = S.in + 2 * kFuseMax;                     // aliases bhi input (dead)
+    for (int q = tid; q < NN; q += kFuseThreads) {
+        if (!S.surv[q]) continue;
+        const int g = S.survPre[q], k = S.nnPos[q];
+        const double z = S.Z[k];
+        pairs[g] = make_double2(S.D[k], z * z);
+        zA[g] = z;
+        S.r0A[g] = S.R0[k];
+        S.r1A[g] = S.R1[k];
+    }
+    if (tid <= cnt) S.kS[tid] = S.survPre[S.nnPre[tid < cnt ? S.mo[tid] : E]];
+    __syncthreads();
+
+    // ---- secular roots: per-lane RootSM, CTA queue --------------------------
+    {
+        RootSM st;
+        int g = -1, ks = 0;
+        bool exhausted = false;
+        unsigned long long evals = 0, terms = 0;
+        for (;;) {
+            while (g < 0 && !exhausted) {
+                const int q = atomicAdd(&S.next, 1);
+                if (q >= T) { exhausted = true; break; }
+                g = q;
+                const int t = upper_index(S.kS, cnt, g);
+                ks = S.kS[t];
+                const int K = S.kS[t + 1] - ks;
+                rs_begin(st, K, g - ks, S.rho[t], PolesPairs{pairs + ks}, zA[ks], Z2Pairs{pairs + ks});
+                if (st.phase == kRsDone) {
+                    S.org[g] = st.org;
+                    S.tau[g] = st.tau;
+                    g = -1;
+                }
+            }
+            if (!__any_sync(0xffffffffu, g >= 0)) break;
+            if (g >= 0) {
+                double sum, sum_abs, sum_d, psi;
+                bool pole = false;
+                const SmemPairs P{pairs + ks};
+                const bool ok = eval_pass(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+                if (!ok) pole = eval_pass_exact(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+                Ev ev;
+                ev.f = 1.0 + st.rho * sum;
+                ev.fp = st.rho * sum_d;
+                ev.abs_sum = st.rho * sum_abs;
+                ev.psi = st.rho * psi;
+                ev.pole = pole;
+                ++evals;
+                terms += (unsigned long long)st.K;
+                rs_consume(st, ev, PolesPairs{pairs + ks}, prm.patched != 0);
+                if (st.phase == kRsDone || st.phase == kRsFail) {
+                    if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                    S.org[g] = st.org;
+                    S.tau[g] = st.tau;
+                    g = -1;
+                }
+            }
+        }
+        if (evals) {
+            atomicAdd(&S.evals, evals);
+            atomicAdd(&S.terms, terms);
+        }
+    }
+    __syncthreads();
+
+    // ---- Gu-Eisenstat refreshed weights (non-root merges) --------------------
+    if (prm.zhat) {
+        for (int g = tid; g < T; g += kFuseThreads) {
+            const int t = upper_index(S.kS, cnt, g);
+            if (S.mf[t] & kMergeRoot) continue;
+            const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
+            const double di = pairs[g].x;
+            double prod = 1.0;
+            unsigned minexp = 0x7ff00000u;
+            for (int j = 0; j < K; ++j) {
+                const double del = (di - pairs[ks + S.org[ks + j]].x) - S.tau[ks + j];
+                const double dd = di - pairs[ks + j].x;
+                if (j != i) minexp = min(minexp, expfield(dd));
+                const double f = (j == i) ? del : del * rcp_nr(dd);
+                prod = prod * f;
+            }
+            if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {
+                prod = 1.0;
+                for (int j = 0; j < K; ++j) {
+                    const double del = (di - pairs[ks + S.org[ks + j]].x) - S.tau[ks + j];
+                    if (j == i) prod = prod * del;
+                    else prod = prod * (del * __drcp_rn(di - pairs[ks + j].x));
+                }
+            }
+            const double mag = sqrt(fmax(0.0, -prod));
+            zA[g] = zA[g] >= 0.0 ? mag : -mag;
+        }
+        __syncthreads();
+    }
+
+    // ---- roots: boundary rows + placement; deflated columns: placement -------
+    for (int g = tid; g < T; g += kFuseThreads) {
+        const int t = upper_index(S.kS, cnt, g);
+        const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
+        const int off = S.mo[t], size = S.ms[t];
+        const double dorg = pairs[ks + S.org[g]].x;
+        const double tau = S.tau[g];
+        const double lam = dorg + tau;
+        // #{dA <= lam} over the merge's active poles
+        int lo = 0, hi = K;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (!(lam < pairs[ks + mid].x)) lo = mid + 1; else hi = mid;
+        }
+        const int pos = j + count_leq(S.D + off, size, lam) - lo;
+        const int p = base + off + pos;
+        w.lam[p] = lam;
+        if (S.mf[t] & kMergeRoot) continue;
+        double nn = 0.0, s0 = 0.0, s1 = 0.0;
+        unsigned minexp = 0x7ff00000u;
+#pragma unroll 4
+        for (int i = 0; i < K; ++i) {
+            const double del = (pairs[ks + i].x - dorg) - tau;
+            minexp = min(minexp, expfield(del));
+            const double y = zA[ks + i] * rcp_nr(del);
+            nn = __fma_rn(y, y, nn);
+            s0 = __fma_rn(S.r0A[ks + i], y, s0);
+            s1 = __fma_rn(S.r1A[ks + i], y, s1);
+        }
+        if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {
+            bool zero = false;
+            nn = 0.0; s0 = 0.0; s1 = 0.0;
+            for (int i = 0; i < K; ++i) {
+                const double del = (pairs[ks + i].x - dorg) - tau;
+                zero |= (del == 0.0);
+                const double y = zA[ks + i] * __drcp_rn(del);
+                nn = __fma_rn(y, y, nn);
+                s0 = __fma_rn(S.r0A[ks + i], y, s0);
+                s1 = __fma_rn(S.r1A[ks + i], y, s1);
+            }
+            if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+        }
+        const double inv = 1.0 / sqrt(nn);
+        w.blo[p] = s0 * inv;
+        w.bhi[p] = s1 * inv;
+    }
+    for (int k = tid; k < E; k += kFuseThreads) {
+        const int q = S.nnPre[k];
+        if (S.flag[k] && S.surv[q]) continue;  // survivor: placed above
+        const int t = upper_index(S.mo, cnt, k);
+        const int off = S.mo[t];
+        const int ks = S.kS[t], K = S.kS[t + 1] - ks;
+        const int tt = (k - off) - (S.survPre[q] - ks);
+        const double v = S.D[k];
+        int lo = 0, hi = K;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const double lj = pairs[ks + S.org[ks + mid]].x + S.tau[ks + mid];
+            if (lj < v) lo = mid + 1; else hi = mid;
+        }
+        const int p = base + off + tt + lo;
+        w.lam[p] = v;
+        if (!(S.mf[t] & kMergeRoot)) {
+            w.blo[p] = S.R0[k];
+            w.bhi[p] = S.R1[k];
+        }
+    }
+
+    // ---- stats / trace -------------------------------------------------------
+    if (traceOut && tid < cnt) {
+        traceOut[2 * (m0 + tid)] = S.nnPre[S.mo[tid] + S.ms[tid]] - S.nnPre[S.mo[tid]];
+        traceOut[2 * (m0 + tid) + 1] = S.kS[tid + 1] - S.kS[tid];
+    }
+    __syncthreads();
+    if (tid == 0 && S.evals) {
+        atomicAdd(&w.counters[0], S.evals);
+        atomicAdd(&w.counters[1], S.terms);
+    }
+}
+
+void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups,
+                        const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
+                        int* launches, Prof* prof) {
+    k_level_fused<<<ngroups, kFuseThreads, sizeof(FuseSmem), s>>>(w, L, gFirst, gCount, prm, traceOut);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
+}
+
+size_t fused_smem_bytes() { return sizeof(FuseSmem); }
+
+void init_fused_attributes() {
+    cudaFuncSetAttribute(k_level_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FuseSmem));
+}
+
+}  // namespace brgpu

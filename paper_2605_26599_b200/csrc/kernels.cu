@@ -25,29 +25,6 @@ namespace brgpu {
 // ---------------------------------------------------------------------------
 // helpers
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void set_status(int* status, int code) {
-    if (code) atomicCAS(status, 0, code);
-}
-
-// number of x[0..n) with x < v   (x ascending)
-__device__ __forceinline__ int count_less(const double* __restrict__ x, int n, double v) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (x[mid] < v) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-// number of x[0..n) with x <= v  (x ascending)
-__device__ __forceinline__ int count_leq(const double* __restrict__ x, int n, double v) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (!(v < x[mid])) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
 __device__ __forceinline__ int find_merge(const LevelDev& L, int p) {
     const int t = p / kTile;
     int m = L.tileFirst[t];
@@ -505,69 +482,6 @@ constexpr int kSecWinQ = BRGPU_SEC_WIN;
 #ifndef BRGPU_SEC_MINB
 #define BRGPU_SEC_MINB 6
 #endif
-#ifndef BRGPU_SEC_UNROLL
-#define BRGPU_SEC_UNROLL 4
-#endif
-constexpr int kSecUnroll = BRGPU_SEC_UNROLL;
-
-// One evaluation pass for one lane: f, f', rho*sum|t|, psi' at (dorg, tau) over
-// K poles in pole order (secular.cpp:26-52).  P yields (d_i, z_i^2) pairs.
-// psi' = sum_{i<=j} dt_i is the prefix of the same sequential sum, so it is
-// snapshotted instead of accumulated separately (bitwise identical).
-// Returns false if some |delta| left the fast reciprocal's domain (incl. a
-// pole, delta == 0); the caller then redoes the pass exactly.
-template <typename P>
-__device__ __forceinline__ bool eval_pass(const P& pairs, int K, int jsplit, double dorg, double tau,
-                                          double& sum, double& sum_abs, double& sum_d, double& psi) {
-    sum = 0.0; sum_abs = 0.0; sum_d = 0.0; psi = 0.0;
-    unsigned minexp = 0x7ff00000u;
-#pragma unroll kSecUnroll
-    for (int i = 0; i < K; ++i) {
-        const double2 dz = pairs(i);
-        const double del = (dz.x - dorg) - tau;
-        minexp = min(minexp, expfield(del));
-        const double r = rcp_nr(del);
-        const double t = dz.y * r;
-        sum += t;
-        sum_abs += fabs(t);
-        sum_d += t * r;
-        if (i == jsplit) psi = sum_d;
-    }
-    if (jsplit >= K) psi = sum_d;
-    return minexp >= kRcpMinExp && minexp != 0x7ff00000u;
-}
-
-// Exact (slow) pass with __drcp_rn and explicit pole detection.
-template <typename P>
-__device__ __noinline__ bool eval_pass_exact(const P& pairs, int K, int jsplit, double dorg, double tau,
-                                             double& sum, double& sum_abs, double& sum_d, double& psi) {
-    sum = 0.0; sum_abs = 0.0; sum_d = 0.0; psi = 0.0;
-    bool pole = false;
-    for (int i = 0; i < K; ++i) {
-        const double2 dz = pairs(i);
-        const double del = (dz.x - dorg) - tau;
-        pole |= (del == 0.0);
-        const double r = __drcp_rn(del);
-        const double t = dz.y * r;
-        sum += t;
-        sum_abs += fabs(t);
-        const double dt = t * r;
-        sum_d += dt;
-        if (i <= jsplit) psi += dt;
-    }
-    return pole;
-}
-
-struct SmemPairs {
-    const double2* p;
-    __device__ __forceinline__ double2 operator()(int i) const { return p[i]; }
-};
-struct GlobalPairs {
-    const double* d;
-    const double* z2;
-    __device__ __forceinline__ double2 operator()(int i) const { return make_double2(d[i], z2[i]); }
-};
-
 // Secular roots (secular.cpp:80-241, tau-relative stop when patched).
 // A CTA owns a chunk of roots; each lane runs one root's iteration as a
 // resumable state machine (RootSM) and pulls the next root from a CTA queue
@@ -582,10 +496,9 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
     if (c0 >= T) return;  // uniform per CTA
     const int c1 = min(c0 + R, T);
     const Window win = range_window(w, L, c0, c1, kSecWinQ);
-    if (win.fits) {
-        for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock)
-            s_dz[i] = make_double2(w.dA[win.P0 + i], w.z2A[win.P0 + i]);
-    }
+    if (!win.fits) return;  // large-K chunk: k_secular_tiled (tiled.cu) owns it
+    for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock)
+        s_dz[i] = make_double2(w.dA[win.P0 + i], w.z2A[win.P0 + i]);
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
 
@@ -604,7 +517,7 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
             int ke;
             active_range(w, L, m, ks, ke);
             const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
-            rs_begin(st, ke - ks, g - ks, rho, w.dA + ks, w.zA + ks, w.z2A + ks);
+            rs_begin(st, ke - ks, g - ks, rho, PolesPtr{w.dA + ks}, w.zA[ks], Z2Ptr{w.z2A + ks});
             if (st.phase == kRsDone) {
                 w.org[g] = st.org;
                 w.tau[g] = st.tau;
@@ -616,16 +529,9 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
             double sum, sum_abs, sum_d, psi;
             bool pole = false;
             const int K = st.K;
-            bool ok;
-            if (win.fits) {
-                const SmemPairs P{s_dz + (ks - win.P0)};
-                ok = eval_pass(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
-                if (!ok) pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
-            } else {
-                const GlobalPairs P{w.dA + ks, w.z2A + ks};
-                ok = eval_pass(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
-                if (!ok) pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
-            }
+            const SmemPairs P{s_dz + (ks - win.P0)};
+            const bool ok = eval_pass(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+            if (!ok) pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
             Ev ev;
             ev.f = 1.0 + st.rho * sum;
             ev.fp = st.rho * sum_d;
@@ -634,7 +540,7 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
             ev.pole = pole;
             ++evals;
             terms += (unsigned long long)K;
-            rs_consume(st, ev, w.dA + ks, patched != 0);
+            rs_consume(st, ev, PolesPtr{w.dA + ks}, patched != 0);
             if (st.phase == kRsDone || st.phase == kRsFail) {
                 if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
                 w.org[g] = st.org;
@@ -674,42 +580,59 @@ __global__ void k_selftest_rcp(long long count, unsigned long long seed, unsigne
 
 // Gu-Eisenstat refreshed weights, one pole per thread, roots in order
 // (secular.cpp:288-313); replaces zA in place by sign(z)*sqrt(max(0,-w)).
+// The roots' (d_origin, tau, d_j) triples stream through shared memory in
+// tiles of kWin covering the CTA's window (one tile when it fits), in root
+// order, so the product order is the checker's.
 __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
-    __shared__ double s_d[kWin], s_tau[kWin];
-    __shared__ int s_org[kWin];
+    __shared__ double s_dorg[kWin], s_tau[kWin], s_dj[kWin];
     const int T = w.survPre[w.nnPre[n]];
     const int g0 = blockIdx.x * kSecBlock;
-    if (g0 >= T) return;
+    if (g0 >= T) return;  // uniform per CTA
     const Window win = cta_window(w, L, T);
-    if (win.fits) {
-        for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock) {
-            s_d[i] = w.dA[win.P0 + i];
-            s_tau[i] = w.tau[win.P0 + i];
-            s_org[i] = w.org[win.P0 + i];
-        }
-        __syncthreads();
-    }
     const int g = g0 + threadIdx.x;
-    if (g >= T) return;
-    const int m = w.aMerge[g];
-    if (L.mFlags[m] & kMergeRoot) return;
-    int ks, ke;
-    active_range(w, L, m, ks, ke);
-    const int i = g - ks, K = ke - ks;
-    const double* __restrict__ dA = win.fits ? s_d + (ks - win.P0) : w.dA + ks;
-    const double* __restrict__ tau = win.fits ? s_tau + (ks - win.P0) : w.tau + ks;
-    const int* __restrict__ org = win.fits ? s_org + (ks - win.P0) : w.org + ks;
-    const double di = dA[i];
+    bool act = g < T;
+    int ks = 0, K = 0, i = 0;
+    double di = 0.0;
+    if (act) {
+        const int m = w.aMerge[g];
+        if (L.mFlags[m] & kMergeRoot) act = false;
+        int ke;
+        active_range(w, L, m, ks, ke);
+        K = ke - ks;
+        i = g - ks;
+        di = w.dA[g];
+    }
     double prod = 1.0;
     unsigned minexp = 0x7ff00000u;
-    for (int j = 0; j < K; ++j) {
-        const double del = (di - dA[org[j]]) - tau[j];
-        const double dd = di - dA[j];
-        if (j != i) minexp = min(minexp, expfield(dd));
-        const double f = (j == i) ? del : del * rcp_nr(dd);
-        prod = prod * f;
+    for (int tlo = win.P0; tlo < win.P1; tlo += kWin) {
+        const int thi = min(tlo + kWin, win.P1);
+        __syncthreads();
+        for (int r = tlo + threadIdx.x; r < thi; r += kSecBlock) {
+            int rks, rke;
+            active_range(w, L, w.aMerge[r], rks, rke);
+            s_dorg[r - tlo] = w.dA[rks + w.org[r]];
+            s_tau[r - tlo] = w.tau[r];
+            s_dj[r - tlo] = w.dA[r];
+        }
+        __syncthreads();
+        if (act) {
+            const int jlo = max(ks, tlo), jhi = min(ks + K, thi);
+            for (int jg = jlo; jg < jhi; ++jg) {
+                const int t = jg - tlo;
+                const double del = (di - s_dorg[t]) - s_tau[t];
+                const double dd = di - s_dj[t];
+                const bool self = (jg - ks) == i;
+                if (!self) minexp = min(minexp, expfield(dd));
+                const double f = self ? del : del * rcp_nr(dd);
+                prod = prod * f;
+            }
+        }
     }
-    if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {  // exact redo (never for distinct scaled poles)
+    if (!act) return;
+    if (minexp < kRcpMinExp || (minexp == 0x7ff00000u && K > 1)) {  // exact redo (global memory)
+        const double* __restrict__ dA = w.dA + ks;
+        const double* __restrict__ tau = w.tau + ks;
+        const int* __restrict__ org = w.org + ks;
         prod = 1.0;
         for (int j = 0; j < K; ++j) {
             const double del = (di - dA[org[j]]) - tau[j];
@@ -723,55 +646,65 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
 
 // Parent boundary rows for root j: R_parent(:,j) = R_child y_j with
 // y = zhat/Delta_j / ||zhat/Delta_j|| streamed (never stored),
-// plus placement of lambda_j in the parent's ascending order.
+// plus placement of lambda_j in the parent's ascending order.  Poles (d, zhat,
+// r0, r1) stream through shared memory in tiles, in pole order.
 __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
     __shared__ double s_d[kWin], s_zh[kWin], s_r0[kWin], s_r1[kWin];
     const int T = w.survPre[w.nnPre[n]];
     const int g0 = blockIdx.x * kSecBlock;
-    if (g0 >= T) return;
+    if (g0 >= T) return;  // uniform per CTA
     const Window win = cta_window(w, L, T);
-    if (win.fits) {
-        for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock) {
-            s_d[i] = w.dA[win.P0 + i];
-            s_zh[i] = w.zA[win.P0 + i];
-            s_r0[i] = w.r0A[win.P0 + i];
-            s_r1[i] = w.r1A[win.P0 + i];
-        }
-        __syncthreads();
-    }
     const int g = g0 + threadIdx.x;
-    if (g >= T) return;
-    const int m = w.aMerge[g];
-    int ks, ke;
-    active_range(w, L, m, ks, ke);
-    const int K = ke - ks, j = g - ks;
-    const int off = L.mOff[m], size = L.mSize[m];
-    const bool is_root = L.mFlags[m] & kMergeRoot;
-    const int sh = ks - win.P0;
-    const double* __restrict__ dA = win.fits ? s_d + sh : w.dA + ks;
-    const double dorg = dA[w.org[g]];
-    const double tau = w.tau[g];
-    const double lam = dorg + tau;
-    // parent position: j + #{deflated <= lam} = j + #{D <= lam} - #{dA <= lam}
-    const int pos = j + count_leq(w.D + off, size, lam) - count_leq(dA, K, lam);
-    const int p = off + pos;
-    w.lam[p] = lam;
-    if (is_root) return;
-    const double* __restrict__ zh = win.fits ? s_zh + sh : w.zA + ks;
-    const double* __restrict__ r0 = win.fits ? s_r0 + sh : w.r0A + ks;
-    const double* __restrict__ r1 = win.fits ? s_r1 + sh : w.r1A + ks;
+    bool act = g < T;
+    int ks = 0, K = 0, p = 0;
+    double dorg = 0.0, tau = 0.0;
+    if (act) {
+        const int m = w.aMerge[g];
+        int ke;
+        active_range(w, L, m, ks, ke);
+        K = ke - ks;
+        const int j = g - ks;
+        const int off = L.mOff[m], size = L.mSize[m];
+        dorg = w.dA[ks + w.org[g]];
+        tau = w.tau[g];
+        const double lam = dorg + tau;
+        // parent position: j + #{deflated <= lam} = j + #{D <= lam} - #{dA <= lam}
+        const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + ks, K, lam);
+        p = off + pos;
+        w.lam[p] = lam;
+        if (L.mFlags[m] & kMergeRoot) act = false;
+    }
     double nn = 0.0, s0 = 0.0, s1 = 0.0;
     unsigned minexp = 0x7ff00000u;
+    for (int tlo = win.P0; tlo < win.P1; tlo += kWin) {
+        const int thi = min(tlo + kWin, win.P1);
+        __syncthreads();
+        for (int r = tlo + threadIdx.x; r < thi; r += kSecBlock) {
+            s_d[r - tlo] = w.dA[r];
+            s_zh[r - tlo] = w.zA[r];
+            s_r0[r - tlo] = w.r0A[r];
+            s_r1[r - tlo] = w.r1A[r];
+        }
+        __syncthreads();
+        if (act) {
+            const int ilo = max(ks, tlo) - tlo, ihi = min(ks + K, thi) - tlo;
 #pragma unroll 4
-    for (int i = 0; i < K; ++i) {
-        const double del = (dA[i] - dorg) - tau;
-        minexp = min(minexp, expfield(del));
-        const double y = zh[i] * rcp_nr(del);
-        nn = __fma_rn(y, y, nn);
-        s0 = __fma_rn(r0[i], y, s0);
-        s1 = __fma_rn(r1[i], y, s1);
+            for (int t = ilo; t < ihi; ++t) {
+                const double del = (s_d[t] - dorg) - tau;
+                minexp = min(minexp, expfield(del));
+                const double y = s_zh[t] * rcp_nr(del);
+                nn = __fma_rn(y, y, nn);
+                s0 = __fma_rn(s_r0[t], y, s0);
+                s1 = __fma_rn(s_r1[t], y, s1);
+            }
+        }
     }
+    if (!act) return;
     if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {  // exact redo; a zero delta is an error
+        const double* __restrict__ dA = w.dA + ks;
+        const double* __restrict__ zh = w.zA + ks;
+        const double* __restrict__ r0 = w.r0A + ks;
+        const double* __restrict__ r1 = w.r1A + ks;
         bool zero = false;
         nn = 0.0; s0 = 0.0; s1 = 0.0;
         for (int i = 0; i < K; ++i) {
@@ -860,6 +793,9 @@ __global__ void k_merge_runs(int n, const double* __restrict__ src, double* __re
 // launchers
 // ---------------------------------------------------------------------------
 static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+void launch_secular_tiled(cudaStream_t s, const Work& w, const LevelDev& L, int n,
+                          const SolveParams& prm);
 
 int selftest_rcp(long long count, unsigned long long seed, unsigned long long* host_bad) {
     unsigned long long* d;
@@ -954,6 +890,7 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
     k_surv_write<<<ntiles, kScanBlock, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_SURVWRITE);
     k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
+    launch_secular_tiled(s, w, L, n, prm);
     PMARK(BRGPU_K_SECULAR);
     int nl = 10;
     if (prm.zhat) {

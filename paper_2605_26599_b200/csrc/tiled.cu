@@ -1,0 +1,152 @@
+// tiled.cu -- large-K tier of the secular solver (Toeplitz / glued-Wilkinson
+// top levels, K up to n/2).
+//
+// Same chunking of roots as k_secular (kernels.cu); this kernel owns exactly
+// the chunks whose pole window does not fit in shared memory.  Every lane
+// still runs its own resumable RootSM (numerics.cuh) and refills from the CTA
+// queue, but evaluations are CTA-SYNCHRONOUS passes: the CTA streams the pole
+// window through shared memory in tiles of (d, z^2) pairs (double-buffered,
+// one coalesced load per tile per CTA instead of one L2 stream per warp) and
+// every lane with a pending evaluation accumulates the tile's intersection
+// with its merge, in pole order -- the checker's summation order, so results
+// are bit-identical to k_secular / oracle/br_oracle.c.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.hpp"
+#include "numerics.cuh"
+
+namespace brgpu {
+
+constexpr int kTiledThreads = 256;
+constexpr int kTile2 = 1024;           // (d, z^2) pairs per tile (16 KB, double-buffered)
+constexpr int kSecChunkBlock = 128;    // must match kSecBlock in kernels.cu (chunk formula)
+constexpr int kSecWinFit = 2048;       // must match kSecWinQ in kernels.cu
+
+__device__ __forceinline__ void tile_load(double2* dst, const double* __restrict__ d,
+                                          const double* __restrict__ z2, int lo, int hi) {
+    for (int i = lo + threadIdx.x; i < hi; i += kTiledThreads) dst[i - lo] = make_double2(d[i], z2[i]);
+}
+
+__global__ void __launch_bounds__(kTiledThreads, 2)
+k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
+    __shared__ double2 s_tile[2][kTile2];
+    __shared__ int s_next;
+    const int T = w.survPre[w.nnPre[n]];
+    const int R = max(kSecChunkBlock, (T + G - 1) / G);
+    // this kernel's grid covers the same G chunks; CTA b owns chunk b
+    const int c0 = blockIdx.x * R;
+    if (c0 >= T) return;
+    const int c1 = min(c0 + R, T);
+    int a0, a1, b0, b1;
+    {
+        const int m0 = w.aMerge[c0], m1 = w.aMerge[c1 - 1];
+        const int o0 = L.mOff[m0], o1 = L.mOff[m1];
+        a0 = w.survPre[w.nnPre[o0]];
+        a1 = w.survPre[w.nnPre[o0 + L.mSize[m0]]];
+        b0 = w.survPre[w.nnPre[o1]];
+        b1 = w.survPre[w.nnPre[o1 + L.mSize[m1]]];
+    }
+    (void)a1; (void)b0;
+    const int P0 = a0, P1 = b1;
+    if (P1 - P0 <= kSecWinFit) return;  // k_secular owns it
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+
+    RootSM st;
+    int g = -1, ks = 0;
+    bool exhausted = false;
+    unsigned long long evals = 0, terms = 0;
+    for (;;) {
+        while (g < 0 && !exhausted) {
+            const int q = atomicAdd(&s_next, 1);
+            if (c0 + q >= c1) { exhausted = true; break; }
+            g = c0 + q;
+            const int m = w.aMerge[g];
+            int ke;
+            const int off = L.mOff[m];
+            ks = w.survPre[w.nnPre[off]];
+            ke = w.survPre[w.nnPre[off + L.mSize[m]]];
+            const double rho = fabs(w.ew[off + L.mNL[m] - 1]);
+            rs_begin(st, ke - ks, g - ks, rho, PolesPtr{w.dA + ks}, w.zA[ks], Z2Ptr{w.z2A + ks});
+            if (st.phase == kRsDone) {
+                w.org[g] = st.org;
+                w.tau[g] = st.tau;
+                g = -1;
+            }
+        }
+        const bool need = g >= 0;
+        if (!__syncthreads_or(need)) break;
+        // one CTA-synchronous evaluation pass over the window
+        double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi = 0.0;
+        unsigned minexp = 0x7ff00000u;
+        const int K = need ? st.K : 0;
+        const int j = st.j;
+        const double dorg = st.dorg, tau = st.tau;
+        int buf = 0;
+        tile_load(s_tile[0], w.dA, w.z2A, P0, min(P0 + kTile2, P1));
+        for (int tlo = P0; tlo < P1; tlo += kTile2) {
+            const int thi = min(tlo + kTile2, P1);
+            __syncthreads();  // tile `buf` complete; previous readers of buf^1 done
+            if (thi < P1) tile_load(s_tile[buf ^ 1], w.dA, w.z2A, thi, min(thi + kTile2, P1));
+            if (need) {
+                const int ilo = max(ks, tlo), ihi = min(ks + K, thi);
+                const double2* __restrict__ tp = s_tile[buf] - tlo;
+#pragma unroll 4
+                for (int i = ilo; i < ihi; ++i) {
+                    const double2 dz = tp[i];
+                    const double del = (dz.x - dorg) - tau;
+                    minexp = min(minexp, expfield(del));
+                    const double r = rcp_nr(del);
+                    const double t = dz.y * r;
+                    sum += t;
+                    sum_abs += fabs(t);
+                    sum_d += t * r;
+                    if (i - ks == j) psi = sum_d;
+                }
+            }
+            buf ^= 1;
+        }
+        __syncthreads();
+        bool pole = false;
+        if (need) {
+            if (j >= K) psi = sum_d;
+            if (minexp < kRcpMinExp || minexp == 0x7ff00000u)  // rare: exact pass from global memory
+                pole = eval_pass_exact(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau, sum, sum_abs,
+                                       sum_d, psi);
+            Ev ev;
+            ev.f = 1.0 + st.rho * sum;
+            ev.fp = st.rho * sum_d;
+            ev.abs_sum = st.rho * sum_abs;
+            ev.psi = st.rho * psi;
+            ev.pole = pole;
+            ++evals;
+            terms += (unsigned long long)K;
+            rs_consume(st, ev, PolesPtr{w.dA + ks}, patched != 0);
+            if (st.phase == kRsDone || st.phase == kRsFail) {
+                if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                w.org[g] = st.org;
+                w.tau[g] = st.tau;
+                g = -1;
+            }
+        }
+    }
+    unsigned long long e = evals, t = terms;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    if ((threadIdx.x & 31) == 0 && e) {
+        atomicAdd(&w.counters[0], e);
+        atomicAdd(&w.counters[1], t);
+    }
+}
+
+void launch_secular_tiled(cudaStream_t s, const Work& w, const LevelDev& L, int n,
+                          const SolveParams& prm) {
+    k_secular_tiled<<<prm.sec_grid, kTiledThreads, 0, s>>>(w, L, n, prm.patched, prm.sec_grid);
+}
+
+}  // namespace brgpu
