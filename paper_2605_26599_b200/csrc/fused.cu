@@ -160,11 +160,27 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     __syncthreads();
 
     // ---- tolerance: max(|D|, |z|) per merge ---------------------------------
-    for (int i = tid; i < E; i += kFuseThreads) {
-        const int t = upper_index(S.mo, cnt, i);
-        const double zv = (i - S.mo[t] < S.mnl[t]) ? bhiIn[i] : bloIn[i];
-        const double v = fmax(fabs(lamIn[i]), fabs(zv));
-        atomicMax(&S.tolb[t], (unsigned long long)__double_as_longlong(v));
+    // (segmented warp max over consecutive elements, one shared atomic per
+    // merge segment: 64-bit shared atomics are CAS loops on sm_100a)
+    for (int b0 = 0; b0 < E; b0 += kFuseThreads) {
+        const int i = b0 + tid;
+        const bool valid = i < E;
+        int t = -1;
+        unsigned long long v = 0ULL;
+        if (valid) {
+            t = upper_index(S.mo, cnt, i);
+            const double zv = (i - S.mo[t] < S.mnl[t]) ? bhiIn[i] : bloIn[i];
+            v = (unsigned long long)__double_as_longlong(fmax(fabs(lamIn[i]), fabs(zv)));
+        }
+        const int lane = tid & 31;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long v2 = __shfl_down_sync(0xffffffffu, v, off);
+            const int t2 = __shfl_down_sync(0xffffffffu, t, off);
+            if (lane + off < 32 && t2 == t && v2 > v) v = v2;
+        }
+        const int tp = __shfl_up_sync(0xffffffffu, t, 1);
+        if (valid && (lane == 0 || tp != t)) atomicMax(&S.tolb[t], v);
     }
     __syncthreads();
 
@@ -303,9 +319,14 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
                 }
             }
         }
-        if (evals) {
-            atomicAdd(&S.evals, evals);
-            atomicAdd(&S.terms, terms);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            evals += __shfl_xor_sync(0xffffffffu, evals, o);
+            terms += __shfl_xor_sync(0xffffffffu, terms, o);
+        }
+        if ((tid & 31) == 0 && evals) {
+            atomicAdd(&w.counters[0], evals);
+            atomicAdd(&w.counters[1], terms);
         }
     }
     __syncthreads();
@@ -412,11 +433,6 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     if (traceOut && tid < cnt) {
         traceOut[2 * (m0 + tid)] = S.nnPre[S.mo[tid] + S.ms[tid]] - S.nnPre[S.mo[tid]];
         traceOut[2 * (m0 + tid) + 1] = S.kS[tid + 1] - S.kS[tid];
-    }
-    __syncthreads();
-    if (tid == 0 && S.evals) {
-        atomicAdd(&w.counters[0], S.evals);
-        atomicAdd(&w.counters[1], S.terms);
     }
 }
 
