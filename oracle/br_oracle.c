@@ -277,7 +277,7 @@ static ev_t eval_shifted(int k, const double* d, const double* z, double rho, in
                          double tau, int jsplit, int ref) {
     ev_t r = {0.0, 0.0, 0.0, 0.0, 0};
     const double dorg = d[org];
-    double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi_d = 0.0;
+    double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi_d = 0.0, psum = 0.0;
     for (int i = 0; i < k; ++i) {
         const double del = (d[i] - dorg) - tau;
         if (del == 0.0) { r.pole = 1; return r; }
@@ -292,13 +292,15 @@ static ev_t eval_shifted(int k, const double* d, const double* z, double rho, in
             dterm = term * rr;
         }
         sum += term;
-        sum_abs += fabs(term);
+        if (ref) sum_abs += fabs(term);
         sum_d += dterm;
-        if (i <= jsplit) psi_d += dterm;
+        if (i <= jsplit) { psi_d += dterm; psum = sum; }
     }
     r.f = 1.0 + rho * sum;
     r.fp = rho * sum_d;
-    r.abs_sum = rho * sum_abs;
+    /* GPU arithmetic: the bracket fixes the term signs (t_i < 0 for i <= j,
+     * t_i > 0 for i > j), so sum|t| = sum t - 2 * sum_{i<=j} t. */
+    r.abs_sum = ref ? rho * sum_abs : rho * (sum - 2.0 * psum);
     r.psi = rho * psi_d;
     return r;
 }
@@ -316,6 +318,8 @@ int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
     const int last = (j == k - 1);
     int org;
     double lo, hi, other_gap = 0.0;
+    int reuse = 0;
+    ev_t mid_ev = {0.0, 0.0, 0.0, 0.0, 0};
     if (last) {
         double zsq = 0.0;
         for (int i = 0; i < k; ++i) zsq += z[i] * z[i];
@@ -331,12 +335,22 @@ int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
         } else {
             org = j + 1; lo = -(d[j + 1] - d[j]); hi = 0.0; other_gap = d[j] - d[j + 1];
         }
+        /* GPU arithmetic: the first iterate (the bracket midpoint) is the probe
+         * point in either origin; reuse its evaluation (f, f', psi' depend on
+         * lambda only) instead of evaluating it again. */
+        if (!ref) { reuse = 1; mid_ev = mid; }
     }
     double tau = 0.5 * (lo + hi);
     int converged = 0;
     for (int iter = 0; iter < 400; ++iter) {
-        ev_t ev = eval_shifted(k, d, z, rho, org, tau, j, ref);
-        ++ne;
+        ev_t ev;
+        if (reuse) {
+            ev = mid_ev;
+            reuse = 0;
+        } else {
+            ev = eval_shifted(k, d, z, rho, org, tau, j, ref);
+            ++ne;
+        }
         if (ev.pole) {
             tau = 0.5 * (lo + hi);
             ev = eval_shifted(k, d, z, rho, org, tau, j, ref);

@@ -331,6 +331,13 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     }
     __syncthreads();
 
+    double* sDorg = S.Z;  // d[origin] per root (lambda = dorg + tau); S.Z is dead after compaction
+    for (int g = tid; g < T; g += kFuseThreads) {
+        const int t = upper_index(S.kS, cnt, g);
+        sDorg[g] = pairs[S.kS[t] + S.org[g]].x;
+    }
+    __syncthreads();
+
     // ---- Gu-Eisenstat refreshed weights (non-root merges) --------------------
     if (prm.zhat) {
         for (int g = tid; g < T; g += kFuseThreads) {
@@ -340,8 +347,9 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
             const double di = pairs[g].x;
             double prod = 1.0;
             unsigned minexp = 0x7ff00000u;
+#pragma unroll 4
             for (int j = 0; j < K; ++j) {
-                const double del = (di - pairs[ks + S.org[ks + j]].x) - S.tau[ks + j];
+                const double del = (di - sDorg[ks + j]) - S.tau[ks + j];
                 const double dd = di - pairs[ks + j].x;
                 if (j != i) minexp = min(minexp, expfield(dd));
                 const double f = (j == i) ? del : del * rcp_nr(dd);
@@ -366,7 +374,7 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
         const int t = upper_index(S.kS, cnt, g);
         const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
         const int off = S.mo[t], size = S.ms[t];
-        const double dorg = pairs[ks + S.org[g]].x;
+        const double dorg = sDorg[g];
         const double tau = S.tau[g];
         const double lam = dorg + tau;
         // #{dA <= lam} over the merge's active poles
@@ -418,7 +426,7 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
         int lo = 0, hi = K;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            const double lj = pairs[ks + S.org[ks + mid]].x + S.tau[ks + mid];
+            const double lj = sDorg[ks + mid] + S.tau[ks + mid];
             if (lj < v) lo = mid + 1; else hi = mid;
         }
         const int p = base + off + tt + lo;
@@ -445,6 +453,7 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 }
 
 size_t fused_smem_bytes() { return sizeof(FuseSmem); }
+static_assert(sizeof(FuseSmem) <= 113 * 1024, "two fused CTAs must fit one SM (227 KB)");
 
 void init_fused_attributes() {
     cudaFuncSetAttribute(k_level_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FuseSmem));

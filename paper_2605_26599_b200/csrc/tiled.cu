@@ -79,7 +79,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
         const bool need = g >= 0;
         if (!__syncthreads_or(need)) break;
         // one CTA-synchronous evaluation pass over the window
-        double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi = 0.0;
+        double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi = 0.0, psum = 0.0;
         unsigned minexp = 0x7ff00000u;
         const int K = need ? st.K : 0;
         const int j = st.j;
@@ -101,9 +101,8 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
                     const double r = rcp_nr(del);
                     const double t = dz.y * r;
                     sum += t;
-                    sum_abs += fabs(t);
                     sum_d += t * r;
-                    if (i - ks == j) psi = sum_d;
+                    if (i - ks == j) { psi = sum_d; psum = sum; }
                 }
             }
             buf ^= 1;
@@ -111,7 +110,8 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
         __syncthreads();
         bool pole = false;
         if (need) {
-            if (j >= K) psi = sum_d;
+            if (j >= K) { psi = sum_d; psum = sum; }
+            sum_abs = sum - 2.0 * psum;  // term signs are fixed by the bracket
             if (minexp < kRcpMinExp || minexp == 0x7ff00000u)  // rare: exact pass from global memory
                 pole = eval_pass_exact(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau, sum, sum_abs,
                                        sum_d, psi);
