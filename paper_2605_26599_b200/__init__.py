@@ -131,6 +131,7 @@ class BrOptions:
     patched_stop: bool = True
     use_graph: bool = True
     subtree: bool = True
+    virtual_ranks: int = 1  # >1: run the multi-GPU decomposition on this device (test mode)
 
 
 @dataclass
@@ -164,14 +165,22 @@ def workspace_query(n: int) -> tuple[int, int]:
 class Solver:
     """One handle = one device + one stream (handles are independent; use one per thread)."""
 
-    def __init__(self, device: int = 0, options: BrOptions | None = None):
+    def __init__(self, device: int = 0, options: BrOptions | None = None, *, rank: int = 0,
+                 nranks: int = 1, nccl_id: bytes | None = None):
         self._lib = _native.lib()
         h = C.c_void_p()
-        rc = self._lib.brgpu_create(C.byref(h), int(device))
+        if nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise InvalidArgument("distributed Solver needs the 128-byte NCCL unique id")
+            buf = C.create_string_buffer(nccl_id, 128)
+            rc = self._lib.brgpu_create_distributed(C.byref(h), int(device), int(rank), int(nranks), buf)
+        else:
+            rc = self._lib.brgpu_create(C.byref(h), int(device))
         if rc:
             _raise(rc, f"brgpu_create(device={device}): {self._lib.brgpu_status_string(rc).decode()}")
         self._h = h
         self.device = device
+        self.rank, self.nranks = rank, nranks
         self.set_options(options or BrOptions())
 
     # options --------------------------------------------------------------
@@ -181,6 +190,8 @@ class Solver:
         self._opt(_native.OPT_PATCHED_STOP, int(o.patched_stop))
         self._opt(_native.OPT_USE_GRAPH, int(o.use_graph))
         self._opt(_native.OPT_SUBTREE, int(o.subtree))
+        if self.nranks == 1:
+            self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o
 
     def _opt(self, k: int, v: int) -> None:
@@ -314,6 +325,47 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be shared with the other ranks."""
+    buf = C.create_string_buffer(128)
+    rc = _native.lib().brgpu_nccl_unique_id(buf)
+    if rc:
+        _raise(rc, "brgpu_nccl_unique_id")
+    return buf.raw
+
+
+def distributed_solver(device: int | None = None, options: BrOptions | None = None) -> Solver:
+    """One Solver per process over torch.distributed's world (torchrun): the NCCL id
+    is created on rank 0 and broadcast with torch.distributed."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    if device is None:
+        import torch
+        device = torch.cuda.current_device()
+    return Solver(device, options, rank=rank, nranks=world, nccl_id=obj[0])
+
+
+def plan_owned(n: int, nranks: int, leaf_cutoff: int = 25, bstart=None) -> list[list[tuple[int, int]]]:
+    """Host-only: the [off, off+len) ranges each rank solves before the exchange."""
+    import numpy as np
+    cap = 4096
+    counts = (C.c_int32 * nranks)()
+    ranges = (C.c_int32 * (2 * cap * nranks))()
+    b = None
+    nblk = 0
+    if bstart is not None:
+        b = np.ascontiguousarray(bstart, dtype=np.int32)
+        nblk = len(b) - 1
+    rc = _native.lib().brgpu_plan_owned(int(n), int(leaf_cutoff), int(nranks),
+                                        b.ctypes.data if b is not None else None, nblk, counts, ranges, cap)
+    if rc:
+        _raise(rc, "brgpu_plan_owned")
+    return [[(ranges[2 * (k * cap + q)], ranges[2 * (k * cap + q) + 1]) for q in range(counts[k])]
+            for k in range(nranks)]
 
 
 _default: Solver | None = None

@@ -19,6 +19,7 @@ OPT_ZHAT = 2
 OPT_PATCHED_STOP = 3
 OPT_USE_GRAPH = 4
 OPT_SUBTREE = 5
+OPT_VIRTUAL_RANKS = 6
 
 
 class Stats(C.Structure):
@@ -45,7 +46,7 @@ EXPORTS = [
     "brgpu_get_ledger", "brgpu_eigvals", "brgpu_eigvals_device", "brgpu_eigvals_batched",
     "brgpu_eigvals_batched_device", "brgpu_get_stats", "brgpu_set_trace", "brgpu_get_trace",
     "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_kernel_class_name", "brgpu_selftest_rcp",
-    "brgpu_version",
+    "brgpu_nccl_unique_id", "brgpu_create_distributed", "brgpu_plan_owned", "brgpu_version",
 ]
 
 NCLASS = 17
@@ -90,5 +91,9 @@ def lib() -> C.CDLL:
     L.brgpu_kernel_class_name.argtypes = [C.c_int]
     L.brgpu_kernel_class_name.restype = C.c_char_p
     L.brgpu_selftest_rcp.argtypes = [hp, C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.brgpu_nccl_unique_id.argtypes = [C.c_void_p]
+    L.brgpu_create_distributed.argtypes = [C.POINTER(hp), C.c_int, C.c_int, C.c_int, C.c_void_p]
+    L.brgpu_plan_owned.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32]
     _lib = L
     return L

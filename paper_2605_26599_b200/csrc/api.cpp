@@ -10,6 +10,8 @@
 //     (merge_tree.cpp:78-92), leaf tasks, per-level merge tables;
 //   * the launch sequence (optionally replayed as one CUDA graph).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is dlopen'ed (torch's copy when already loaded)
 
 #include <algorithm>
 #include <cstdio>
@@ -93,7 +95,11 @@ struct Plan {
     std::vector<int> mOff, mSize, mNL, mFlags, mLevel;
     std::vector<int> tileFirst;
     std::vector<int> gFirst, gCount;  // fused groups (level-local first merge, count)
-    std::vector<LevelHost> levels;
+    std::vector<LevelHost> levels;    // phase 1: merges owned by this rank (all, when nranks == 1)
+    std::vector<LevelHost> levels2;   // phase 2: top merges shared by all ranks (after the exchange)
+    int nranks = 1, rank = 0;
+    // owned[k] = ranges [off, off+len) whose phase-1 state rank k computes and broadcasts
+    std::vector<std::vector<std::pair<int, int>>> owned;
     std::vector<std::vector<int>> runPasses;  // run boundaries before each merge pass
     int height = 0;
     int maxM = 0;
@@ -152,6 +158,11 @@ struct Handle {
     uint64_t bufgen = 1;  // bumped whenever a buffer baked into a graph moves
     brgpu_stats stats{};
     std::vector<brgpu_trace> traceRecs;
+    // distribution: one process per GPU over NCCL, or P virtual ranks on this device
+    int nranks = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    int virt = 1;
+    std::vector<std::unique_ptr<Handle>> subs;
 };
 
 int fail(Handle* h, int code, const std::string& msg) {
@@ -170,78 +181,64 @@ int fail(Handle* h, int code, const std::string& msg) {
 // planning
 // ---------------------------------------------------------------------------
 struct NodeRec {
-    int off, size, nl, level, root;
+    int off, size, nl, level, root, owner;  // owner: rank, or -1 for the shared top of a split block
 };
 
-int build_node(int off, int size, int cutoff, bool root, std::vector<NodeRec>& internal,
-               std::vector<std::pair<int, int>>& leaves) {
+struct LeafRec {
+    int off, size, owner;
+};
+
+// Split tree of one block (merge_tree.cpp:34-60).  For a block split across
+// ranks, nodes at depth < D are "top" (owner -1, all ranks after the
+// exchange) and the depth-D nodes, left to right, are owned by ranks 0..2^D-1
+// together with their whole subtrees.
+int build_node(int off, int size, int cutoff, bool root, int depth, int D, int owner, int* nextOwner,
+               std::vector<NodeRec>& internal, std::vector<LeafRec>& leaves,
+               std::vector<std::pair<int, int>>* ownedBig) {
+    if (depth == D && owner < 0 && nextOwner) {
+        owner = (*nextOwner)++;
+        if (ownedBig) ownedBig[owner].emplace_back(off, size);
+    }
     if (size <= cutoff) {
-        leaves.emplace_back(off, size);
+        leaves.push_back({off, size, owner});
         return 0;
     }
     const int nl = size / 2;
     const int idx = (int)internal.size();
-    internal.push_back({off, size, nl, 0, root ? 1 : 0});
-    const int ll = build_node(off, nl, cutoff, false, internal, leaves);
-    const int rl = build_node(off + nl, size - nl, cutoff, false, internal, leaves);
+    internal.push_back({off, size, nl, 0, root ? 1 : 0, owner});
+    const int ll = build_node(off, nl, cutoff, false, depth + 1, D, owner, nextOwner, internal, leaves, ownedBig);
+    const int rl = build_node(off + nl, size - nl, cutoff, false, depth + 1, D, owner, nextOwner, internal,
+                              leaves, ownedBig);
     const int lev = 1 + std::max(ll, rl);
     internal[idx].level = lev;
     return lev;
 }
 
-std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
-                                const std::vector<int>& segs, bool fuse) {
-    auto p = std::make_unique<Plan>();
-    p->n = n;
-    p->cutoff = cutoff;
-    p->bstart = bstart;
-    p->segs = segs;
-    std::vector<NodeRec> internal;
-    std::vector<std::pair<int, int>> leaves;
-    const int nblk = (int)bstart.size() - 1;
-    for (int b = 0; b < nblk; ++b) {
-        const int off = bstart[b], sz = bstart[b + 1] - off;
-        if (sz <= cutoff) {
-            p->tOff.push_back(off);
-            p->tSize.push_back(sz);
-            p->tFlags.push_back(1);  // values only
-            p->maxLeaf = std::max(p->maxLeaf, sz);
-            continue;
-        }
-        const int h = build_node(off, sz, cutoff, true, internal, leaves);
-        p->height = std::max(p->height, h);
-    }
-    for (auto& lf : leaves) {
-        p->tOff.push_back(lf.first);
-        p->tSize.push_back(lf.second);
-        p->tFlags.push_back(0);
-        p->maxLeaf = std::max(p->maxLeaf, lf.second);
-    }
-    for (auto& nd : internal) p->cutPos.push_back(nd.off + nd.nl - 1);
-    // merges grouped by level, offset order
-    std::stable_sort(internal.begin(), internal.end(), [](const NodeRec& a, const NodeRec& b) {
+// Level tables of a set of merges (grouped by level, offset order) appended to
+// the plan's merge arrays; fused SMEM groups where every merge of the level fits.
+void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<LevelHost>& out) {
+    std::stable_sort(nodes.begin(), nodes.end(), [](const NodeRec& a, const NodeRec& b) {
         return a.level != b.level ? a.level < b.level : a.off < b.off;
     });
-    const int ntiles = (n + kTile - 1) / kTile;
+    const int ntiles = (p->n + kTile - 1) / kTile;
     size_t i = 0;
-    while (i < internal.size()) {
-        const int lev = internal[i].level;
+    while (i < nodes.size()) {
+        const int lev = nodes[i].level;
         LevelHost L;
         L.level = lev;
         L.m0 = (int)p->mOff.size();
         L.tile0 = (int)p->tileFirst.size();
         size_t j = i;
-        while (j < internal.size() && internal[j].level == lev) {
-            p->mOff.push_back(internal[j].off);
-            p->mSize.push_back(internal[j].size);
-            p->mNL.push_back(internal[j].nl);
-            p->mFlags.push_back(internal[j].root ? kMergeRoot : 0);
+        while (j < nodes.size() && nodes[j].level == lev) {
+            p->mOff.push_back(nodes[j].off);
+            p->mSize.push_back(nodes[j].size);
+            p->mNL.push_back(nodes[j].nl);
+            p->mFlags.push_back(nodes[j].root ? kMergeRoot : 0);
             p->mLevel.push_back(lev);
             ++j;
         }
         L.M = (int)(j - i);
         p->maxM = std::max(p->maxM, L.M);
-        // fused SMEM tier when every merge of the level fits a group
         int maxSize = 0;
         for (int q = 0; q < L.M; ++q) maxSize = std::max(maxSize, p->mSize[L.m0 + q]);
         L.fused = fuse && maxSize <= kFuseMaxElems;
@@ -270,9 +267,78 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
             while (m < L.M && (long long)p->mOff[L.m0 + m] + p->mSize[L.m0 + m] <= start) ++m;
             p->tileFirst.push_back(m);
         }
-        p->levels.push_back(L);
+        out.push_back(L);
         i = j;
     }
+}
+
+// Plan of rank `rank` out of `nranks` (1: the whole solve).  Blocks of at
+// least 2^D * 2(cutoff+1) elements (D = floor(log2 nranks)) are split by
+// subtree; smaller blocks go to ranks in contiguous chunks of the total size.
+std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
+                                const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0) {
+    auto p = std::make_unique<Plan>();
+    p->n = n;
+    p->cutoff = cutoff;
+    p->bstart = bstart;
+    p->segs = segs;
+    p->nranks = nranks;
+    p->rank = rank;
+    p->owned.assign((size_t)nranks, {});
+    int D = 0;
+    while ((2 << D) <= nranks) ++D;
+    const int Peff = 1 << D;
+    const long long bigMin = (long long)Peff * 2 * (cutoff + 1);
+    std::vector<NodeRec> internal;
+    std::vector<LeafRec> leaves;
+    const int nblk = (int)bstart.size() - 1;
+    long long smallTotal = 0;
+    if (nranks > 1)
+        for (int b = 0; b < nblk; ++b) {
+            const int sz = bstart[b + 1] - bstart[b];
+            if (sz < bigMin) smallTotal += sz;
+        }
+    long long smallSeen = 0;
+    for (int b = 0; b < nblk; ++b) {
+        const int off = bstart[b], sz = bstart[b + 1] - off;
+        const bool big = nranks > 1 && sz >= bigMin;
+        int owner = 0;  // small blocks: contiguous chunks by cumulative size
+        if (nranks > 1 && !big) {
+            owner = (int)std::min<long long>(nranks - 1, smallTotal ? smallSeen * nranks / smallTotal : 0);
+            smallSeen += sz;
+            auto& ow = p->owned[(size_t)owner];
+            if (!ow.empty() && ow.back().first + ow.back().second == off) ow.back().second += sz;
+            else ow.emplace_back(off, sz);
+        }
+        if (sz <= cutoff) {
+            if (owner == rank || nranks == 1) {
+                p->tOff.push_back(off);
+                p->tSize.push_back(sz);
+                p->tFlags.push_back(1);  // values only
+                p->maxLeaf = std::max(p->maxLeaf, sz);
+            }
+            continue;
+        }
+        int next = 0;
+        const int h = build_node(off, sz, cutoff, true, 0, big ? D : -1, big ? -1 : owner,
+                                 big ? &next : nullptr, internal, leaves, big ? p->owned.data() : nullptr);
+        p->height = std::max(p->height, h);
+    }
+    for (auto& lf : leaves) {
+        if (nranks > 1 && lf.owner != rank) continue;
+        p->tOff.push_back(lf.off);
+        p->tSize.push_back(lf.size);
+        p->tFlags.push_back(0);
+        p->maxLeaf = std::max(p->maxLeaf, lf.size);
+    }
+    for (auto& nd : internal) p->cutPos.push_back(nd.off + nd.nl - 1);  // prepare is full on every rank
+    std::vector<NodeRec> mine, top;
+    for (auto& nd : internal) {
+        if (nranks == 1 || nd.owner == rank) mine.push_back(nd);
+        else if (nd.owner < 0) top.push_back(nd);
+    }
+    add_levels(p.get(), mine, fuse, p->levels);
+    add_levels(p.get(), top, fuse, p->levels2);
     // final merge passes: runs = blocks, merged pairwise inside each segment;
     // a segment with an odd run count gets an empty partner so that pairs
     // (2k, 2k+1) of a pass table never straddle segments.
@@ -408,17 +474,11 @@ int status_message(Handle* h, int st) {
     }
 }
 
-int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
+void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* launches, Prof* prof) {
     cudaStream_t s = h->stream;
-    if (prof) prof_mark(prof, (void*)s, -1);
     const int n = p->n;
-    const int nblk = (int)p->bstart.size() - 1;
-    launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
-                   p->d_cut, launches, prof);
-    launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
-                  launches, prof);
     SolveParams prm{n, h->zhat, h->patched, h->tol_scale, h->sec_grid};
-    for (const LevelHost& lh : p->levels) {
+    for (const LevelHost& lh : levels) {
         LevelDev L;
         L.mOff = p->d_mOff + lh.m0;
         L.mSize = p->d_mSize + lh.m0;
@@ -435,8 +495,28 @@ int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
             if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
         }
     }
+}
+
+// Stage A: scale + cuts (full), this rank's leaves and phase-1 merges.
+void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
+    cudaStream_t s = h->stream;
+    if (prof) prof_mark(prof, (void*)s, -1);
+    const int n = p->n;
+    const int nblk = (int)p->bstart.size() - 1;
+    launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
+                   p->d_cut, launches, prof);
+    launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
+                  launches, prof);
+    run_levels(h, p, p->levels, launches, prof);
+}
+
+// Stage B: shared top merges, rescale, cross-block merge passes.
+void run_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
+    cudaStream_t s = h->stream;
+    const int n = p->n;
+    const int nblk = (int)p->bstart.size() - 1;
+    run_levels(h, p, p->levels2, launches, prof);
     launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
-    // cross-block merge passes (ping-pong lam <-> D), result back in lam
     double* src = h->w.lam;
     double* dst = h->w.D;
     for (size_t q = 0; q < p->runPasses.size(); ++q) {
@@ -444,9 +524,135 @@ int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
                           prof);
         std::swap(src, dst);
     }
-    if (src != h->w.lam) {
-        cudaMemcpyAsync(h->w.lam, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    if (src != h->w.lam) cudaMemcpyAsync(h->w.lam, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+}
+
+int exchange_nccl(Handle* h, Plan* p);
+
+int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
+    run_stage_a(h, p, launches, prof);
+    if (p->nranks > 1) {
+        const int r = exchange_nccl(h, p);
+        if (r) return r;
     }
+    run_stage_b(h, p, launches, prof);
+    return BRGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL (dlopen'ed) and the phase-1 -> phase-2 exchange
+// ---------------------------------------------------------------------------
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) return a;
+        a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+        a.CommInitRank = (decltype(a.CommInitRank))dlsym(lib, "ncclCommInitRank");
+        a.CommDestroy = (decltype(a.CommDestroy))dlsym(lib, "ncclCommDestroy");
+        a.Broadcast = (decltype(a.Broadcast))dlsym(lib, "ncclBroadcast");
+        a.GroupStart = (decltype(a.GroupStart))dlsym(lib, "ncclGroupStart");
+        a.GroupEnd = (decltype(a.GroupEnd))dlsym(lib, "ncclGroupEnd");
+        a.GetErrorString = (decltype(a.GetErrorString))dlsym(lib, "ncclGetErrorString");
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Broadcast && a.GroupStart &&
+               a.GroupEnd && a.GetErrorString;
+        return a;
+    }();
+    return api;
+}
+
+// Every rank ends phase 1 with the state (lam, blo, bhi) of the ranges it
+// owns; one grouped in-place broadcast per owned range replicates the full
+// state on all ranks for the shared top merges.
+int exchange_nccl(Handle* h, Plan* p) {
+    NcclApi& N = nccl_api();
+    if (!h->comm || !N.ok) return fail(h, BRGPU_ERR_NCCL, "distributed plan without an NCCL communicator");
+    double* arrs[3] = {h->w.lam, h->w.blo, h->w.bhi};
+    ncclResult_t r = N.GroupStart();
+    for (int k = 0; k < p->nranks && r == ncclSuccess; ++k)
+        for (const auto& rg : p->owned[(size_t)k])
+            for (double* a : arrs) {
+                r = N.Broadcast(a + rg.first, a + rg.first, (size_t)rg.second, ncclDouble, k, h->comm, h->stream);
+                if (r != ncclSuccess) break;
+            }
+    const ncclResult_t r2 = N.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(h, BRGPU_ERR_NCCL, std::string("ncclBroadcast: ") + N.GetErrorString(r != ncclSuccess ? r : r2));
+    return BRGPU_OK;
+}
+
+int ensure_buf_sizes(Handle* h, Plan* p);
+
+// P virtual ranks on this device (test mode): each runs its own phase-1 plan
+// in its own workspace; the exchange is device copies; phase 2 on rank 0.
+// Bitwise identical to the single-rank solve by construction (tested).
+int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::vector<int>& segs) {
+    const int P = h->virt;
+    cudaStream_t s = h->stream;
+    while ((int)h->subs.size() < P) {
+        auto sub = std::make_unique<Handle>();
+        sub->device = h->device;
+        sub->sms = h->sms;
+        sub->stream = h->stream;
+        h->subs.push_back(std::move(sub));
+    }
+    std::vector<std::unique_ptr<Plan>> plans;
+    for (int k = 0; k < P; ++k) {
+        Handle* u = h->subs[(size_t)k].get();
+        u->leaf_cutoff = h->leaf_cutoff; u->zhat = h->zhat; u->patched = h->patched;
+        u->use_graph = 0; u->subtree = h->subtree; u->trace = 0; u->tol_scale = h->tol_scale;
+        u->sec_grid = h->sec_grid;
+        if (int r = ensure_work(u, n)) return fail(h, r, u->err);
+        u->w.status = h->w.status;
+        u->w.counters = h->w.counters;
+        CUDA_TRY(h, cudaMemcpyAsync(u->w.dw, h->w.dw, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(h, cudaMemcpyAsync(u->w.ew, h->w.ew, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        plans.push_back(make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, P, k));
+        if (int r = upload_plan(u, plans.back().get())) return fail(h, r, u->err);
+        if (int r = ensure_buf_sizes(u, plans.back().get())) return fail(h, r, u->err);
+        CUDA_TRY(h, cudaMemsetAsync(u->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
+        int launches = 0;
+        run_stage_a(u, plans.back().get(), &launches, nullptr);
+    }
+    for (int k = 0; k < P; ++k)
+        for (const auto& rg : plans[(size_t)k]->owned[(size_t)k])
+            for (int j = 0; j < P; ++j) {
+                if (j == k) continue;
+                Handle* a = h->subs[(size_t)k].get();
+                Handle* b = h->subs[(size_t)j].get();
+                const size_t bytes = sizeof(double) * (size_t)rg.second;
+                CUDA_TRY(h, cudaMemcpyAsync(b->w.lam + rg.first, a->w.lam + rg.first, bytes, cudaMemcpyDeviceToDevice, s));
+                CUDA_TRY(h, cudaMemcpyAsync(b->w.blo + rg.first, a->w.blo + rg.first, bytes, cudaMemcpyDeviceToDevice, s));
+                CUDA_TRY(h, cudaMemcpyAsync(b->w.bhi + rg.first, a->w.bhi + rg.first, bytes, cudaMemcpyDeviceToDevice, s));
+            }
+    int launches = 0;
+    run_stage_b(h->subs[0].get(), plans[0].get(), &launches, nullptr);
+    CUDA_TRY(h, cudaMemcpyAsync(h->w.lam, h->subs[0]->w.lam, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
+    for (auto& pl : plans) free_plan(pl.get());
+    h->stats.n = n;
+    h->stats.blocks = (int)bstart.size() - 1;
+    h->stats.graph_replayed = 0;
+    return BRGPU_OK;
+}
+
+int ensure_buf_sizes(Handle* h, Plan* p) {
+    if (int r = ensure_buf(h, h->sbits, h->sbitsCap, (int64_t)p->bstart.size())) return r;
+    if (int r = ensure_buf(h, h->mTol, h->mTolCap, std::max(p->maxM, 1))) return r;
+    if (h->trace)
+        if (int r = ensure_buf(h, h->traceBuf, h->traceCap, 2 * (int64_t)std::max<size_t>(p->mOff.size(), 1))) return r;
     return BRGPU_OK;
 }
 
@@ -474,18 +680,16 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
         }
         bstart.push_back(n);
     }
+    if (h->virt > 1) return solve_virtual(h, n, bstart, segs);
     Plan* p = h->plan.get();
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs) {
         if (h->plan) free_plan(h->plan.get());
-        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0);
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, h->nranks, h->rank);
         p = h->plan.get();
         int r = upload_plan(h, p);
         if (r) return r;
     }
-    if (int r = ensure_buf(h, h->sbits, h->sbitsCap, (int64_t)bstart.size())) return r;
-    if (int r = ensure_buf(h, h->mTol, h->mTolCap, std::max(p->maxM, 1))) return r;
-    if (h->trace)
-        if (int r = ensure_buf(h, h->traceBuf, h->traceCap, 2 * (int64_t)std::max<size_t>(p->mOff.size(), 1))) return r;
+    if (int r = ensure_buf_sizes(h, p)) return r;
     CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 4, s));
     int launches = 0;
@@ -652,6 +856,16 @@ int brgpu_destroy(brgpu_handle* hh) {
     Handle* h = &hh->h;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto& u : h->subs) {
+        if (u->plan) free_plan(u->plan.get());
+        free_work(u.get());
+        if (u->sbits) cudaFree(u->sbits);
+        if (u->mTol) cudaFree(u->mTol);
+        if (u->traceBuf) cudaFree(u->traceBuf);
+    }
+    h->subs.clear();
+    if (h->comm && nccl_api().ok) nccl_api().CommDestroy(h->comm);
+    h->comm = nullptr;
     if (h->plan) free_plan(h->plan.get());
     free_work(h);
     if (h->sbits) cudaFree(h->sbits);
@@ -682,6 +896,11 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
         case BRGPU_OPT_PATCHED_STOP: h->patched = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
         case BRGPU_OPT_USE_GRAPH: h->use_graph = v != 0; return BRGPU_OK;
         case BRGPU_OPT_SUBTREE: h->subtree = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        case BRGPU_OPT_VIRTUAL_RANKS:
+            if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
+            if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
+            h->virt = (int)v;
+            return BRGPU_OK;
         default: return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "unknown option");
     }
 }
@@ -695,6 +914,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_PATCHED_STOP: *v = h->patched; return BRGPU_OK;
         case BRGPU_OPT_USE_GRAPH: *v = h->use_graph; return BRGPU_OK;
         case BRGPU_OPT_SUBTREE: *v = h->subtree; return BRGPU_OK;
+        case BRGPU_OPT_VIRTUAL_RANKS: *v = h->virt; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }
 }
@@ -852,6 +1072,56 @@ int brgpu_selftest_rcp(brgpu_handle* hh, int64_t count, uint64_t seed, uint64_t*
     const int r = brgpu::selftest_rcp(count, seed, &bad);
     *mismatches = bad;
     return r;
+}
+
+int brgpu_nccl_unique_id(void* out) {
+    NcclApi& N = nccl_api();
+    if (!out) return BRGPU_ERR_INVALID_ARGUMENT;
+    if (!N.ok) return BRGPU_ERR_NCCL;
+    ncclUniqueId id;
+    if (N.GetUniqueId(&id) != ncclSuccess) return BRGPU_ERR_NCCL;
+    std::memcpy(out, &id, sizeof(id));
+    return BRGPU_OK;
+}
+
+int brgpu_create_distributed(brgpu_handle** out, int device, int rank, int nranks, const void* unique_id) {
+    if (!out || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !unique_id))
+        return BRGPU_ERR_INVALID_ARGUMENT;
+    int rc = brgpu_create(out, device);
+    if (rc) return rc;
+    Handle* h = &(*out)->h;
+    h->nranks = nranks;
+    h->rank = rank;
+    if (nranks > 1) {
+        NcclApi& N = nccl_api();
+        if (!N.ok) { brgpu_destroy(*out); *out = nullptr; return BRGPU_ERR_NCCL; }
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        if (N.CommInitRank(&h->comm, nranks, id, rank) != ncclSuccess) {
+            brgpu_destroy(*out);
+            *out = nullptr;
+            return BRGPU_ERR_NCCL;
+        }
+    }
+    return BRGPU_OK;
+}
+
+int brgpu_plan_owned(int64_t n, int32_t leaf_cutoff, int32_t nranks, const int32_t* bstart, int32_t nblk,
+                     int32_t* counts, int32_t* ranges, int32_t cap) {
+    if (n <= 0 || nranks < 1 || !counts || leaf_cutoff < 5) return BRGPU_ERR_INVALID_ARGUMENT;
+    std::vector<int> b;
+    if (bstart && nblk > 0) b.assign(bstart, bstart + nblk + 1);
+    else b = {0, (int)n};
+    auto p = make_plan((int)n, leaf_cutoff, b, {0, (int)n}, true, nranks, 0);
+    for (int k = 0; k < nranks; ++k) {
+        const auto& ow = p->owned[(size_t)k];
+        counts[k] = (int32_t)ow.size();
+        for (int q = 0; q < (int)ow.size() && q < cap && ranges; ++q) {
+            ranges[2 * (k * cap + q)] = ow[(size_t)q].first;
+            ranges[2 * (k * cap + q) + 1] = ow[(size_t)q].second;
+        }
+    }
+    return BRGPU_OK;
 }
 
 int brgpu_set_trace(brgpu_handle* hh, int enable) {
