@@ -48,11 +48,11 @@ CONFIGS = {
 }
 
 # FP64 pipe operations per algorithmic unit (verified in SASS of this
-# build): secular pole term 2 DADD (delta) + 5 DFMA (reciprocal) + 2 DMUL + 3 DADD
-# (sum, |sum|, derivative; psi' is a prefix snapshot of the derivative sum, no add) = 12;
-# refreshed-weight term 3 DADD + 5 DFMA + 2 DMUL = 10; boundary-row term 2 DADD + 5 DFMA
-# + 1 DMUL + 3 DFMA = 11.
-OPS_PER_TERM = {"secular": 12, "zhat": 10, "rows": 11}
+# build): secular pole term 2 DADD (delta) + 5 DFMA (reciprocal) + 2 DMUL + 2 DADD
+# (sum, derivative; psi' and sum_{i<=j} t are prefix snapshots, sum|t| follows from the
+# bracket's sign split) = 11; refreshed-weight term 3 DADD + 5 DFMA + 2 DMUL = 10;
+# boundary-row term 2 DADD + 5 DFMA + 1 DMUL + 3 DFMA = 11.
+OPS_PER_TERM = {"secular": 11, "zhat": 10, "rows": 11}
 # algorithmic bytes per element per level of the memory-bound classes
 BYTES_PER_ELEM = {"merge_tol": 16, "merge_scatter": 56, "nn_flag": 9, "nn_write": 5,
                   "deflated_out": 53, "segment_walk": 0, "surv_count": 1, "surv_write": 0}
@@ -279,32 +279,39 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
         peak = fp64_peak(dev)
         roof = None
         if prof:
+            # FP64 work per kernel class (algorithmic lane-ops, see OPS_PER_TERM)
+            grid_terms = stats["pole_terms"] - stats["pole_terms_fused"]
+            work = {
+                "secular": OPS_PER_TERM["secular"] * grid_terms,
+                "zhat": OPS_PER_TERM["zhat"] * stats["k2_nonroot_grid"],
+                "rows": OPS_PER_TERM["rows"] * stats["k2_nonroot_grid"],
+                "fused_level": (OPS_PER_TERM["secular"] * stats["pole_terms_fused"]
+                                + (OPS_PER_TERM["zhat"] + OPS_PER_TERM["rows"]) * stats["k2_nonroot_fused"]),
+            }
+            pk = peak["lane_ops_per_s"] / 1e12
+            fp64 = {}
+            for k, ops in work.items():
+                if k in prof and ops > 0:
+                    t = prof[k][0] * 1e-3
+                    fp64[k] = {"ms": prof[k][0], "tops": ops / t / 1e12, "frac_of_peak": ops / t / 1e12 / pk}
             dom = max(prof, key=lambda k: prof[k][0])
             dom_ms, dom_launch = prof[dom]
-            pt = {"secular": stats["pole_terms"], "zhat": stats["zhat_terms"], "rows": stats["row_terms"]}
-            if dom in OPS_PER_TERM:
-                ops = OPS_PER_TERM[dom] * pt[dom]
-                ach = ops / (dom_ms * 1e-3) / 1e12
-                pk = peak["lane_ops_per_s"] / 1e12
+            if dom in work:
+                ach = work[dom] / (dom_ms * 1e-3) / 1e12
                 roof = {"bound": "fp64", "kernel": dom, "achieved": ach, "peak": pk,
                         "unit": "TFLOP/s (FP64 pipe lane-ops: DADD/DMUL/DFMA = 1)", "frac": ach / pk,
                         "traffic": None, "launches": dom_launch, "avg_launch_ms": dom_ms / dom_launch,
-                        "peak_source": "measured DFMA probe (libbrprobe.so), burst"}
+                        "peak_source": "measured DFMA probe (libbrprobe.so), burst",
+                        "work_note": "fused_level = secular + zhat + rows FP64 work of the SMEM levels"}
             else:
                 levels = stats["height"]
                 byts = BYTES_PER_ELEM.get(dom, 0) * N * levels
                 ach = byts / (dom_ms * 1e-3) / 1e9
-                pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
+                hb = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
                     if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-                roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk, "unit": "GB/s",
-                        "frac": ach / pk, "traffic": None, "launches": dom_launch,
+                roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hb, "unit": "GB/s",
+                        "frac": ach / hb, "traffic": None, "launches": dom_launch,
                         "avg_launch_ms": dom_ms / dom_launch}
-            fp64 = {}
-            for k in OPS_PER_TERM:
-                if k in prof:
-                    ops = OPS_PER_TERM[k] * pt[k]
-                    fp64[k] = {"ms": prof[k][0], "tops": ops / (prof[k][0] * 1e-3) / 1e12,
-                               "frac_of_peak": ops / (prof[k][0] * 1e-3) / peak["lane_ops_per_s"]}
         # --- CPU baseline: the reference composition on this box's host cores
         import oracle as O
         cores = os.cpu_count() or 1
@@ -337,8 +344,10 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
             "gpu_launches": launches * args.steps,
             "kernel_profile_ms": {k: round(v[0], 4) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])},
             "work": {"sum_k": stats["sum_k"], "sum_k2": stats["sum_k2"], "max_k": stats["max_k"],
-                     "pole_terms": stats["pole_terms"], "evals": stats["evals"], "merges": stats["merges"],
-                     "height": stats["height"]},
+                     "pole_terms": stats["pole_terms"], "pole_terms_fused": stats["pole_terms_fused"],
+                     "evals": stats["evals"], "merges": stats["merges"], "height": stats["height"],
+                     "k2_nonroot_fused": stats["k2_nonroot_fused"],
+                     "k2_nonroot_grid": stats["k2_nonroot_grid"]},
             "fp64_peak_probe": peak,
             "sorted_output": ok,
             "ledger": vars(s.ledger()),

@@ -305,8 +305,80 @@ static ev_t eval_shifted(int k, const double* d, const double* z, double rho, in
     return r;
 }
 
+/* ---- 32-way split arithmetic (GPU spec for merges larger than the fused SMEM
+ * tier, size > BRO_SPLIT_MIN_SIZE): a warp owns one root / pole; lane l
+ * accumulates the terms i = l, l+32, ... in increasing order; the 32 partials
+ * are combined by the xor butterfly a[l] <- a[l] + a[l ^ off], off = 16..1
+ * (every lane ends with the same value; this is lane 0's). */
+#define BRO_SPLIT 32
+#define BRO_SPLIT_MIN_SIZE 8192
+#define BRO_SPLIT_MIN_K 1024
+/* split iff the merge is larger than 8192 or its active rank exceeds 1024 */
+
+static double bfly_add(double* a) {
+    double b[BRO_SPLIT];
+    for (int off = BRO_SPLIT / 2; off >= 1; off >>= 1) {
+        for (int l = 0; l < BRO_SPLIT; ++l) b[l] = a[l] + a[l ^ off];
+        memcpy(a, b, sizeof(b));
+    }
+    return a[0];
+}
+
+static double bfly_mul(double* a) {
+    double b[BRO_SPLIT];
+    for (int off = BRO_SPLIT / 2; off >= 1; off >>= 1) {
+        for (int l = 0; l < BRO_SPLIT; ++l) b[l] = a[l] * a[l ^ off];
+        memcpy(a, b, sizeof(b));
+    }
+    return a[0];
+}
+
+static ev_t eval_split(int k, const double* d, const double* z, double rho, int org, double tau,
+                       int jsplit) {
+    ev_t r = {0.0, 0.0, 0.0, 0.0, 0};
+    const double dorg = d[org];
+    double S[BRO_SPLIT], SD[BRO_SPLIT], PS[BRO_SPLIT], PU[BRO_SPLIT];
+    for (int l = 0; l < BRO_SPLIT; ++l) {
+        S[l] = 0.0; SD[l] = 0.0; PS[l] = 0.0; PU[l] = 0.0;
+        for (int i = l; i < k; i += BRO_SPLIT) {
+            const double del = (d[i] - dorg) - tau;
+            if (del == 0.0) r.pole = 1;
+            const double zz = z[i] * z[i];
+            const double rr = 1.0 / del;
+            const double t = zz * rr;
+            S[l] += t;
+            SD[l] += t * rr;
+            if (i <= jsplit) { PS[l] = SD[l]; PU[l] = S[l]; }
+        }
+    }
+    if (r.pole) return r;
+    const double sum = bfly_add(S), sd = bfly_add(SD), ps = bfly_add(PS), pu = bfly_add(PU);
+    r.f = 1.0 + rho * sum;
+    r.fp = rho * sd;
+    r.abs_sum = rho * (sum - 2.0 * pu);
+    r.psi = rho * ps;
+    return r;
+}
+
+static double zsq_split(int k, const double* z) {
+    double S[BRO_SPLIT];
+    for (int l = 0; l < BRO_SPLIT; ++l) {
+        S[l] = 0.0;
+        for (int i = l; i < k; i += BRO_SPLIT) S[l] += z[i] * z[i];
+    }
+    return bfly_add(S);
+}
+
+static int solve_root_impl(int k, const double* d, const double* z, double rho, int j, int patched,
+                           int ref, int split, int* origin, double* tau_out, int* nevals);
+
 int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
                    int patched, int ref, int* origin, double* tau_out, int* nevals) {
+    return solve_root_impl(k, d, z, rho, j, patched, ref, 0, origin, tau_out, nevals);
+}
+
+static int solve_root_impl(int k, const double* d, const double* z, double rho, int j, int patched,
+                           int ref, int split, int* origin, double* tau_out, int* nevals) {
     int ne = 0;
     if (j < 0 || j >= k) return BRO_INVALID_ARGUMENT;
     if (k == 1) {
@@ -322,13 +394,15 @@ int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
     ev_t mid_ev = {0.0, 0.0, 0.0, 0.0, 0};
     if (last) {
         double zsq = 0.0;
-        for (int i = 0; i < k; ++i) zsq += z[i] * z[i];
+        if (split) zsq = zsq_split(k, z);
+        else for (int i = 0; i < k; ++i) zsq += z[i] * z[i];
         org = k - 1;
         lo = 0.0;
         hi = rho * zsq;
     } else {
         const double gap = d[j + 1] - d[j];
-        ev_t mid = eval_shifted(k, d, z, rho, j, 0.5 * gap, j, ref);
+        ev_t mid = split ? eval_split(k, d, z, rho, j, 0.5 * gap, j)
+                         : eval_shifted(k, d, z, rho, j, 0.5 * gap, j, ref);
         ++ne;
         if (mid.pole || mid.f > 0.0) {
             org = j; lo = 0.0; hi = gap; other_gap = d[j + 1] - d[j];
@@ -348,12 +422,12 @@ int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
             ev = mid_ev;
             reuse = 0;
         } else {
-            ev = eval_shifted(k, d, z, rho, org, tau, j, ref);
+            ev = split ? eval_split(k, d, z, rho, org, tau, j) : eval_shifted(k, d, z, rho, org, tau, j, ref);
             ++ne;
         }
         if (ev.pole) {
             tau = 0.5 * (lo + hi);
-            ev = eval_shifted(k, d, z, rho, org, tau, j, ref);
+            ev = split ? eval_split(k, d, z, rho, org, tau, j) : eval_shifted(k, d, z, rho, org, tau, j, ref);
             ++ne;
             if (ev.pole) break;
         }
@@ -433,7 +507,7 @@ int bro_refreshed_weights(int k, const double* d, const double* z, const int* or
 
 /* One parent boundary-row pair for root (org, tau): secular.cpp:272-286 + dense.hpp:48-53. */
 static int root_rows(int k, const double* d, const double* zh, const double* r0, const double* r1,
-                     int org, double tau, int ref, double* blo, double* bhi, double* ybuf) {
+                     int org, double tau, int ref, int split, double* blo, double* bhi, double* ybuf) {
     const double dorg = d[org];
     if (ref) {
         double norm_sq = 0.0;
@@ -452,6 +526,22 @@ static int root_rows(int k, const double* d, const double* zh, const double* r0,
             a1 += r1[i] * y;
         }
         *blo = a0; *bhi = a1;
+    } else if (split) {
+        double NN[BRO_SPLIT], S0[BRO_SPLIT], S1[BRO_SPLIT];
+        for (int l = 0; l < BRO_SPLIT; ++l) {
+            NN[l] = 0.0; S0[l] = 0.0; S1[l] = 0.0;
+            for (int i = l; i < k; i += BRO_SPLIT) {
+                const double del = (d[i] - dorg) - tau;
+                if (del == 0.0) return BRO_ZERO_DENOMINATOR;
+                const double y = zh[i] * (1.0 / del);
+                NN[l] = fma(y, y, NN[l]);
+                S0[l] = fma(r0[i], y, S0[l]);
+                S1[l] = fma(r1[i], y, S1[l]);
+            }
+        }
+        const double nn = bfly_add(NN), s0 = bfly_add(S0), s1 = bfly_add(S1);
+        const double inv = 1.0 / sqrt(nn);
+        *blo = s0 * inv; *bhi = s1 * inv;
     } else {
         double nn = 0.0, s0 = 0.0, s1 = 0.0;
         for (int i = 0; i < k; ++i) {
@@ -635,6 +725,7 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
     memset(&mo, 0, sizeof(mo));
     const int n = (int)size, nL = (int)(size / 2), nR = n - nL;
     const int ref = o->ref_arith;
+    int split = !ref && n > BRO_SPLIT_MIN_SIZE;
     double* lamL = lam + off;
     double* lamR = lam + off + nL;
     double* buf = (double*)malloc(sizeof(double) * (size_t)n * 11);
@@ -680,6 +771,7 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
     deflate_walk(n, D, Z, is_root ? NULL : R0, is_root ? NULL : R1, tol, ref, act, defl, &info);
     const int K = info.K;
     mo.K = K; mo.nn = info.nn; mo.nrot = info.nrot;
+    if (!ref && K > BRO_SPLIT_MIN_K) split = 1;
     for (int a = 0; a < K; ++a) {
         dA[a] = D[act[a]];
         zA[a] = Z[act[a]];
@@ -692,7 +784,7 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
 #pragma omp parallel for schedule(dynamic, 16) reduction(+ : evals) if (par && K >= 64)
     for (int j = 0; j < K; ++j) {
         int ne = 0;
-        int st = bro_solve_root(K, dA, zA, rho, j, o->patched_stop, ref, &org[j], &tau[j], &ne);
+        int st = solve_root_impl(K, dA, zA, rho, j, o->patched_stop, ref, split, &org[j], &tau[j], &ne);
         evals += ne;
         if (st) {
 #pragma omp atomic write
@@ -710,11 +802,24 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
             for (int i = 0; i < K; ++i) {
                 const double di = dA[i];
                 double w = 1.0;
-                for (int j = 0; j < K; ++j) {
-                    const double del = (di - dA[org[j]]) - tau[j];
-                    if (i == j) w *= del;
-                    else if (ref) w *= del / (di - dA[j]);
-                    else w *= del * (1.0 / (di - dA[j]));
+                if (split) {
+                    double W[BRO_SPLIT];
+                    for (int l = 0; l < BRO_SPLIT; ++l) {
+                        W[l] = 1.0;
+                        for (int j = l; j < K; j += BRO_SPLIT) {
+                            const double del = (di - dA[org[j]]) - tau[j];
+                            if (i == j) W[l] *= del;
+                            else W[l] *= del * (1.0 / (di - dA[j]));
+                        }
+                    }
+                    w = bfly_mul(W);
+                } else {
+                    for (int j = 0; j < K; ++j) {
+                        const double del = (di - dA[org[j]]) - tau[j];
+                        if (i == j) w *= del;
+                        else if (ref) w *= del / (di - dA[j]);
+                        else w *= del * (1.0 / (di - dA[j]));
+                    }
                 }
                 const double mag = sqrt(fmax(0.0, -w));
                 zh[i] = zA[i] >= 0.0 ? mag : -mag;
@@ -730,7 +835,7 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
 #pragma omp for schedule(static)
             for (int j = 0; j < K; ++j) {
                 double b0, b1;
-                int st = root_rows(K, dA, zh, r0A, r1A, org[j], tau[j], ref, &b0, &b1, ybuf);
+                int st = root_rows(K, dA, zh, r0A, r1A, org[j], tau[j], ref, split, &b0, &b1, ybuf);
                 if (st) {
 #pragma omp atomic write
                     st_all = st;

@@ -27,7 +27,9 @@ class Stats(C.Structure):
                 ("merges", C.c_int64), ("sum_k", C.c_int64), ("sum_k2", C.c_double),
                 ("sum_nn", C.c_int64), ("rotations", C.c_int64), ("evals", C.c_int64),
                 ("pole_terms", C.c_double), ("zhat_terms", C.c_double), ("row_terms", C.c_double),
-                ("max_k", C.c_int64), ("kernel_launches", C.c_int32), ("graph_replayed", C.c_int32)]
+                ("max_k", C.c_int64), ("kernel_launches", C.c_int32), ("graph_replayed", C.c_int32),
+                ("evals_fused", C.c_int64), ("pole_terms_fused", C.c_double),
+                ("k2_nonroot_fused", C.c_double), ("k2_nonroot_grid", C.c_double)]
 
 
 class Ledger(C.Structure):

@@ -731,7 +731,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
 int finish_solve(Handle* h) {
     cudaStream_t s = h->stream;
     CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
     {
         float a = 0.f, b = 0.f;
@@ -741,16 +741,22 @@ int finish_solve(Handle* h) {
         h->timing.main_ms = b;
         h->timing.device_ms = (double)a + (double)b;
     }
-    h->stats.evals = (int64_t)h->hcnt[0];
-    h->stats.pole_terms = (double)h->hcnt[1];
+    h->stats.evals = (int64_t)(h->hcnt[0] + h->hcnt[2]);
+    h->stats.pole_terms = (double)(h->hcnt[1] + h->hcnt[3]);
+    h->stats.evals_fused = (int64_t)h->hcnt[2];
+    h->stats.pole_terms_fused = (double)h->hcnt[3];
     if (h->trace && h->plan) {
         Plan* p = h->plan.get();
         const size_t M = p->mOff.size();
         std::vector<int> tb(2 * M);
         if (M) CUDA_TRY(h, cudaMemcpy(tb.data(), h->traceBuf, sizeof(int) * 2 * M, cudaMemcpyDeviceToHost));
         h->traceRecs.resize(M);
-        double sk2 = 0, szt = 0;
+        double sk2 = 0, szt = 0, k2f = 0, k2g = 0;
         int64_t sk = 0, snn = 0, mk = 0;
+        std::vector<char> fusedMerge(M, 0);
+        for (const auto* lv : {&p->levels, &p->levels2})
+            for (const LevelHost& lh : *lv)
+                for (int q = 0; q < lh.M; ++q) fusedMerge[(size_t)(lh.m0 + q)] = lh.fused;
         for (size_t m = 0; m < M; ++m) {
             brgpu_trace& t = h->traceRecs[m];
             t.level = p->mLevel[m];
@@ -760,12 +766,17 @@ int finish_solve(Handle* h) {
             t.nn = tb[2 * m];
             t.k = tb[2 * m + 1];
             sk += t.k; snn += t.nn; sk2 += (double)t.k * (double)t.k;
-            if (!t.is_root) szt += (double)t.k * (double)t.k;
+            if (!t.is_root) {
+                szt += (double)t.k * (double)t.k;
+                (fusedMerge[m] ? k2f : k2g) += (double)t.k * (double)t.k;
+            }
             mk = std::max<int64_t>(mk, t.k);
         }
         h->stats.sum_k = sk; h->stats.sum_k2 = sk2; h->stats.sum_nn = snn;
         h->stats.row_terms = szt; h->stats.zhat_terms = h->zhat ? szt : 0.0; h->stats.max_k = mk;
         h->stats.rotations = snn - sk;
+        h->stats.k2_nonroot_fused = k2f;
+        h->stats.k2_nonroot_grid = k2g;
     }
     if (h->hsmall[1]) return status_message(h, h->hsmall[1]);
     return BRGPU_OK;

@@ -325,8 +325,8 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
             terms += __shfl_xor_sync(0xffffffffu, terms, o);
         }
         if ((tid & 31) == 0 && evals) {
-            atomicAdd(&w.counters[0], evals);
-            atomicAdd(&w.counters[1], terms);
+            atomicAdd(&w.counters[2], evals);
+            atomicAdd(&w.counters[3], terms);
         }
     }
     __syncthreads();

@@ -512,10 +512,11 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
         while (g < 0 && !exhausted) {
             const int q = atomicAdd(&s_next, 1);
             if (c0 + q >= c1) { exhausted = true; break; }
-            g = c0 + q;
-            const int m = w.aMerge[g];
+            const int m = w.aMerge[c0 + q];
             int ke;
             active_range(w, L, m, ks, ke);
+            if (split_mode(L.mSize[m], ke - ks)) continue;  // warp-per-root tier (warp.cu)
+            g = c0 + q;
             const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
             rs_begin(st, ke - ks, g - ks, rho, PolesPtr{w.dA + ks}, w.zA[ks], Z2Ptr{w.z2A + ks});
             if (st.phase == kRsDone) {
@@ -595,9 +596,9 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
     double di = 0.0;
     if (act) {
         const int m = w.aMerge[g];
-        if (L.mFlags[m] & kMergeRoot) act = false;
         int ke;
         active_range(w, L, m, ks, ke);
+        if ((L.mFlags[m] & kMergeRoot) || split_mode(L.mSize[m], ke - ks)) act = false;
         K = ke - ks;
         i = g - ks;
         di = w.dA[g];
@@ -658,6 +659,11 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
     bool act = g < T;
     int ks = 0, K = 0, p = 0;
     double dorg = 0.0, tau = 0.0;
+    if (act) {  // warp-per-root tier owns split merges
+        int a0, a1;
+        active_range(w, L, w.aMerge[g], a0, a1);
+        if (split_mode(L.mSize[w.aMerge[g]], a1 - a0)) act = false;
+    }
     if (act) {
         const int m = w.aMerge[g];
         int ke;
@@ -796,6 +802,9 @@ static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 void launch_secular_tiled(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                           const SolveParams& prm);
+void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
+void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
+void launch_rows_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
 
 int selftest_rcp(long long count, unsigned long long seed, unsigned long long* host_bad) {
     unsigned long long* d;
@@ -891,18 +900,21 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
     PMARK(BRGPU_K_SURVWRITE);
     k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
     launch_secular_tiled(s, w, L, n, prm);
+    launch_secular_warp(s, w, L, n, prm);
     PMARK(BRGPU_K_SECULAR);
-    int nl = 10;
+    int nl = 12;  // tol .. surv_write (9) + 3 secular tiers
     if (prm.zhat) {
         k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
+        launch_zhat_warp(s, w, L, n, prm);
         PMARK(BRGPU_K_ZHAT);
-        ++nl;
+        nl += 2;
     }
     k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
+    launch_rows_warp(s, w, L, n, prm);
     PMARK(BRGPU_K_ROWS);
     k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_DEFLATED);
-    *launches += nl + 2;
+    *launches += nl + 3;  // rows, rows_warp, deflated_out
 }
 
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,

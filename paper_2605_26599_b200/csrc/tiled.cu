@@ -62,12 +62,13 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
         while (g < 0 && !exhausted) {
             const int q = atomicAdd(&s_next, 1);
             if (c0 + q >= c1) { exhausted = true; break; }
-            g = c0 + q;
-            const int m = w.aMerge[g];
+            const int m = w.aMerge[c0 + q];
             int ke;
             const int off = L.mOff[m];
             ks = w.survPre[w.nnPre[off]];
             ke = w.survPre[w.nnPre[off + L.mSize[m]]];
+            if (split_mode(L.mSize[m], ke - ks)) continue;  // warp-per-root tier (warp.cu)
+            g = c0 + q;
             const double rho = fabs(w.ew[off + L.mNL[m] - 1]);
             rs_begin(st, ke - ks, g - ks, rho, PolesPtr{w.dA + ks}, w.zA[ks], Z2Ptr{w.z2A + ks});
             if (st.phase == kRsDone) {

@@ -1,0 +1,330 @@
+// warp.cu -- warp-per-root tier for merges larger than the fused SMEM tier
+// (size > kSplitMinSize): the upper levels of random inputs (few roots, latency
+// bound) and the large-K top levels of Toeplitz / glued Wilkinson.
+//
+// One warp owns one root (secular, rows) or one pole (refreshed weights).  Lane
+// l accumulates the terms l, l+32, ... in increasing order and the 32 partials
+// meet in the xor butterfly (bfly_add / bfly_mul) -- the split arithmetic the
+// checker states for these merges (oracle/br_oracle.c, BRO_SPLIT_MIN_SIZE), so
+// results stay bit-identical.  Every lane runs the same RootSM update on the
+// same butterfly result, so the per-root control flow has no divergence.  The
+// CTA's pole window streams through shared memory in tiles shared by its 8
+// warps (one coalesced L2 read per tile per CTA).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.hpp"
+#include "numerics.cuh"
+
+namespace brgpu {
+
+constexpr int kWarpThreads = 256;  // 8 warps
+constexpr int kWarpTile = 1024;    // (d, z^2) pairs per tile
+
+__device__ __forceinline__ void merge_active(const Work& w, const LevelDev& L, int m, int& ks, int& ke) {
+    const int off = L.mOff[m];
+    ks = w.survPre[w.nnPre[off]];
+    ke = w.survPre[w.nnPre[off + L.mSize[m]]];
+}
+
+// first index i >= lo with (i - ks) % 32 == lane
+__device__ __forceinline__ int strided_start(int lo, int ks, int lane) {
+    const int r = (lane - (lo - ks)) & 31;
+    return lo + r;
+}
+
+// ---------------------------------------------------------------------------
+// secular roots, one warp per root
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelDev L, int n, int patched) {
+    __shared__ double2 s_tile[2][kWarpTile];
+    __shared__ int s_next;
+    const int T = w.survPre[w.nnPre[n]];
+    const int G = (int)gridDim.x;
+    const int R = max(kWarpThreads / 32, (T + G - 1) / G);
+    const int c0 = blockIdx.x * R;
+    if (c0 >= T) return;
+    const int c1 = min(c0 + R, T);
+    int P0, P1, tmp;
+    merge_active(w, L, w.aMerge[c0], P0, tmp);
+    merge_active(w, L, w.aMerge[c1 - 1], tmp, P1);
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+
+    RootSM st;
+    int g = -1, ks = 0;
+    bool exhausted = false;
+    unsigned long long evals = 0, terms = 0;
+    for (;;) {
+        while (g < 0 && !exhausted) {
+            int q = 0;
+            if (lane == 0) q = atomicAdd(&s_next, 1);
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (c0 + q >= c1) { exhausted = true; break; }
+            const int gg = c0 + q;
+            const int m = w.aMerge[gg];
+            int ke;
+            merge_active(w, L, m, ks, ke);
+            if (!split_mode(L.mSize[m], ke - ks)) continue;  // lane-per-root tier owns it
+            g = gg;
+            const int K = ke - ks, j = g - ks;
+            const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+            double zsq = 0.0;
+            if (j == K - 1 && K > 1) {
+                for (int i = ks + lane; i < ke; i += 32) zsq += w.z2A[i];
+                zsq = bfly_add(zsq);
+            }
+            rs_begin_zsq(st, K, j, rho, PolesPtr{w.dA + ks}, w.zA[ks], zsq);
+            if (st.phase == kRsDone) {
+                if (lane == 0) { w.org[g] = st.org; w.tau[g] = st.tau; }
+                g = -1;
+            }
+        }
+        const bool need = g >= 0;
+        if (!__syncthreads_or(need)) break;
+        double sum = 0.0, sum_d = 0.0, psi = 0.0, psum = 0.0;
+        unsigned minexp = 0x7ff00000u;
+        const int K = need ? st.K : 0;
+        const int j = st.j;
+        const double dorg = st.dorg, tau = st.tau;
+        int buf = 0;
+        for (int i = P0 + (int)threadIdx.x; i < min(P0 + kWarpTile, P1); i += kWarpThreads)
+            s_tile[0][i - P0] = make_double2(w.dA[i], w.z2A[i]);
+        for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
+            const int thi = min(tlo + kWarpTile, P1);
+            __syncthreads();
+            if (thi < P1)
+                for (int i = thi + (int)threadIdx.x; i < min(thi + kWarpTile, P1); i += kWarpThreads)
+                    s_tile[buf ^ 1][i - thi] = make_double2(w.dA[i], w.z2A[i]);
+            if (need) {
+                const int lo = max(ks, tlo), hi = min(ks + K, thi);
+                const double2* __restrict__ tp = s_tile[buf] - tlo;
+#pragma unroll 4
+                for (int i = strided_start(lo, ks, lane); i < hi; i += 32) {
+                    const double2 dz = tp[i];
+                    const double del = (dz.x - dorg) - tau;
+                    minexp = min(minexp, expfield(del));
+                    const double r = rcp_nr(del);
+                    const double t = dz.y * r;
+                    sum += t;
+                    sum_d += t * r;
+                    if (i - ks <= j) { psi = sum_d; psum = sum; }
+                }
+            }
+            buf ^= 1;
+        }
+        __syncthreads();
+        if (need) {
+            // lanes without terms have minexp = 0x7ff00000 (neutral for min)
+            const unsigned mx = bfly_min(minexp);
+            bool pole = false;
+            if (mx < kRcpMinExp) {  // rare: exact strided pass from global memory
+                sum = 0.0; sum_d = 0.0; psi = 0.0; psum = 0.0;
+                for (int i = ks + lane; i < ks + K; i += 32) {
+                    const double del = (w.dA[i] - dorg) - tau;
+                    pole |= (del == 0.0);
+                    const double r = __drcp_rn(del);
+                    const double t = w.z2A[i] * r;
+                    sum += t;
+                    sum_d += t * r;
+                    if (i - ks <= j) { psi = sum_d; psum = sum; }
+                }
+                pole = __any_sync(0xffffffffu, pole);
+            }
+            const double S = bfly_add(sum), SD = bfly_add(sum_d);
+            const double PS = bfly_add(psi), PU = bfly_add(psum);
+            Ev ev;
+            ev.f = 1.0 + st.rho * S;
+            ev.fp = st.rho * SD;
+            ev.abs_sum = st.rho * (S - 2.0 * PU);
+            ev.psi = st.rho * PS;
+            ev.pole = pole;
+            ++evals;
+            terms += (unsigned long long)K;
+            rs_consume(st, ev, PolesPtr{w.dA + ks}, patched != 0);
+            if (st.phase == kRsDone || st.phase == kRsFail) {
+                if (lane == 0) {
+                    if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                    w.org[g] = st.org;
+                    w.tau[g] = st.tau;
+                }
+                g = -1;
+            }
+        }
+    }
+    if (lane == 0 && evals) {
+        atomicAdd(&w.counters[0], evals);
+        atomicAdd(&w.counters[1], terms);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// refreshed weights, one warp per pole (product over roots, split by lane)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, int n) {
+    __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
+    const int T = w.survPre[w.nnPre[n]];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {  // uniform per CTA
+        const int g = base + wid;
+        bool act = g < T;
+        int ks = 0, K = 0, i = 0;
+        double di = 0.0;
+        if (act) {
+            const int m = w.aMerge[g];
+            int ke;
+            merge_active(w, L, m, ks, ke);
+            act = split_mode(L.mSize[m], ke - ks) && !(L.mFlags[m] & kMergeRoot);
+            K = ke - ks;
+            i = g - ks;
+            di = w.dA[g];
+        }
+        if (!__syncthreads_or(act)) continue;
+        const int gl = min(base + 8, T) - 1;
+        int P0, P1, tmp;
+        merge_active(w, L, w.aMerge[base], P0, tmp);
+        merge_active(w, L, w.aMerge[gl], tmp, P1);
+        double prod = 1.0;
+        unsigned minexp = 0x7ff00000u;
+        for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
+            const int thi = min(tlo + kWarpTile, P1);
+            __syncthreads();
+            for (int r = tlo + (int)threadIdx.x; r < thi; r += kWarpThreads) {
+                int rks, rke;
+                merge_active(w, L, w.aMerge[r], rks, rke);
+                s_dorg[r - tlo] = w.dA[rks + w.org[r]];
+                s_tau[r - tlo] = w.tau[r];
+                s_dj[r - tlo] = w.dA[r];
+            }
+            __syncthreads();
+            if (act) {
+                const int lo = max(ks, tlo), hi = min(ks + K, thi);
+                for (int jg = strided_start(lo, ks, lane); jg < hi; jg += 32) {
+                    const int t = jg - tlo;
+                    const double del = (di - s_dorg[t]) - s_tau[t];
+                    const double dd = di - s_dj[t];
+                    const bool self = (jg - ks) == i;
+                    if (!self) minexp = min(minexp, expfield(dd));
+                    const double f = self ? del : del * rcp_nr(dd);
+                    prod = prod * f;
+                }
+            }
+        }
+        if (act) {
+            const unsigned mx = bfly_min(minexp);
+            if (mx < kRcpMinExp) {  // exact redo
+                prod = 1.0;
+                for (int jg = ks + lane; jg < ks + K; jg += 32) {
+                    const double del = (di - w.dA[ks + w.org[jg]]) - w.tau[jg];
+                    if (jg - ks == i) prod = prod * del;
+                    else prod = prod * (del * __drcp_rn(di - w.dA[jg]));
+                }
+            }
+            const double W = bfly_mul(prod);
+            if (lane == 0) {
+                const double mag = sqrt(fmax(0.0, -W));
+                w.zA[g] = w.zA[g] >= 0.0 ? mag : -mag;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// boundary rows + placement, one warp per root
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
+    __shared__ double s_d[kWarpTile], s_zh[kWarpTile], s_r0[kWarpTile], s_r1[kWarpTile];
+    const int T = w.survPre[w.nnPre[n]];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {
+        const int g = base + wid;
+        bool act = g < T, rows = false;
+        int ks = 0, K = 0, p = 0;
+        double dorg = 0.0, tau = 0.0;
+        if (act) {
+            const int m = w.aMerge[g];
+            int ke;
+            merge_active(w, L, m, ks, ke);
+            act = split_mode(L.mSize[m], ke - ks);
+            if (act) {
+                K = ke - ks;
+                const int j = g - ks;
+                const int off = L.mOff[m], size = L.mSize[m];
+                dorg = w.dA[ks + w.org[g]];
+                tau = w.tau[g];
+                const double lam = dorg + tau;
+                const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + ks, K, lam);
+                p = off + pos;
+                if (lane == 0) w.lam[p] = lam;
+                rows = !(L.mFlags[m] & kMergeRoot);
+            }
+        }
+        if (!__syncthreads_or(rows)) continue;
+        const int gl = min(base + 8, T) - 1;
+        int P0, P1, tmp;
+        merge_active(w, L, w.aMerge[base], P0, tmp);
+        merge_active(w, L, w.aMerge[gl], tmp, P1);
+        double nn = 0.0, s0 = 0.0, s1 = 0.0;
+        unsigned minexp = 0x7ff00000u;
+        for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
+            const int thi = min(tlo + kWarpTile, P1);
+            __syncthreads();
+            for (int r = tlo + (int)threadIdx.x; r < thi; r += kWarpThreads) {
+                s_d[r - tlo] = w.dA[r];
+                s_zh[r - tlo] = w.zA[r];
+                s_r0[r - tlo] = w.r0A[r];
+                s_r1[r - tlo] = w.r1A[r];
+            }
+            __syncthreads();
+            if (rows) {
+                const int lo = max(ks, tlo), hi = min(ks + K, thi);
+#pragma unroll 4
+                for (int i = strided_start(lo, ks, lane); i < hi; i += 32) {
+                    const int t = i - tlo;
+                    const double del = (s_d[t] - dorg) - tau;
+                    minexp = min(minexp, expfield(del));
+                    const double y = s_zh[t] * rcp_nr(del);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(s_r0[t], y, s0);
+                    s1 = __fma_rn(s_r1[t], y, s1);
+                }
+            }
+        }
+        if (rows) {
+            const unsigned mx = bfly_min(minexp);
+            if (mx < kRcpMinExp) {  // exact redo; a zero delta is an error
+                bool zero = false;
+                nn = 0.0; s0 = 0.0; s1 = 0.0;
+                for (int i = ks + lane; i < ks + K; i += 32) {
+                    const double del = (w.dA[i] - dorg) - tau;
+                    zero |= (del == 0.0);
+                    const double y = w.zA[i] * __drcp_rn(del);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(w.r0A[i], y, s0);
+                    s1 = __fma_rn(w.r1A[i], y, s1);
+                }
+                if (__any_sync(0xffffffffu, zero) && lane == 0) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+            }
+            const double NN = bfly_add(nn), S0 = bfly_add(s0), S1 = bfly_add(s1);
+            if (lane == 0) {
+                const double inv = 1.0 / sqrt(NN);
+                w.blo[p] = S0 * inv;
+                w.bhi[p] = S1 * inv;
+            }
+        }
+    }
+}
+
+void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
+    k_secular_warp<<<prm.sec_grid, kWarpThreads, 0, s>>>(w, L, n, prm.patched);
+}
+void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
+    k_zhat_warp<<<prm.sec_grid, kWarpThreads, 0, s>>>(w, L, n);
+}
+void launch_rows_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
+    k_rows_warp<<<prm.sec_grid, kWarpThreads, 0, s>>>(w, L, n);
+}
+
+}  // namespace brgpu
