@@ -383,31 +383,41 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     const double tol = merge_tol(L, m, tol_scale);
     if (q > qs && fabs(w.D[k] - w.D[w.nnPos[q - 1]]) <= tol) return;  // not a head
     w.survFlag[q] = 1;
+    // the current survivor lives in registers; the next entry is prefetched so a
+    // long cluster (glued Wilkinson: runs of ~700) is a compute chain, not a
+    // chain of dependent L2 round trips
     int prev = k;
-    double dprev_nn = w.D[k];
-    for (int q2 = q + 1; q2 < qe; ++q2) {
-        const int k2 = w.nnPos[q2];
-        const double d2 = w.D[k2];
+    double dp = w.D[k], zp = w.Z[k], x0p = w.R0[k], x1p = w.R1[k];
+    double dprev_nn = dp;
+    int q2 = q + 1;
+    int k2 = q2 < qe ? w.nnPos[q2] : 0;
+    double d2 = 0.0, zq = 0.0, x0q = 0.0, x1q = 0.0;
+    if (q2 < qe) { d2 = w.D[k2]; zq = w.Z[k2]; x0q = w.R0[k2]; x1q = w.R1[k2]; }
+    for (; q2 < qe; ++q2) {
         if (fabs(d2 - dprev_nn) > tol) break;  // next segment head
+        // prefetch the next entry (only this walker ever touches it) while this step computes
+        const int kn = q2 + 1 < qe ? w.nnPos[q2 + 1] : 0;
+        double dn = 0.0, zn = 0.0, x0n = 0.0, x1n = 0.0;
+        if (q2 + 1 < qe) { dn = w.D[kn]; zn = w.Z[kn]; x0n = w.R0[kn]; x1n = w.R1[kn]; }
         dprev_nn = d2;
-        if (fabs(d2 - w.D[prev]) <= tol) {
-            const double zp = w.Z[prev], zq = w.Z[k2];
+        if (fabs(d2 - dp) <= tol) {
             const double r = hyp(zp, zq);
-            const double c = zp / r, s = zq / r;
-            w.Z[prev] = r;
+            const double c = zp / r, sn = zq / r;
             w.Z[k2] = 0.0;
-            double xp = w.R0[prev], xq = w.R0[k2];
-            w.R0[prev] = c * xp + s * xq;
-            w.R0[k2] = c * xq - s * xp;
-            xp = w.R1[prev]; xq = w.R1[k2];
-            w.R1[prev] = c * xp + s * xq;
-            w.R1[k2] = c * xq - s * xp;
+            w.R0[k2] = c * x0q - sn * x0p;
+            w.R1[k2] = c * x1q - sn * x1p;
+            zp = r;
+            x0p = c * x0p + sn * x0q;
+            x1p = c * x1p + sn * x1q;
             w.survFlag[q2] = 0;
         } else {
+            w.Z[prev] = zp; w.R0[prev] = x0p; w.R1[prev] = x1p;  // retire the survivor
             w.survFlag[q2] = 1;
-            prev = k2;
+            prev = k2; dp = d2; zp = zq; x0p = x0q; x1p = x1q;
         }
+        k2 = kn; d2 = dn; zq = zn; x0q = x0n; x1q = x1n;
     }
+    w.Z[prev] = zp; w.R0[prev] = x0p; w.R1[prev] = x1p;
 }
 
 __global__ void __launch_bounds__(kScanBlock) k_surv_count(Work w, int n) {
