@@ -372,6 +372,25 @@ static double zsq_split(int k, const double* z) {
 static int solve_root_impl(int k, const double* d, const double* z, double rho, int j, int patched,
                            int ref, int split, int* origin, double* tau_out, int* nevals);
 
+/* Root in (lo, hi) of A t^2 + B t + C = 0 (stable form), NaN if none. */
+static double quad_root_in(double A, double B, double C, double lo, double hi) {
+    double t = NAN;
+    if (A == 0.0) {
+        if (B != 0.0) t = -C / B;
+        return (isfinite(t) && t > lo && t < hi) ? t : NAN;
+    }
+    const double disc = B * B - 4.0 * A * C;
+    if (disc >= 0.0) {
+        const double sq = sqrt(disc);
+        const double q = -0.5 * (B + (B >= 0 ? sq : -sq));
+        const double r1 = q / A;
+        const double r2 = (q != 0.0) ? C / q : NAN;
+        if (isfinite(r1) && r1 > lo && r1 < hi) t = r1;
+        else if (isfinite(r2) && r2 > lo && r2 < hi) t = r2;
+    }
+    return t;
+}
+
 int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
                    int patched, int ref, int* origin, double* tau_out, int* nevals) {
     return solve_root_impl(k, d, z, rho, j, patched, ref, 0, origin, tau_out, nevals);
@@ -392,6 +411,8 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
     double lo, hi, other_gap = 0.0;
     int reuse = 0;
     ev_t mid_ev = {0.0, 0.0, 0.0, 0.0, 0};
+    int gmode = 0;
+    double gA = 0.0, gB = 0.0, gC = 0.0;
     if (last) {
         double zsq = 0.0;
         if (split) zsq = zsq_split(k, z);
@@ -413,6 +434,27 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
          * point in either origin; reuse its evaluation (f, f', psi' depend on
          * lambda only) instead of evaluating it again. */
         if (!ref) { reuse = 1; mid_ev = mid; }
+        /* GPU arithmetic, dlaed4-style start: when the rest of the secular sum
+         * (all poles but j, j+1) varies little over the half bracket
+         * (|f'_rest| gap/2 <= |f_rest| at the probe), the first step solves the
+         * two-nearest-poles-plus-constant model exactly instead of the lumped
+         * two-pole model. */
+        if (!ref && !mid.pole) {
+            const double tp = 0.5 * gap;
+            const double rj = 1.0 / ((d[j] - d[j]) - tp);
+            const double rj1 = 1.0 / ((d[j + 1] - d[j]) - tp);
+            const double z2j = z[j] * z[j], z2j1 = z[j + 1] * z[j + 1];
+            const double tj = z2j * rj, tj1 = z2j1 * rj1;
+            const double crest = mid.f - rho * tj - rho * tj1;
+            const double fprest = mid.fp - rho * (tj * rj) - rho * (tj1 * rj1);
+            if (fabs(fprest) * tp <= fabs(crest)) {
+                const double a = rho * z2j, b = rho * z2j1;
+                gmode = 1;
+                gA = crest;
+                if (org == j) { gB = -(crest * gap + a + b); gC = a * gap; }
+                else { gB = crest * gap - a - b; gC = -(b * gap); }
+            }
+        }
     }
     double tau = 0.5 * (lo + hi);
     int converged = 0;
@@ -438,7 +480,9 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
         const double scale = patched ? fmin(lambda_abs, fabs(tau)) : lambda_abs;
         if (hi - lo <= 4.0 * U_RND * scale) { converged = 1; break; }
         double tau_next = NAN;
-        if (iter < 100) {
+        if (iter == 0 && gmode) {
+            tau_next = quad_root_in(gA, gB, gC, lo, hi);
+        } else if (iter < 100) {
             const double dl = -tau;
             if (last) {
                 const double b = ev.fp * dl * dl;

@@ -310,7 +310,7 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
                 ev.pole = pole;
                 ++evals;
                 terms += (unsigned long long)st.K;
-                rs_consume(st, ev, PolesPairs{pairs + ks}, prm.patched != 0);
+                rs_consume(st, ev, PolesPairs{pairs + ks}, Z2Pairs{pairs + ks}, prm.patched != 0);
                 if (st.phase == kRsDone || st.phase == kRsFail) {
                     if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
                     S.org[g] = st.org;

@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
             ev.pole = pole;
             ++evals;
             terms += (unsigned long long)K;
-            rs_consume(st, ev, PolesPtr{w.dA + ks}, patched != 0);
+            rs_consume(st, ev, PolesPtr{w.dA + ks}, Z2Ptr{w.z2A + ks}, patched != 0);
             if (st.phase == kRsDone || st.phase == kRsFail) {
                 if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
                 w.org[g] = st.org;

@@ -124,7 +124,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
             ev.pole = pole;
             ++evals;
             terms += (unsigned long long)K;
-            rs_consume(st, ev, PolesPtr{w.dA + ks}, patched != 0);
+            rs_consume(st, ev, PolesPtr{w.dA + ks}, Z2Ptr{w.z2A + ks}, patched != 0);
             if (st.phase == kRsDone || st.phase == kRsFail) {
                 if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
                 w.org[g] = st.org;
