@@ -430,12 +430,18 @@ int ensure_work(Handle* h, int64_t n) {
     w.dA = dbl + 9 * c; w.zA = dbl + 10 * c; w.z2A = dbl + 11 * c; w.r0A = dbl + 12 * c;
     w.r1A = dbl + 13 * c; w.tau = dbl + 14 * c;
     const int64_t ntiles = (c + 1023) / 1024 + 1;
-    const int64_t ni = 5 * c + 2 + 2 * ntiles + 8;
+    const int64_t ni = 5 * c + 2 + 2 * ntiles + 8 + 2 * (2 * ntiles + 4);
     int* ib = nullptr;
     CUDA_TRY(h, cudaMalloc(&ib, sizeof(int) * ni));
     w.nnPre = ib; w.nnPos = ib + c + 1; w.survPre = ib + 2 * c + 1; w.aMerge = ib + 3 * c + 2;
     w.org = ib + 4 * c + 2; w.tileCnt = ib + 5 * c + 2; w.tileOff = ib + 5 * c + 2 + ntiles;
     w.status = ib + 5 * c + 2 + 2 * ntiles;
+    {
+        // 8-byte aligned look-back states after status (+2 ints of padding)
+        int* sp = ib + 5 * c + 2 + 2 * ntiles + 8;
+        if (reinterpret_cast<uintptr_t>(sp) % 8) ++sp;
+        w.scanState = reinterpret_cast<unsigned long long*>(sp);
+    }
     uint8_t* bb = nullptr;
     CUDA_TRY(h, cudaMalloc(&bb, 3 * c + 64));
     w.nnFlag = bb; w.survFlag = bb + c; h->split = bb + 2 * c;

@@ -51,6 +51,7 @@ struct Work {
     int* tileCnt;    // per-1024 tile counts (scan scratch)
     int* tileOff;
     int* status;     // first error code
+    unsigned long long* scanState;  // look-back tile states (2*ntiles) + 2 tickets
     unsigned long long* counters;  // [0] evals
 };
 

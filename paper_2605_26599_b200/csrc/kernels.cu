@@ -4,12 +4,12 @@
 //
 // Level pipeline (grid tier; one launch per step covers ALL merges of a
 // level, positions are level-global so no host round trip is needed):
-//   k_merge_tol      max(|D|,|z|) per merge              deflate.cpp:55-60
-//   k_merge_scatter  stable merge of the sorted children deflate.cpp:62-66, build_z deflate.cpp:31-41
-//   k_nn_flag/…      small-z flags + compaction          deflate.cpp:70-75
+//   k_merge_scatter  stable merge of the sorted children deflate.cpp:62-66, build_z deflate.cpp:31-41,
+//                    + per-merge max(|D|,|z|)            deflate.cpp:55-60
+//   k_nn_scan        small-z flags + compaction, 1 pass  deflate.cpp:70-75
 //   k_segment_walk   close-pole Givens walk per segment  deflate.cpp:76-95, 109-140
-//   k_surv_*         survivor compaction                 deflate.cpp:100-105
-//   k_secular        one root per thread                 secular.cpp:80-241
+//   k_surv_scan      survivor compaction, 1 pass         deflate.cpp:100-105
+//   k_secular        lane-per-root RootSM + CTA queue    secular.cpp:80-241 (tiled.cu, warp.cu: other tiers)
 //   k_zhat           refreshed weights, one pole/thread  secular.cpp:288-313
 //   k_rows           R_parent(:,j) = R_child y_j + parent placement
 //   k_deflated_out   deflated columns to parent order
@@ -272,98 +272,112 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __r
 // ---------------------------------------------------------------------------
 // level pipeline
 // ---------------------------------------------------------------------------
-__global__ void k_merge_tol(Work w, LevelDev L, int n) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = p < n ? find_merge(L, p) : -1;
-    double v = 0.0;
-    if (m >= 0) {
-        const int off = L.mOff[m], nl = L.mNL[m];
-        const double zv = p < off + nl ? w.bhi[p] : w.blo[p];
-        v = fmax(fabs(w.lam[p]), fabs(zv));
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, m);
-    unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-    if (peers == 0xffffffffu) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long y = __shfl_xor_sync(0xffffffffu, bits, o);
-            bits = y > bits ? y : bits;
-        }
-        if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(&L.mTol[m], bits);
-    } else if (m >= 0) {
-        atomicMax(&L.mTol[m], bits);
-    }
-}
-
 // Stable merge of the two sorted children (== std::stable_sort of the
-// concatenation by '<', deflate.cpp:62-66) and z = (sign*bhi_L, blo_R).
+// concatenation by '<', deflate.cpp:62-66), z = (sign*bhi_L, blo_R), and the
+// per-merge deflation scale max(|D|, |z|) (deflate.cpp:55-60; order-free max,
+// segmented warp reduction + one atomicMax per merge segment).
 __global__ void k_merge_scatter(Work w, LevelDev L, int n) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const int m = find_merge(L, p);
-    if (m < 0) return;
-    const int off = L.mOff[m], nl = L.mNL[m], nr = L.mSize[m] - nl;
-    const double v = w.lam[p];
-    int sp;
-    double z, r0, r1;
-    if (p < off + nl) {
-        sp = p + count_less(w.lam + off + nl, nr, v);
-        const double em = w.ew[off + nl - 1];
-        const double b = w.bhi[p];
-        z = em < 0 ? -b : b;
-        r0 = w.blo[p];
-        r1 = 0.0;
-    } else {
-        sp = (p - nl) + count_leq(w.lam + off, nl, v);
-        z = w.blo[p];
-        r0 = 0.0;
-        r1 = w.bhi[p];
+    const int m = p < n ? find_merge(L, p) : -1;
+    unsigned long long bits = 0ULL;
+    if (m >= 0) {
+        const int off = L.mOff[m], nl = L.mNL[m], nr = L.mSize[m] - nl;
+        const double v = w.lam[p];
+        int sp;
+        double z, r0, r1;
+        if (p < off + nl) {
+            sp = p + count_less(w.lam + off + nl, nr, v);
+            const double em = w.ew[off + nl - 1];
+            const double b = w.bhi[p];
+            z = em < 0 ? -b : b;
+            r0 = w.blo[p];
+            r1 = 0.0;
+        } else {
+            sp = (p - nl) + count_leq(w.lam + off, nl, v);
+            z = w.blo[p];
+            r0 = 0.0;
+            r1 = w.bhi[p];
+        }
+        w.D[sp] = v;
+        w.Z[sp] = z;
+        w.R0[sp] = r0;
+        w.R1[sp] = r1;
+        bits = (unsigned long long)__double_as_longlong(fmax(fabs(v), fabs(z)));
     }
-    w.D[sp] = v;
-    w.Z[sp] = z;
-    w.R0[sp] = r0;
-    w.R1[sp] = r1;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long b2 = __shfl_down_sync(0xffffffffu, bits, off);
+        const int m2 = __shfl_down_sync(0xffffffffu, m, off);
+        if (lane + off < 32 && m2 == m && b2 > bits) bits = b2;
+    }
+    const int mp = __shfl_up_sync(0xffffffffu, m, 1);
+    if (m >= 0 && (lane == 0 || mp != m)) atomicMax(&L.mTol[m], bits);
 }
 
-// non-negligible flags |z| > tol (deflate.cpp:72) + per-tile counts
-__global__ void __launch_bounds__(kScanBlock) k_nn_flag(Work w, LevelDev L, int n, double tol_scale) {
-    const int k = blockIdx.x * kScanBlock + threadIdx.x;
+// ---------------------------------------------------------------------------
+// single-pass compaction scans (decoupled look-back).  Tile states are packed
+// 64-bit words: bits 62-63 status (1 aggregate, 2 inclusive), low 32 the count;
+// tiles are taken in ticket order so every predecessor is resident or done.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kTileAgg = 1ULL << 62, kTileInc = 2ULL << 62;
+
+__device__ __forceinline__ int cta_lookback(unsigned long long* state, int tile, int aggregate,
+                                            int* s_bcast) {
+    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors per step
+        const int lane = threadIdx.x;
+        if (lane == 0)
+            atomicExch(&state[tile], ((tile == 0 ? 2ULL : 1ULL) << 62) | (unsigned)aggregate);
+        int prefix = 0;
+        if (tile > 0) {
+            int j = tile - 1;
+            for (;;) {
+                const int idx = j - lane;
+                unsigned long long v = idx >= 0 ? *(volatile unsigned long long*)&state[idx] : (2ULL << 62);
+                while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+                    if ((v >> 62) == 0) v = *(volatile unsigned long long*)&state[idx];
+                }
+                const unsigned incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+                // closest inclusive predecessor = lowest set lane; sum lanes [0, k]
+                const int k = incl ? __ffs(incl) - 1 : 31;
+                int c = lane <= k ? (int)(unsigned)(v & 0xffffffffULL) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                prefix += c;
+                if (incl) break;
+                j -= 32;
+            }
+            if (lane == 0) atomicExch(&state[tile], kTileInc | (unsigned)(prefix + aggregate));
+        }
+        if (lane == 0) *s_bcast = prefix;
+    }
+    __syncthreads();
+    return *s_bcast;
+}
+
+// non-negligible flags |z| > tol (deflate.cpp:72), their exclusive prefix over
+// positions and the NN list (sorted positions), in one pass
+__global__ void __launch_bounds__(kScanBlock) k_nn_scan(Work w, LevelDev L, int n, double tol_scale,
+                                                        unsigned long long* state, int* ticket) {
+    __shared__ int s_tile, s_pref;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int k = tile * kScanBlock + threadIdx.x;
     int f = 0;
     if (k < n) {
         const int m = find_merge(L, k);
         if (m >= 0) f = fabs(w.Z[k]) > merge_tol(L, m, tol_scale);
         w.nnFlag[k] = (uint8_t)f;
     }
-    const int s = block_sum<kScanBlock>(f);
-    if (threadIdx.x == 0) w.tileCnt[blockIdx.x] = s;
-}
-
-// exclusive scan of tile counts (one CTA); total -> *total_dst[*idx_src or 0]
-__global__ void __launch_bounds__(kScanBlock) k_scan_tiles(int* __restrict__ tileCnt,
-                                                           int* __restrict__ tileOff, int ntiles,
-                                                           int* __restrict__ total_dst,
-                                                           const int* __restrict__ idx_src) {
-    int carry = 0;
-    for (int base = 0; base < ntiles; base += kScanBlock) {
-        const int i = base + threadIdx.x;
-        const int v = i < ntiles ? tileCnt[i] : 0;
-        int tot;
-        const int ex = block_exclusive_scan<kScanBlock>(v, tot);
-        if (i < ntiles) tileOff[i] = carry + ex;
-        carry += tot;
-    }
-    if (threadIdx.x == 0) total_dst[idx_src ? *idx_src : 0] = carry;
-}
-
-__global__ void __launch_bounds__(kScanBlock) k_nn_write(Work w, int n) {
-    const int k = blockIdx.x * kScanBlock + threadIdx.x;
-    const int f = k < n ? w.nnFlag[k] : 0;
     int tot;
-    const int ex = block_exclusive_scan<kScanBlock>(f, tot) + w.tileOff[blockIdx.x];
+    const int ex = block_exclusive_scan<kScanBlock>(f, tot);
+    const int base = cta_lookback(state, tile, tot, &s_pref);
     if (k < n) {
-        w.nnPre[k] = ex;
-        if (f) w.nnPos[ex] = k;
+        w.nnPre[k] = base + ex;
+        if (f) w.nnPos[base + ex] = k;
     }
+    if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= n) w.nnPre[n] = base + tot;
 }
 
 // Close-pole deflation (deflate.cpp:76-95).  A segment is a maximal run of
@@ -420,21 +434,22 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     w.Z[prev] = zp; w.R0[prev] = x0p; w.R1[prev] = x1p;
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_surv_count(Work w, int n) {
-    const int q = blockIdx.x * kScanBlock + threadIdx.x;
+// survivor prefix over NN indices + compacted active problem (deflate.cpp:100-105),
+// one pass; tile 0 always runs so survPre[NN] is written even when NN == 0
+__global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, int n,
+                                                          unsigned long long* state, int* ticket) {
+    __shared__ int s_tile, s_pref;
     const int NN = w.nnPre[n];
-    const int f = q < NN ? w.survFlag[q] : 0;
-    const int s = block_sum<kScanBlock>(f);
-    if (threadIdx.x == 0) w.tileCnt[blockIdx.x] = s;
-}
-
-// survivor prefix + compacted active problem (deflate.cpp:100-105)
-__global__ void __launch_bounds__(kScanBlock) k_surv_write(Work w, LevelDev L, int n) {
-    const int q = blockIdx.x * kScanBlock + threadIdx.x;
-    const int NN = w.nnPre[n];
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile > 0 && tile * kScanBlock >= NN) return;  // uniform per CTA
+    const int q = tile * kScanBlock + threadIdx.x;
     const int f = q < NN ? w.survFlag[q] : 0;
     int tot;
-    const int g = block_exclusive_scan<kScanBlock>(f, tot) + w.tileOff[blockIdx.x];
+    const int ex = block_exclusive_scan<kScanBlock>(f, tot);
+    const int base = cta_lookback(state, tile, tot, &s_pref);
+    const int g = base + ex;
     if (q < NN) {
         w.survPre[q] = g;
         if (f) {
@@ -448,12 +463,9 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_write(Work w, LevelDev L, i
             w.aMerge[g] = find_merge(L, k);
         }
     }
+    if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= NN) w.survPre[NN] = base + tot;
 }
 
-// Roots of a CTA are a contiguous range of level-global active indices; the
-// poles they need are the union of their merges' active ranges, itself a
-// contiguous window [P0, P1).  Windows up to kWin entries are staged in shared
-// memory (broadcast reads in the pole loop); larger ones read global memory.
 constexpr int kSecBlock = 128;
 constexpr int kWin = 1024;
 
@@ -890,29 +902,24 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                   const SolveParams& prm, int* launches, Prof* prof) {
     const int ntiles = cdiv(n, kScanBlock);
     cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
-    k_merge_tol<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
-    PMARK(BRGPU_K_TOL);
+    // tile states + tickets of the two single-pass scans (2*ntiles + 2 words)
+    cudaMemsetAsync(w.scanState, 0, sizeof(unsigned long long) * (size_t)(2 * ntiles + 2), s);
+    unsigned long long* st1 = w.scanState;
+    unsigned long long* st2 = w.scanState + ntiles;
+    int* tk = reinterpret_cast<int*>(w.scanState + 2 * ntiles);
     k_merge_scatter<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_SCATTER);
-    k_nn_flag<<<ntiles, kScanBlock, 0, s>>>(w, L, n, prm.tol_scale);
+    k_nn_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, prm.tol_scale, st1, tk);
     PMARK(BRGPU_K_NNFLAG);
-    k_scan_tiles<<<1, kScanBlock, 0, s>>>(w.tileCnt, w.tileOff, ntiles, w.nnPre + n, nullptr);
-    PMARK(BRGPU_K_SCAN);
-    k_nn_write<<<ntiles, kScanBlock, 0, s>>>(w, n);
-    PMARK(BRGPU_K_NNWRITE);
     k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
     PMARK(BRGPU_K_WALK);
-    k_surv_count<<<ntiles, kScanBlock, 0, s>>>(w, n);
-    PMARK(BRGPU_K_SURVCOUNT);
-    k_scan_tiles<<<1, kScanBlock, 0, s>>>(w.tileCnt, w.tileOff, ntiles, w.survPre, w.nnPre + n);
-    PMARK(BRGPU_K_SCAN);
-    k_surv_write<<<ntiles, kScanBlock, 0, s>>>(w, L, n);
+    k_surv_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, st2, tk + 1);
     PMARK(BRGPU_K_SURVWRITE);
     k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
     launch_secular_tiled(s, w, L, n, prm);
     launch_secular_warp(s, w, L, n, prm);
     PMARK(BRGPU_K_SECULAR);
-    int nl = 12;  // tol .. surv_write (9) + 3 secular tiers
+    int nl = 7;  // scatter, nn_scan, walk, surv_scan + 3 secular tiers
     if (prm.zhat) {
         k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
         launch_zhat_warp(s, w, L, n, prm);
