@@ -441,6 +441,7 @@ int ensure_work(Handle* h, int64_t n) {
         int* sp = ib + 5 * c + 2 + 2 * ntiles + 8;
         if (reinterpret_cast<uintptr_t>(sp) % 8) ++sp;
         w.scanState = reinterpret_cast<unsigned long long*>(sp);
+        w.levelModes = ib + 5 * c + 2 + 2 * ntiles + 1;
     }
     uint8_t* bb = nullptr;
     CUDA_TRY(h, cudaMalloc(&bb, 3 * c + 64));

@@ -52,6 +52,7 @@ struct Work {
     int* tileOff;
     int* status;     // first error code
     unsigned long long* scanState;  // look-back tile states (2*ntiles) + 2 tickets
+    int* levelModes;  // bit0: level has lane-per-root merges, bit1: warp-per-root merges
     unsigned long long* counters;  // [0] evals
 };
 

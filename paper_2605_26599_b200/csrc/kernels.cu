@@ -466,6 +466,20 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, in
     if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= NN) w.survPre[NN] = base + tot;
 }
 
+// Which secular tiers a level needs (merges with K > 0): bit0 lane-per-root,
+// bit1 warp-per-root.  Kernels of an absent tier exit on their first load.
+__global__ void k_level_modes(Work w, LevelDev L) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    int bits = 0;
+    if (m < L.M) {
+        const int off = L.mOff[m];
+        const int K = w.survPre[w.nnPre[off + L.mSize[m]]] - w.survPre[w.nnPre[off]];
+        if (K > 0) bits = split_mode(L.mSize[m], K) ? 2 : 1;
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if ((threadIdx.x & 31) == 0 && bits) atomicOr(w.levelModes, bits);
+}
+
 constexpr int kSecBlock = 128;
 constexpr int kWin = 1024;
 
@@ -512,11 +526,13 @@ constexpr int kSecWinQ = BRGPU_SEC_WIN;
 __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, LevelDev L, int n, int patched) {
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ int s_next;
+    if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int R = max(kSecBlock, (T + (int)gridDim.x - 1) / (int)gridDim.x);
     const int c0 = blockIdx.x * R;
     if (c0 >= T) return;  // uniform per CTA
     const int c1 = min(c0 + R, T);
+    if (!chunk_has_mode(w, L, c0, c1, false)) return;  // all roots belong to warp.cu
     const Window win = range_window(w, L, c0, c1, kSecWinQ);
     if (!win.fits) return;  // large-K chunk: k_secular_tiled (tiled.cu) owns it
     for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock)
@@ -608,6 +624,7 @@ __global__ void k_selftest_rcp(long long count, unsigned long long seed, unsigne
 // order, so the product order is the checker's.
 __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
     __shared__ double s_dorg[kWin], s_tau[kWin], s_dj[kWin];
+    if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int g0 = blockIdx.x * kSecBlock;
     if (g0 >= T) return;  // uniform per CTA
@@ -627,6 +644,7 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
     }
     double prod = 1.0;
     unsigned minexp = 0x7ff00000u;
+    if (!__syncthreads_or(act)) return;
     for (int tlo = win.P0; tlo < win.P1; tlo += kWin) {
         const int thi = min(tlo + kWin, win.P1);
         __syncthreads();
@@ -673,6 +691,7 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
 // r0, r1) stream through shared memory in tiles, in pole order.
 __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
     __shared__ double s_d[kWin], s_zh[kWin], s_r0[kWin], s_r1[kWin];
+    if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int g0 = blockIdx.x * kSecBlock;
     if (g0 >= T) return;  // uniform per CTA
@@ -686,6 +705,7 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
         active_range(w, L, w.aMerge[g], a0, a1);
         if (split_mode(L.mSize[w.aMerge[g]], a1 - a0)) act = false;
     }
+    if (!__syncthreads_or(act)) return;
     if (act) {
         const int m = w.aMerge[g];
         int ke;
@@ -704,6 +724,7 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
     }
     double nn = 0.0, s0 = 0.0, s1 = 0.0;
     unsigned minexp = 0x7ff00000u;
+    if (!__syncthreads_or(act)) return;
     for (int tlo = win.P0; tlo < win.P1; tlo += kWin) {
         const int thi = min(tlo + kWin, win.P1);
         __syncthreads();
@@ -915,11 +936,13 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
     PMARK(BRGPU_K_WALK);
     k_surv_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, st2, tk + 1);
     PMARK(BRGPU_K_SURVWRITE);
+    cudaMemsetAsync(w.levelModes, 0, sizeof(int), s);
+    k_level_modes<<<cdiv(L.M, 256), 256, 0, s>>>(w, L);
     k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
     launch_secular_tiled(s, w, L, n, prm);
     launch_secular_warp(s, w, L, n, prm);
     PMARK(BRGPU_K_SECULAR);
-    int nl = 7;  // scatter, nn_scan, walk, surv_scan + 3 secular tiers
+    int nl = 8;  // scatter, nn_scan, walk, surv_scan, modes + 3 secular tiers
     if (prm.zhat) {
         k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
         launch_zhat_warp(s, w, L, n, prm);

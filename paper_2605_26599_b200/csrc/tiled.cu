@@ -33,12 +33,14 @@ __global__ void __launch_bounds__(kTiledThreads, 2)
 k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
     __shared__ double2 s_tile[2][kTile2];
     __shared__ int s_next;
+    if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int R = max(kSecChunkBlock, (T + G - 1) / G);
     // this kernel's grid covers the same G chunks; CTA b owns chunk b
     const int c0 = blockIdx.x * R;
     if (c0 >= T) return;
     const int c1 = min(c0 + R, T);
+    if (!chunk_has_mode(w, L, c0, c1, false)) return;
     int a0, a1, b0, b1;
     {
         const int m0 = w.aMerge[c0], m1 = w.aMerge[c1 - 1];

@@ -40,12 +40,14 @@ __device__ __forceinline__ int strided_start(int lo, int ks, int lane) {
 __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelDev L, int n, int patched) {
     __shared__ double2 s_tile[2][kWarpTile];
     __shared__ int s_next;
+    if (!(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int G = (int)gridDim.x;
     const int R = max(kWarpThreads / 32, (T + G - 1) / G);
     const int c0 = blockIdx.x * R;
     if (c0 >= T) return;
     const int c1 = min(c0 + R, T);
+    if (!chunk_has_mode(w, L, c0, c1, true)) return;
     int P0, P1, tmp;
     merge_active(w, L, w.aMerge[c0], P0, tmp);
     merge_active(w, L, w.aMerge[c1 - 1], tmp, P1);
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, int n) {
     __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
+    if (!(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {  // uniform per CTA
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
     __shared__ double s_d[kWarpTile], s_zh[kWarpTile], s_r0[kWarpTile], s_r1[kWarpTile];
+    if (!(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {
