@@ -234,7 +234,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
     s.set_trace(False)
     solve()
     launches = s.stats()["kernel_launches"]
-    prof = s.profile_kernels(td, te) if (not batch and world == 1) else {}
+    prof = s.profile_kernels(td, te, batch) if world == 1 else {}
 
     # --- timed region: K steps, L2 flushed before each, device time per step
     sampler = ClockSampler(dev)

@@ -286,14 +286,20 @@ class Solver:
         self._lib.brgpu_get_timing(self._h, C.byref(t))
         return {"device_ms": t.device_ms, "pre_ms": t.pre_ms, "main_ms": t.main_ms}
 
-    def profile_kernels(self, d, e) -> dict:
-        """Kernel-by-kernel profile of one solve of device-resident torch tensors:
+    def profile_kernels(self, d, e, batch: int = 0) -> dict:
+        """Kernel-by-kernel profile of one solve of device-resident torch tensors
+        (a batch of ``batch`` matrices when batch > 0; d is then (batch, n)):
         {class: (total_ms, launches)} from CUDA events on the handle's stream."""
-        n = d.numel()
         ms = (C.c_double * _native.NCLASS)()
         cnt = (C.c_int32 * _native.NCLASS)()
-        rc = self._lib.brgpu_profile_kernels(self._h, n, d.data_ptr(), e.data_ptr() if n > 1 else None,
-                                             ms, cnt)
+        if batch:
+            n = d.numel() // batch
+            rc = self._lib.brgpu_profile_kernels_batched(self._h, batch, n, d.data_ptr(),
+                                                         e.data_ptr() if n > 1 else None, ms, cnt)
+        else:
+            n = d.numel()
+            rc = self._lib.brgpu_profile_kernels(self._h, n, d.data_ptr(),
+                                                 e.data_ptr() if n > 1 else None, ms, cnt)
         if rc:
             self._fail(rc)
         return {self._lib.brgpu_kernel_class_name(c).decode(): (ms[c], cnt[c])

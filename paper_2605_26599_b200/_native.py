@@ -47,7 +47,8 @@ EXPORTS = [
     "brgpu_set_option", "brgpu_get_option", "brgpu_workspace_query", "brgpu_reserve",
     "brgpu_get_ledger", "brgpu_eigvals", "brgpu_eigvals_device", "brgpu_eigvals_batched",
     "brgpu_eigvals_batched_device", "brgpu_get_stats", "brgpu_set_trace", "brgpu_get_trace",
-    "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_kernel_class_name", "brgpu_selftest_rcp",
+    "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_profile_kernels_batched",
+    "brgpu_kernel_class_name", "brgpu_selftest_rcp",
     "brgpu_nccl_unique_id", "brgpu_create_distributed", "brgpu_plan_owned", "brgpu_version",
 ]
 
@@ -90,6 +91,8 @@ def lib() -> C.CDLL:
     L.brgpu_get_timing.argtypes = [hp, C.POINTER(Timing)]
     L.brgpu_profile_kernels.argtypes = [hp, C.c_int64, _dp, _dp, C.POINTER(C.c_double),
                                         C.POINTER(C.c_int32)]
+    L.brgpu_profile_kernels_batched.argtypes = [hp, C.c_int64, C.c_int64, _dp, _dp,
+                                                C.POINTER(C.c_double), C.POINTER(C.c_int32)]
     L.brgpu_kernel_class_name.argtypes = [C.c_int]
     L.brgpu_kernel_class_name.restype = C.c_char_p
     L.brgpu_selftest_rcp.argtypes = [hp, C.c_int64, C.c_uint64, C.POINTER(C.c_uint64)]

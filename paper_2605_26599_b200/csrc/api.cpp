@@ -1060,14 +1060,15 @@ const char* brgpu_kernel_class_name(int c) {
     return (c >= 0 && c < BRGPU_NCLASS) ? names[c] : "?";
 }
 
-int brgpu_profile_kernels(brgpu_handle* hh, int64_t n, const double* d, const double* e,
-                          double* class_ms, int32_t* class_launches) {
+static int profile_impl(brgpu_handle* hh, int64_t batch, int64_t n, const double* d, const double* e,
+                        double* class_ms, int32_t* class_launches) {
     if (!hh || !class_ms || !class_launches) return BRGPU_ERR_INVALID_ARGUMENT;
     Handle* h = &hh->h;
     CUDA_TRY(h, cudaSetDevice(h->device));
     Prof prof;
     h->prof = &prof;
-    const int r = solve_device(h, n, d, e, h->w.lam, false);
+    const int r = batch ? brgpu_eigvals_batched_device(hh, batch, n, d, e, h->w.lam, nullptr)
+                        : solve_device(h, n, d, e, h->w.lam, false);
     h->prof = nullptr;
     for (int c = 0; c < BRGPU_NCLASS; ++c) { class_ms[c] = 0.0; class_launches[c] = 0; }
     if (r == BRGPU_OK) {
@@ -1081,6 +1082,17 @@ int brgpu_profile_kernels(brgpu_handle* hh, int64_t n, const double* d, const do
     }
     for (auto e2 : prof.ev) cudaEventDestroy(e2);
     return r;
+}
+
+int brgpu_profile_kernels(brgpu_handle* hh, int64_t n, const double* d, const double* e,
+                          double* class_ms, int32_t* class_launches) {
+    return profile_impl(hh, 0, n, d, e, class_ms, class_launches);
+}
+
+int brgpu_profile_kernels_batched(brgpu_handle* hh, int64_t batch, int64_t n, const double* d,
+                                  const double* e, double* class_ms, int32_t* class_launches) {
+    if (batch <= 0) return BRGPU_ERR_INVALID_ARGUMENT;
+    return profile_impl(hh, batch, n, d, e, class_ms, class_launches);
 }
 
 int brgpu_selftest_rcp(brgpu_handle* hh, int64_t count, uint64_t seed, uint64_t* mismatches) {

@@ -225,6 +225,12 @@ __global__ void k_cuts(int ncut, const int* __restrict__ cutPos, const double* _
 // sweeps are a serial chain of dependent loads/stores, so they must hit SMEM
 // latency, not L1-thrashing local memory (4 x MAXM doubles per thread).
 constexpr int kLeafThreads = 64;
+// per-thread SMEM doubles: d[MAXM], e[MAXM-1] (e[m-1] is never read), r0, r1.
+// At MAXM = 16 this is 63 doubles = 32256 B per 64-thread CTA, so 7 CTAs fit in
+// one SM (7 x (32256 + 1024 reserved) <= 233472 B) and the 65536 leaves of an
+// n = 2^20 problem (1024 CTAs <= 7 x 148) run in ONE wave instead of two.
+template <int MAXM>
+constexpr int leaf_smem_bytes() { return (4 * MAXM - 1) * kLeafThreads * (int)sizeof(double); }
 
 template <int MAXM>
 __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __restrict__ tOff,
@@ -244,11 +250,11 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __r
     constexpr int S = kLeafThreads;
     const Strided<S> d{leaf_sm + threadIdx.x};
     const Strided<S> e{leaf_sm + MAXM * S + threadIdx.x};
-    const Strided<S> r0{leaf_sm + 2 * MAXM * S + threadIdx.x};
-    const Strided<S> r1{leaf_sm + 3 * MAXM * S + threadIdx.x};
+    const Strided<S> r0{leaf_sm + (2 * MAXM - 1) * S + threadIdx.x};
+    const Strided<S> r1{leaf_sm + (3 * MAXM - 1) * S + threadIdx.x};
     for (int i = 0; i < m; ++i) {
         d[i] = dw[off + i];
-        e[i] = (i + 1 < m) ? ew[off + i] : 0.0;
+        if (i + 1 < m) e[i] = ew[off + i];
         r0[i] = 0.0;
         r1[i] = 0.0;
     }
@@ -862,10 +868,8 @@ int selftest_rcp(long long count, unsigned long long seed, unsigned long long* h
 int sec_ctas_per_sm() { return BRGPU_SEC_MINB; }
 
 void init_kernel_attributes() {
-    cudaFuncSetAttribute(k_leaf<26>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4 * 26 * kLeafThreads * (int)sizeof(double));
-    cudaFuncSetAttribute(k_leaf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4 * 32 * kLeafThreads * (int)sizeof(double));
+    cudaFuncSetAttribute(k_leaf<26>, cudaFuncAttributeMaxDynamicSharedMemorySize, leaf_smem_bytes<26>());
+    cudaFuncSetAttribute(k_leaf<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, leaf_smem_bytes<32>());
 }
 
 void launch_copy_input(cudaStream_t s, int n, const double* d, const double* e, double* dw,
@@ -903,15 +907,15 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
     if (ntask <= 0) return;
     const int grid = cdiv(ntask, kLeafThreads);
     if (maxm <= 16) {
-        const size_t sm = 4 * 16 * kLeafThreads * sizeof(double);
+        const size_t sm = leaf_smem_bytes<16>();
         k_leaf<16><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
     } else if (maxm <= 26) {
-        const size_t sm = 4 * 26 * kLeafThreads * sizeof(double);
+        const size_t sm = leaf_smem_bytes<26>();
         k_leaf<26><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
     } else {
-        const size_t sm = 4 * 32 * kLeafThreads * sizeof(double);
+        const size_t sm = leaf_smem_bytes<32>();
         k_leaf<32><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
     }
