@@ -963,13 +963,19 @@ static int solve_impl(int64_t n, const double* d, const double* e, double* w, co
         if (fabs(e[i]) <= U_RND * (fabs(d[i]) + fabs(d[i + 1]))) bstart[nblk++] = i + 1;
     bstart[nblk] = n;
 
-    /* scale each block by max(|d|,|e|,1) and build its tree */
+    /* scale each block by max(|d|,|e|,1) and build its tree.
+     * GPU mode also lifts TINY blocks (max < 2^-500) by the power of two
+     * 2^ilogb(max): exact, and it keeps y = zhat/Delta and its square from
+     * overflowing when every pole gap is below ~1e-154 (the reference's
+     * max(.,1) never enlarges, so such blocks end in inf/NaN there). */
     int32_t height = 0;
     for (int64_t b = 0; b < nblk; ++b) {
         const int64_t off = bstart[b], sz = bstart[b + 1] - off;
-        double s = 1.0;
-        for (int64_t i = 0; i < sz; ++i) s = fmax(s, fabs(d[off + i]));
-        for (int64_t i = 0; i + 1 < sz; ++i) s = fmax(s, fabs(e[off + i]));
+        double mx = 0.0;
+        for (int64_t i = 0; i < sz; ++i) mx = fmax(mx, fabs(d[off + i]));
+        for (int64_t i = 0; i + 1 < sz; ++i) mx = fmax(mx, fabs(e[off + i]));
+        double s = fmax(1.0, mx);
+        if (!o->ref_arith && mx > 0.0 && mx < 0x1p-500) s = ldexp(1.0, ilogb(mx));
         scale[b] = s;
         for (int64_t i = 0; i < sz; ++i) dw[off + i] = d[off + i] / s;
         for (int64_t i = 0; i + 1 < sz; ++i) ew[off + i] = e[off + i] / s;

@@ -132,6 +132,7 @@ class BrOptions:
     use_graph: bool = True
     subtree: bool = True
     virtual_ranks: int = 1  # >1: run the multi-GPU decomposition on this device (test mode)
+    exact_passes: bool = False  # test hook: every pole pass through the exact-reciprocal path
 
 
 @dataclass
@@ -190,6 +191,7 @@ class Solver:
         self._opt(_native.OPT_PATCHED_STOP, int(o.patched_stop))
         self._opt(_native.OPT_USE_GRAPH, int(o.use_graph))
         self._opt(_native.OPT_SUBTREE, int(o.subtree))
+        self._opt(_native.OPT_EXACT_PASSES, int(o.exact_passes))
         if self.nranks == 1:
             self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o

@@ -20,6 +20,7 @@ OPT_PATCHED_STOP = 3
 OPT_USE_GRAPH = 4
 OPT_SUBTREE = 5
 OPT_VIRTUAL_RANKS = 6
+OPT_EXACT_PASSES = 7
 
 
 class Stats(C.Structure):

@@ -127,6 +127,7 @@ struct Handle {
     int patched = 1;
     int use_graph = 1;
     int subtree = 1;
+    int exact = 0;
     int trace = 0;
     double tol_scale = 1.0;
     std::string err;
@@ -425,6 +426,7 @@ int ensure_work(Handle* h, int64_t n) {
     double* dbl = nullptr;
     CUDA_TRY(h, cudaMalloc(&dbl, sizeof(double) * nd));
     Work& w = h->w;
+    w.exact = h->exact;
     w.dw = dbl; w.ew = dbl + c; w.lam = dbl + 2 * c; w.blo = dbl + 3 * c; w.bhi = dbl + 4 * c;
     w.D = dbl + 5 * c; w.Z = dbl + 6 * c; w.R0 = dbl + 7 * c; w.R1 = dbl + 8 * c;
     w.dA = dbl + 9 * c; w.zA = dbl + 10 * c; w.z2A = dbl + 11 * c; w.r0A = dbl + 12 * c;
@@ -608,6 +610,7 @@ int ensure_buf_sizes(Handle* h, Plan* p);
 int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::vector<int>& segs) {
     const int P = h->virt;
     cudaStream_t s = h->stream;
+    CUDA_TRY(h, cudaEventRecord(h->tev[2], s));
     while ((int)h->subs.size() < P) {
         auto sub = std::make_unique<Handle>();
         sub->device = h->device;
@@ -619,7 +622,7 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
     for (int k = 0; k < P; ++k) {
         Handle* u = h->subs[(size_t)k].get();
         u->leaf_cutoff = h->leaf_cutoff; u->zhat = h->zhat; u->patched = h->patched;
-        u->use_graph = 0; u->subtree = h->subtree; u->trace = 0; u->tol_scale = h->tol_scale;
+        u->use_graph = 0; u->subtree = h->subtree; u->trace = 0; u->exact = h->exact; u->w.exact = h->exact; u->tol_scale = h->tol_scale;
         u->sec_grid = h->sec_grid;
         if (int r = ensure_work(u, n)) return fail(h, r, u->err);
         u->w.status = h->w.status;
@@ -647,6 +650,8 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
     int launches = 0;
     run_stage_b(h->subs[0].get(), plans[0].get(), &launches, nullptr);
     CUDA_TRY(h, cudaMemcpyAsync(h->w.lam, h->subs[0]->w.lam, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(h, cudaEventRecord(h->tev[3], s));
+    CUDA_TRY(h, cudaGetLastError());
     CUDA_TRY(h, cudaStreamSynchronize(s));
     for (auto& pl : plans) free_plan(pl.get());
     h->stats.n = n;
@@ -741,9 +746,11 @@ int finish_solve(Handle* h) {
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
     {
+        // both pairs are recorded on every path; a failure here must not leave a
+        // pending error for the next CUDA_TRY (of this or any other handle)
         float a = 0.f, b = 0.f;
-        cudaEventElapsedTime(&a, h->tev[0], h->tev[1]);
-        cudaEventElapsedTime(&b, h->tev[2], h->tev[3]);
+        if (cudaEventElapsedTime(&a, h->tev[0], h->tev[1]) != cudaSuccess) { a = 0.f; cudaGetLastError(); }
+        if (cudaEventElapsedTime(&b, h->tev[2], h->tev[3]) != cudaSuccess) { b = 0.f; cudaGetLastError(); }
         h->timing.pre_ms = a;
         h->timing.main_ms = b;
         h->timing.device_ms = (double)a + (double)b;
@@ -914,6 +921,11 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
         case BRGPU_OPT_PATCHED_STOP: h->patched = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
         case BRGPU_OPT_USE_GRAPH: h->use_graph = v != 0; return BRGPU_OK;
         case BRGPU_OPT_SUBTREE: h->subtree = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        case BRGPU_OPT_EXACT_PASSES:
+            h->exact = v != 0;
+            h->w.exact = h->exact;
+            if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
+            return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -933,6 +945,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_USE_GRAPH: *v = h->use_graph; return BRGPU_OK;
         case BRGPU_OPT_SUBTREE: *v = h->subtree; return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS: *v = h->virt; return BRGPU_OK;
+        case BRGPU_OPT_EXACT_PASSES: *v = h->exact; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }
 }

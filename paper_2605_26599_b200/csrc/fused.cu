@@ -276,6 +276,8 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
 
     // ---- secular roots: per-lane RootSM, CTA queue --------------------------
     {
+        // per-thread prefix snapshot slot; S.Z is dead between compaction and sDorg
+        double2* snap = reinterpret_cast<double2*>(S.Z) + tid;
         RootSM st;
         int g = -1, ks = 0;
         bool exhausted = false;
@@ -300,8 +302,10 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
                 double sum, sum_abs, sum_d, psi;
                 bool pole = false;
                 const SmemPairs P{pairs + ks};
-                const bool ok = eval_pass(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
-                if (!ok) pole = eval_pass_exact(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+                if (!w.exact && eval_guard(P, st.K, st.j, st.dorg, st.tau))
+                    eval_fast(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi, snap);
+                else
+                    pole = eval_pass_exact(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
                 Ev ev;
                 ev.f = 1.0 + st.rho * sum;
                 ev.fp = st.rho * sum_d;
@@ -346,16 +350,16 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
             const double di = pairs[g].x;
             double prod = 1.0;
-            unsigned minexp = 0x7ff00000u;
+            const bool fast = !w.exact && zhat_guard(PolesPairs{pairs + ks}, K, i);
+            if (fast) {
 #pragma unroll 4
-            for (int j = 0; j < K; ++j) {
-                const double del = (di - sDorg[ks + j]) - S.tau[ks + j];
-                const double dd = di - pairs[ks + j].x;
-                if (j != i) minexp = min(minexp, expfield(dd));
-                const double f = (j == i) ? del : del * rcp_nr(dd);
-                prod = prod * f;
-            }
-            if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {
+                for (int j = 0; j < K; ++j) {
+                    const double del = (di - sDorg[ks + j]) - S.tau[ks + j];
+                    const double dd = di - pairs[ks + j].x;
+                    const double f = (j == i) ? del : del * rcp_nr(dd);
+                    prod = prod * f;
+                }
+            } else {
                 prod = 1.0;
                 for (int j = 0; j < K; ++j) {
                     const double del = (di - pairs[ks + S.org[ks + j]].x) - S.tau[ks + j];
@@ -388,17 +392,15 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
         w.lam[p] = lam;
         if (S.mf[t] & kMergeRoot) continue;
         double nn = 0.0, s0 = 0.0, s1 = 0.0;
-        unsigned minexp = 0x7ff00000u;
+        if (!w.exact && eval_guard(SmemPairs{pairs + ks}, K, j, dorg, tau)) {
 #pragma unroll 4
-        for (int i = 0; i < K; ++i) {
-            const double del = (pairs[ks + i].x - dorg) - tau;
-            minexp = min(minexp, expfield(del));
-            const double y = zA[ks + i] * rcp_nr(del);
-            nn = __fma_rn(y, y, nn);
-            s0 = __fma_rn(S.r0A[ks + i], y, s0);
-            s1 = __fma_rn(S.r1A[ks + i], y, s1);
-        }
-        if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {
+            for (int i = 0; i < K; ++i) {
+                const double y = zA[ks + i] * rcp_nr((pairs[ks + i].x - dorg) - tau);
+                nn = __fma_rn(y, y, nn);
+                s0 = __fma_rn(S.r0A[ks + i], y, s0);
+                s1 = __fma_rn(S.r1A[ks + i], y, s1);
+            }
+        } else {
             bool zero = false;
             nn = 0.0; s0 = 0.0; s1 = 0.0;
             for (int i = 0; i < K; ++i) {

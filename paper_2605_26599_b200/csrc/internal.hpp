@@ -54,6 +54,7 @@ struct Work {
     unsigned long long* scanState;  // look-back tile states (2*ntiles) + 2 tickets
     int* levelModes;  // bit0: level has lane-per-root merges, bit1: warp-per-root merges
     unsigned long long* counters;  // [0] evals
+    int exact;       // test hook (BRGPU_OPT_EXACT_PASSES): every pole pass takes the exact path
 };
 
 // One level's merges (device pointers into the plan arrays).

@@ -194,13 +194,22 @@ __global__ void k_block_scale(int n, const double* __restrict__ d, const double*
 }
 
 // in place: dw /= s, ew /= s inside the block, 0 at block boundaries
+// Block scale: max(1, |d|, |e|); tiny blocks (max < 2^-500) are
+// lifted by the power of two 2^ilogb(max) instead -- exact, and it keeps the
+// boundary-row sums from overflowing (the checker's GPU-mode rule).
+__device__ __forceinline__ double block_scale_of(unsigned long long bits) {
+    const double mx = __longlong_as_double((long long)bits);
+    if (mx > 0.0 && mx < 0x1p-500) return ldexp(1.0, ilogb(mx));
+    return fmax(1.0, mx);
+}
+
 __global__ void k_apply_scale(int n, const int* __restrict__ bstart, int nblk,
                               const unsigned long long* __restrict__ sbits,
                               double* __restrict__ dw, double* __restrict__ ew) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
-    const double s = fmax(1.0, __longlong_as_double((long long)sbits[b]));
+    const double s = block_scale_of(sbits[b]);
     dw[i] = dw[i] / s;
     ew[i] = (i + 1 < bstart[b + 1]) ? ew[i] / s : 0.0;
 }
@@ -531,6 +540,7 @@ constexpr int kSecWinQ = BRGPU_SEC_WIN;
 // shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
 __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, LevelDev L, int n, int patched) {
     __shared__ double2 s_dz[kSecWinQ];
+    __shared__ double2 s_snap[kSecBlock];
     __shared__ int s_next;
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -575,8 +585,10 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
             bool pole = false;
             const int K = st.K;
             const SmemPairs P{s_dz + (ks - win.P0)};
-            const bool ok = eval_pass(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
-            if (!ok) pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+            if (!w.exact && eval_guard(P, K, st.j, st.dorg, st.tau))
+                eval_fast(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi, s_snap + threadIdx.x);
+            else
+                pole = eval_pass_exact(P, K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
             Ev ev;
             ev.f = 1.0 + st.rho * sum;
             ev.fp = st.rho * sum_d;
@@ -649,8 +661,8 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
         di = w.dA[g];
     }
     double prod = 1.0;
-    unsigned minexp = 0x7ff00000u;
     if (!__syncthreads_or(act)) return;
+    const bool fast = act && !w.exact && zhat_guard(PolesPtr{w.dA + ks}, K, i);
     for (int tlo = win.P0; tlo < win.P1; tlo += kWin) {
         const int thi = min(tlo + kWin, win.P1);
         __syncthreads();
@@ -662,21 +674,19 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
             s_dj[r - tlo] = w.dA[r];
         }
         __syncthreads();
-        if (act) {
+        if (fast) {
             const int jlo = max(ks, tlo), jhi = min(ks + K, thi);
             for (int jg = jlo; jg < jhi; ++jg) {
                 const int t = jg - tlo;
                 const double del = (di - s_dorg[t]) - s_tau[t];
                 const double dd = di - s_dj[t];
-                const bool self = (jg - ks) == i;
-                if (!self) minexp = min(minexp, expfield(dd));
-                const double f = self ? del : del * rcp_nr(dd);
+                const double f = ((jg - ks) == i) ? del : del * rcp_nr(dd);
                 prod = prod * f;
             }
         }
     }
     if (!act) return;
-    if (minexp < kRcpMinExp || (minexp == 0x7ff00000u && K > 1)) {  // exact redo (global memory)
+    if (!fast) {  // exact redo (global memory)
         const double* __restrict__ dA = w.dA + ks;
         const double* __restrict__ tau = w.tau + ks;
         const int* __restrict__ org = w.org + ks;
@@ -729,8 +739,8 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
         if (L.mFlags[m] & kMergeRoot) act = false;
     }
     double nn = 0.0, s0 = 0.0, s1 = 0.0;
-    unsigned minexp = 0x7ff00000u;
     if (!__syncthreads_or(act)) return;
+    const bool fast = act && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, g - ks, dorg, tau);
     for (int tlo = win.P0; tlo < win.P1; tlo += kWin) {
         const int thi = min(tlo + kWin, win.P1);
         __syncthreads();
@@ -741,13 +751,11 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
             s_r1[r - tlo] = w.r1A[r];
         }
         __syncthreads();
-        if (act) {
+        if (fast) {
             const int ilo = max(ks, tlo) - tlo, ihi = min(ks + K, thi) - tlo;
 #pragma unroll 4
             for (int t = ilo; t < ihi; ++t) {
-                const double del = (s_d[t] - dorg) - tau;
-                minexp = min(minexp, expfield(del));
-                const double y = s_zh[t] * rcp_nr(del);
+                const double y = s_zh[t] * rcp_nr((s_d[t] - dorg) - tau);
                 nn = __fma_rn(y, y, nn);
                 s0 = __fma_rn(s_r0[t], y, s0);
                 s1 = __fma_rn(s_r1[t], y, s1);
@@ -755,7 +763,7 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
         }
     }
     if (!act) return;
-    if (minexp < kRcpMinExp || minexp == 0x7ff00000u) {  // exact redo; a zero delta is an error
+    if (!fast) {  // exact redo; a zero delta is an error
         const double* __restrict__ dA = w.dA + ks;
         const double* __restrict__ zh = w.zA + ks;
         const double* __restrict__ r0 = w.r0A + ks;
@@ -824,7 +832,7 @@ __global__ void k_rescale(int n, const int* __restrict__ bstart, int nblk,
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
-    const double s = fmax(1.0, __longlong_as_double((long long)sbits[b]));
+    const double s = block_scale_of(sbits[b]);
     lam[i] = lam[i] * s;
 }
 

@@ -32,6 +32,7 @@ __device__ __forceinline__ void tile_load(double2* dst, const double* __restrict
 __global__ void __launch_bounds__(kTiledThreads, 2)
 k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
     __shared__ double2 s_tile[2][kTile2];
+    __shared__ double2 s_snap[kTiledThreads];
     __shared__ int s_next;
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -82,42 +83,54 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
         const bool need = g >= 0;
         if (!__syncthreads_or(need)) break;
         // one CTA-synchronous evaluation pass over the window
-        double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi = 0.0, psum = 0.0;
-        unsigned minexp = 0x7ff00000u;
+        double sum = 0.0, sum_abs = 0.0, sum_d = 0.0, psi = 0.0;
         const int K = need ? st.K : 0;
         const int j = st.j;
         const double dorg = st.dorg, tau = st.tau;
+        const bool fast = need && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(s_snap + threadIdx.x);
+        snap_if(sa, 0, j < 0 ? 0 : 1, 0.0, 0.0);
         int buf = 0;
         tile_load(s_tile[0], w.dA, w.z2A, P0, min(P0 + kTile2, P1));
         for (int tlo = P0; tlo < P1; tlo += kTile2) {
             const int thi = min(tlo + kTile2, P1);
             __syncthreads();  // tile `buf` complete; previous readers of buf^1 done
             if (thi < P1) tile_load(s_tile[buf ^ 1], w.dA, w.z2A, thi, min(thi + kTile2, P1));
-            if (need) {
+            if (fast) {
                 const int ilo = max(ks, tlo), ihi = min(ks + K, thi);
                 const double2* __restrict__ tp = s_tile[buf] - tlo;
-#pragma unroll 4
-                for (int i = ilo; i < ihi; ++i) {
-                    const double2 dz = tp[i];
-                    const double del = (dz.x - dorg) - tau;
-                    minexp = min(minexp, expfield(del));
-                    const double r = rcp_nr(del);
+                const int jg = ks + j;
+                auto term = [&](double2 dz, int i) {
+                    const double r = rcp_nr((dz.x - dorg) - tau);
                     const double t = dz.y * r;
                     sum += t;
                     sum_d += t * r;
-                    if (i - ks == j) { psi = sum_d; psum = sum; }
+                    snap_if(sa, i, jg, sum, sum_d);
+                };
+                int i = ilo;
+                for (; i + 4 <= ihi; i += 4) {
+                    const double2 a0 = tp[i], a1 = tp[i + 1], a2 = tp[i + 2], a3 = tp[i + 3];
+                    term(a0, i);
+                    term(a1, i + 1);
+                    term(a2, i + 2);
+                    term(a3, i + 3);
                 }
+                for (; i < ihi; ++i) term(tp[i], i);
             }
             buf ^= 1;
         }
         __syncthreads();
         bool pole = false;
         if (need) {
-            if (j >= K) { psi = sum_d; psum = sum; }
-            sum_abs = sum - 2.0 * psum;  // term signs are fixed by the bracket
-            if (minexp < kRcpMinExp || minexp == 0x7ff00000u)  // rare: exact pass from global memory
+            if (fast) {
+                snap_if(sa, 0, j >= K ? 0 : 1, sum, sum_d);
+                const double2 sn = ld_snap(sa);
+                psi = sn.y;
+                sum_abs = sum - 2.0 * sn.x;  // term signs are fixed by the bracket
+            } else {  // rare: exact pass from global memory
                 pole = eval_pass_exact(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau, sum, sum_abs,
                                        sum_d, psi);
+            }
             Ev ev;
             ev.f = 1.0 + st.rho * sum;
             ev.fp = st.rho * sum_d;

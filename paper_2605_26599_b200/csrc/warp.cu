@@ -87,10 +87,12 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
         const bool need = g >= 0;
         if (!__syncthreads_or(need)) break;
         double sum = 0.0, sum_d = 0.0, psi = 0.0, psum = 0.0;
-        unsigned minexp = 0x7ff00000u;
         const int K = need ? st.K : 0;
         const int j = st.j;
         const double dorg = st.dorg, tau = st.tau;
+        // neighbour range guard (eval_guard, numerics.cuh); on failure the warp
+        // skips the fast pass and runs the exact one below
+        const bool fast = need && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau);
         int buf = 0;
         for (int i = P0 + (int)threadIdx.x; i < min(P0 + kWarpTile, P1); i += kWarpThreads)
             s_tile[0][i - P0] = make_double2(w.dA[i], w.z2A[i]);
@@ -100,29 +102,38 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
             if (thi < P1)
                 for (int i = thi + (int)threadIdx.x; i < min(thi + kWarpTile, P1); i += kWarpThreads)
                     s_tile[buf ^ 1][i - thi] = make_double2(w.dA[i], w.z2A[i]);
-            if (need) {
+            if (fast) {
                 const int lo = max(ks, tlo), hi = min(ks + K, thi);
                 const double2* __restrict__ tp = s_tile[buf] - tlo;
+                // terms i <= j, then the prefix snapshot, then i > j: a lane's
+                // strided terms are split at one point, so the two loops differ
+                // across lanes by at most one trip (no per-term snapshot selects)
+                const int mid = min(hi, ks + j + 1);
+                int i = strided_start(lo, ks, lane);
 #pragma unroll 4
-                for (int i = strided_start(lo, ks, lane); i < hi; i += 32) {
+                for (; i < mid; i += 32) {
                     const double2 dz = tp[i];
-                    const double del = (dz.x - dorg) - tau;
-                    minexp = min(minexp, expfield(del));
-                    const double r = rcp_nr(del);
+                    const double r = rcp_nr((dz.x - dorg) - tau);
                     const double t = dz.y * r;
                     sum += t;
                     sum_d += t * r;
-                    if (i - ks <= j) { psi = sum_d; psum = sum; }
+                }
+                if (lo < mid) { psi = sum_d; psum = sum; }
+#pragma unroll 4
+                for (; i < hi; i += 32) {
+                    const double2 dz = tp[i];
+                    const double r = rcp_nr((dz.x - dorg) - tau);
+                    const double t = dz.y * r;
+                    sum += t;
+                    sum_d += t * r;
                 }
             }
             buf ^= 1;
         }
         __syncthreads();
         if (need) {
-            // lanes without terms have minexp = 0x7ff00000 (neutral for min)
-            const unsigned mx = bfly_min(minexp);
             bool pole = false;
-            if (mx < kRcpMinExp) {  // rare: exact strided pass from global memory
+            if (!fast) {  // rare: exact strided pass from global memory
                 sum = 0.0; sum_d = 0.0; psi = 0.0; psum = 0.0;
                 for (int i = ks + lane; i < ks + K; i += 32) {
                     const double del = (w.dA[i] - dorg) - tau;
@@ -190,7 +201,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
         merge_active(w, L, w.aMerge[base], P0, tmp);
         merge_active(w, L, w.aMerge[gl], tmp, P1);
         double prod = 1.0;
-        unsigned minexp = 0x7ff00000u;
+        const bool fast = act && !w.exact && zhat_guard(PolesPtr{w.dA + ks}, K, i);
         for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
             const int thi = min(tlo + kWarpTile, P1);
             __syncthreads();
@@ -202,22 +213,31 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
                 s_dj[r - tlo] = w.dA[r];
             }
             __syncthreads();
-            if (act) {
+            if (fast) {
+                // roots before the pole, the pole's own factor, roots after:
+                // one split point per lane, so no per-term self select
                 const int lo = max(ks, tlo), hi = min(ks + K, thi);
-                for (int jg = strided_start(lo, ks, lane); jg < hi; jg += 32) {
+                const int mid = min(hi, ks + i);
+                int jg = strided_start(lo, ks, lane);
+#pragma unroll 4
+                for (; jg < mid; jg += 32) {
                     const int t = jg - tlo;
-                    const double del = (di - s_dorg[t]) - s_tau[t];
-                    const double dd = di - s_dj[t];
-                    const bool self = (jg - ks) == i;
-                    if (!self) minexp = min(minexp, expfield(dd));
-                    const double f = self ? del : del * rcp_nr(dd);
-                    prod = prod * f;
+                    prod = prod * (((di - s_dorg[t]) - s_tau[t]) * rcp_nr(di - s_dj[t]));
+                }
+                if (jg == ks + i && jg < hi) {
+                    const int t = jg - tlo;
+                    prod = prod * ((di - s_dorg[t]) - s_tau[t]);
+                    jg += 32;
+                }
+#pragma unroll 4
+                for (; jg < hi; jg += 32) {
+                    const int t = jg - tlo;
+                    prod = prod * (((di - s_dorg[t]) - s_tau[t]) * rcp_nr(di - s_dj[t]));
                 }
             }
         }
         if (act) {
-            const unsigned mx = bfly_min(minexp);
-            if (mx < kRcpMinExp) {  // exact redo
+            if (!fast) {  // exact redo
                 prod = 1.0;
                 for (int jg = ks + lane; jg < ks + K; jg += 32) {
                     const double del = (di - w.dA[ks + w.org[jg]]) - w.tau[jg];
@@ -271,7 +291,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
         merge_active(w, L, w.aMerge[base], P0, tmp);
         merge_active(w, L, w.aMerge[gl], tmp, P1);
         double nn = 0.0, s0 = 0.0, s1 = 0.0;
-        unsigned minexp = 0x7ff00000u;
+        const bool fast = rows && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, g - ks, dorg, tau);
         for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
             const int thi = min(tlo + kWarpTile, P1);
             __syncthreads();
@@ -282,14 +302,12 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
                 s_r1[r - tlo] = w.r1A[r];
             }
             __syncthreads();
-            if (rows) {
+            if (fast) {
                 const int lo = max(ks, tlo), hi = min(ks + K, thi);
 #pragma unroll 4
                 for (int i = strided_start(lo, ks, lane); i < hi; i += 32) {
                     const int t = i - tlo;
-                    const double del = (s_d[t] - dorg) - tau;
-                    minexp = min(minexp, expfield(del));
-                    const double y = s_zh[t] * rcp_nr(del);
+                    const double y = s_zh[t] * rcp_nr((s_d[t] - dorg) - tau);
                     nn = __fma_rn(y, y, nn);
                     s0 = __fma_rn(s_r0[t], y, s0);
                     s1 = __fma_rn(s_r1[t], y, s1);
@@ -297,8 +315,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
             }
         }
         if (rows) {
-            const unsigned mx = bfly_min(minexp);
-            if (mx < kRcpMinExp) {  // exact redo; a zero delta is an error
+            if (!fast) {  // exact redo; a zero delta is an error
                 bool zero = false;
                 nn = 0.0; s0 = 0.0; s1 = 0.0;
                 for (int i = ks + lane; i < ks + K; i += 32) {

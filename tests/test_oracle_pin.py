@@ -185,3 +185,17 @@ def test_sturm_certificate_sample():
     for i in np.linspace(0, len(w) - 1, 25).astype(int):
         assert O.sturm_count(d, e, w[i] - tol) <= i
         assert O.sturm_count(d, e, w[i] + tol) >= i + 1
+
+
+@pytest.mark.parametrize("fam,n", [("sym-uniform", 2000), ("wilkinson", 1000), ("clustered", 800)])
+@pytest.mark.parametrize("scale", [2.0 ** -1010, 2.0 ** -1040, 2.0 ** 1000])
+def test_gpu_arith_extreme_scales(fam, n, scale):
+    """GPU mode lifts tiny blocks by an exact power of two (block scale rule), so
+    tiny and huge matrices keep the relative tolerance; the reference's max(.,1)
+    rule never enlarges a block and overflows the boundary-row sums instead."""
+    d, e = G.generate(fam, n)
+    d, e = d * scale, e * scale
+    w = O.eigvals(d, e, threads=1).w
+    assert np.all(np.isfinite(w))
+    truth = sl.eigvalsh_tridiagonal(d / scale, e / scale) * scale
+    assert np.max(np.abs(w - truth)) <= G.tolerance(d, e) * (1 + 1e-12) + 64 * 2.0 ** -1074
