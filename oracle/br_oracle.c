@@ -282,19 +282,21 @@ static ev_t eval_shifted(int k, const double* d, const double* z, double rho, in
         const double del = (d[i] - dorg) - tau;
         if (del == 0.0) { r.pole = 1; return r; }
         const double zz = z[i] * z[i];
-        double term, dterm;
         if (ref) {
-            term = zz / del;
-            dterm = term / del;
+            const double term = zz / del;
+            const double dterm = term / del;
+            sum += term;
+            sum_abs += fabs(term);
+            sum_d += dterm;
+            if (i <= jsplit) { psi_d += dterm; psum = sum; }
         } else {
+            /* GPU spec: one reciprocal, t = z^2 r, f' accumulates fma(t, r, .) */
             const double rr = 1.0 / del;
-            term = zz * rr;
-            dterm = term * rr;
+            const double term = zz * rr;
+            sum += term;
+            sum_d = fma(term, rr, sum_d);
+            if (i <= jsplit) { psi_d = sum_d; psum = sum; }
         }
-        sum += term;
-        if (ref) sum_abs += fabs(term);
-        sum_d += dterm;
-        if (i <= jsplit) { psi_d += dterm; psum = sum; }
     }
     r.f = 1.0 + rho * sum;
     r.fp = rho * sum_d;
@@ -347,7 +349,7 @@ static ev_t eval_split(int k, const double* d, const double* z, double rho, int 
             const double rr = 1.0 / del;
             const double t = zz * rr;
             S[l] += t;
-            SD[l] += t * rr;
+            SD[l] = fma(t, rr, SD[l]);
             if (i <= jsplit) { PS[l] = SD[l]; PU[l] = S[l]; }
         }
     }

@@ -104,7 +104,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
                     const double r = rcp_nr((dz.x - dorg) - tau);
                     const double t = dz.y * r;
                     sum += t;
-                    sum_d += t * r;
+                    sum_d = __fma_rn(t, r, sum_d);
                     snap_if(sa, i, jg, sum, sum_d);
                 };
                 int i = ilo;

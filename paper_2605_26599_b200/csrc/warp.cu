@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
                     const double r = rcp_nr((dz.x - dorg) - tau);
                     const double t = dz.y * r;
                     sum += t;
-                    sum_d += t * r;
+                    sum_d = __fma_rn(t, r, sum_d);
                 }
                 if (lo < mid) { psi = sum_d; psum = sum; }
 #pragma unroll 4
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
                     const double r = rcp_nr((dz.x - dorg) - tau);
                     const double t = dz.y * r;
                     sum += t;
-                    sum_d += t * r;
+                    sum_d = __fma_rn(t, r, sum_d);
                 }
             }
             buf ^= 1;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
                     const double r = __drcp_rn(del);
                     const double t = w.z2A[i] * r;
                     sum += t;
-                    sum_d += t * r;
+                    sum_d = __fma_rn(t, r, sum_d);
                     if (i - ks <= j) { psi = sum_d; psum = sum; }
                 }
                 pole = __any_sync(0xffffffffu, pole);
