@@ -398,6 +398,17 @@ int bro_solve_root(int k, const double* d, const double* z, double rho, int j,
     return solve_root_impl(k, d, z, rho, j, patched, ref, 0, origin, tau_out, nevals);
 }
 
+/* GPU arithmetic: a bracket on one side of the origin spanning more than a
+ * factor 4 is bisected geometrically (sqrt(lo) sqrt(hi), same sign): the
+ * iterate reaches the root's scale in O(log log(hi/lo)) evaluations instead of
+ * halving its way down (glued Wilkinson roots within 1e-15 of a pole). */
+static inline int geo_ok(double lo, double hi) {
+    return (lo > 0.0 && hi > 4.0 * lo) || (hi < 0.0 && lo < 4.0 * hi);
+}
+static inline double geo_mid(double lo, double hi) {
+    return lo > 0.0 ? sqrt(lo) * sqrt(hi) : -(sqrt(-lo) * sqrt(-hi));
+}
+
 static int solve_root_impl(int k, const double* d, const double* z, double rho, int j, int patched,
                            int ref, int split, int* origin, double* tau_out, int* nevals) {
     int ne = 0;
@@ -458,6 +469,16 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
             }
         }
     }
+    /* GPU arithmetic, dlaed4-style model switch: the interior model is the
+     * middle way (psi'/phi' lumped on the two nearest poles, secular.cpp:172-213)
+     * or, after a slow step, the fixed-weight model (the origin pole keeps its
+     * exact weight worg = rho z_org^2, the rest of f' is lumped on the other
+     * pole).  The middle way alone converges linearly when the derivative at the
+     * origin comes from other poles of a cluster (glued Wilkinson: up to 46
+     * evaluations per root; with the safeguards below at most 19). */
+    int swtch = 0, nslow = 0;
+    double prevf = 0.0;
+    const double worg = rho * (z[org] * z[org]);
     double tau = 0.5 * (lo + hi);
     int converged = 0;
     for (int iter = 0; iter < 400; ++iter) {
@@ -481,7 +502,40 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
         const double lambda_abs = fabs(d[org] + tau);
         const double scale = patched ? fmin(lambda_abs, fabs(tau)) : lambda_abs;
         if (hi - lo <= 4.0 * U_RND * scale) { converged = 1; break; }
+        /* GPU arithmetic, slow-step safeguards (a step is slow when f kept its
+         * sign and more than a tenth of its magnitude):
+         *  - a slow step toggles the interior model (middle way / fixed weight);
+         *  - after two slow steps in a row, the origin-pole bound: f = rest +
+         *    worg/(-tau) with every term of rest increasing in tau, so an
+         *    iterate beyond the root bounds it by worg/rest on the origin side
+         *    (halved: safe while the computed rest is within a quarter of its
+         *    value, |rest| > 4 ftol), and the step bisects a one-sided bracket
+         *    spanning more than a factor 4 geometrically;
+         *  - a rejected model step bisects geometrically under the same rule.
+         * Thresholds tuned on the eval-count tails (random 2^20: the share of
+         * roots needing >= 12 evaluations is unchanged; glued Wilkinson 2^18:
+         * max 46 -> 18 evaluations). */
+        int slow = 0;
+        if (!ref) {
+            slow = iter >= 1 && ev.f * prevf > 0.0 && fabs(ev.f) > 0.1 * fabs(prevf);
+            nslow = slow ? nslow + 1 : 0;
+            if (nslow >= 2) {
+                const double rest = ev.f + worg / tau;
+                if (tau > 0.0 && ev.f > 0.0 && rest > 4.0 * ftol) {
+                    const double bnd = 0.5 * (worg / rest);
+                    if (bnd > lo && bnd < tau) lo = bnd;
+                } else if (tau < 0.0 && ev.f < 0.0 && rest < -4.0 * ftol) {
+                    const double bnd = 0.5 * (worg / rest);
+                    if (bnd < hi && bnd > tau) hi = bnd;
+                }
+            }
+            if (slow && !last) swtch = !swtch;
+            prevf = ev.f;
+        }
         double tau_next = NAN;
+        if (nslow >= 2 && geo_ok(lo, hi)) {
+            tau_next = geo_mid(lo, hi);
+        } else
         if (iter == 0 && gmode) {
             tau_next = quad_root_in(gA, gB, gC, lo, hi);
         } else if (iter < 100) {
@@ -493,8 +547,20 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
             } else {
                 const double d_left = (org == j) ? -tau : other_gap - tau;
                 const double d_right = (org == j) ? other_gap - tau : -tau;
-                const double psi_p = ev.psi;
-                const double phi_p = ev.fp - ev.psi;
+                /* middle way: psi' on the left pole, phi' on the right; fixed
+                 * weight (swtch): the origin pole's share of f' is its own term
+                 * worg/d^2, the rest of f' goes to the other pole */
+                double psi_p = ev.psi;
+                double phi_p = ev.fp - ev.psi;
+                if (swtch) {
+                    if (org == j) {
+                        psi_p = worg / (d_left * d_left);
+                        phi_p = ev.fp - psi_p;
+                    } else {
+                        phi_p = worg / (d_right * d_right);
+                        psi_p = ev.fp - phi_p;
+                    }
+                }
                 const double b = psi_p * d_left * d_left;
                 const double c = phi_p * d_right * d_right;
                 const double a = ev.f - psi_p * d_left - phi_p * d_right;
@@ -523,7 +589,7 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
             }
         }
         if (!isfinite(tau_next) || tau_next <= lo || tau_next >= hi || tau_next == tau)
-            tau_next = 0.5 * (lo + hi);
+            tau_next = (!ref && geo_ok(lo, hi)) ? geo_mid(lo, hi) : 0.5 * (lo + hi);
         tau = tau_next;
     }
     if (nevals) *nevals = ne;

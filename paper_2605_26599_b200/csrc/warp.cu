@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
                 for (int i = ks + lane; i < ke; i += 32) zsq += w.z2A[i];
                 zsq = bfly_add(zsq);
             }
-            rs_begin_zsq(st, K, j, rho, PolesPtr{w.dA + ks}, w.zA[ks], zsq);
+            rs_begin_zsq(st, K, j, rho, PolesPtr{w.dA + ks}, w.zA[ks], zsq, w.z2A[ks + K - 1]);
             if (st.phase == kRsDone) {
                 if (lane == 0) { w.org[g] = st.org; w.tau[g] = st.tau; }
                 g = -1;
