@@ -678,30 +678,83 @@ typedef struct {
     double tol;
 } defl_info;
 
+/* GPU arithmetic of a close-pole group (deflate.cpp:76-95, 109-140 restated):
+ * a survivor s absorbs its members k1, k2, ... (consecutive non-negligible
+ * poles within tol of d_s) by the rotation chain of the reference.  Composed,
+ * the chain is r_i = |(z_s, z_k1, .., z_ki)|, survivor row r_i x_s = sum of
+ * z x over the group so far, member row x_k' = c x_k - s x_p with c =
+ * r_{i-1}/r_i, s = z_k/r_i, x_p = S_{i-1}/r_{i-1}.  Here it is evaluated from
+ * sequential prefix sums Q = sum z^2, S0/S1 = sum z x (one add per member on
+ * the dependency chain instead of a hypot + two divisions), so a walk of a
+ * glued-Wilkinson cluster (runs of ~10^4) is a cheap prefix pass followed by
+ * independent per-member updates.  The survivor's z becomes sqrt(Q) >= 0. */
+static void group_member(double Qp, double S0p, double S1p, double zk, double* x0, double* x1) {
+    const double Qn = Qp + zk * zk;
+    const double rp = sqrt(Qp), R = sqrt(Qn);
+    const double irp = 1.0 / rp, iR = 1.0 / R;
+    const double c = rp * iR, sn = zk * iR;
+    const double xp0 = S0p * irp, xp1 = S1p * irp;
+    if (x0) *x0 = c * *x0 - sn * xp0;
+    if (x1) *x1 = c * *x1 - sn * xp1;
+}
+
 /* D, Z, R0, R1: merged (sorted) order, modified in place by the rotations.
  * act[K]: sorted positions of survivors.  defl[n-K]: sorted positions of the
  * deflated poles in walk order.  R0/R1 may be NULL (root-only merge). */
 static void deflate_walk(int n, const double* D, double* Z, double* R0, double* R1, double tol,
                          int ref, int* act, int* defl, defl_info* info) {
     int prev = -1, K = 0, nd = 0, nn = 0, nrot = 0;
+    /* GPU arithmetic: running group sums of the current survivor */
+    int L = 0;
+    double Q = 0.0, S0 = 0.0, S1 = 0.0;
+#define GROUP_CLOSE()                                              \
+    do {                                                           \
+        if (!ref && prev >= 0 && L > 0) {                          \
+            const double R_ = sqrt(Q), iR_ = 1.0 / R_;            \
+            Z[prev] = R_;                                          \
+            if (R0) R0[prev] = S0 * iR_;                           \
+            if (R1) R1[prev] = S1 * iR_;                           \
+        }                                                          \
+    } while (0)
     for (int k = 0; k < n; ++k) {
         if (fabs(Z[k]) <= tol) { defl[nd++] = k; continue; }
         ++nn;
         if (prev >= 0 && fabs(D[k] - D[prev]) <= tol) {
-            const double zp = Z[prev], zq = Z[k];
-            const double r = hyp(zp, zq, ref);
-            const double c = zp / r, s = zq / r;
-            Z[prev] = r;
-            Z[k] = 0.0;
-            if (R0) { double xp = R0[prev], xq = R0[k]; R0[prev] = c * xp + s * xq; R0[k] = c * xq - s * xp; }
-            if (R1) { double xp = R1[prev], xq = R1[k]; R1[prev] = c * xp + s * xq; R1[k] = c * xq - s * xp; }
+            if (ref) {
+                const double zp = Z[prev], zq = Z[k];
+                const double r = hyp(zp, zq, ref);
+                const double c = zp / r, s = zq / r;
+                Z[prev] = r;
+                Z[k] = 0.0;
+                if (R0) { double xp = R0[prev], xq = R0[k]; R0[prev] = c * xp + s * xq; R0[k] = c * xq - s * xp; }
+                if (R1) { double xp = R1[prev], xq = R1[k]; R1[prev] = c * xp + s * xq; R1[k] = c * xq - s * xp; }
+            } else {
+                const double zk = Z[k];
+                const double x0 = R0 ? R0[k] : 0.0, x1 = R1 ? R1[k] : 0.0;
+                group_member(Q, S0, S1, zk, R0 ? &R0[k] : NULL, R1 ? &R1[k] : NULL);
+                Q = Q + zk * zk;
+                S0 = S0 + zk * x0;
+                S1 = S1 + zk * x1;
+                Z[k] = 0.0;
+                ++L;
+            }
             defl[nd++] = k;
             ++nrot;
             continue;
         }
+        GROUP_CLOSE();
         prev = k;
         act[K++] = k;
+        if (!ref) {
+            const double zs = Z[k];
+            L = 0;
+            Q = zs * zs;
+            S0 = R0 ? zs * R0[k] : 0.0;
+            S1 = R1 ? zs * R1[k] : 0.0;
+        }
     }
+    GROUP_CLOSE();
+#undef GROUP_CLOSE
     info->n = n; info->K = K; info->nn = nn; info->nrot = nrot; info->tol = tol;
 }
 

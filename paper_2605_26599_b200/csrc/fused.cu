@@ -223,37 +223,63 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     __syncthreads();
 
     // ---- close-pole deflation: segment heads walk their runs ----------------
-    for (int q = tid; q < NN; q += kFuseThreads) {
-        const int k = S.nnPos[q];
-        const int t = upper_index(S.mo, cnt, k);
-        const int qs = S.nnPre[S.mo[t]], qe = S.nnPre[S.mo[t] + S.ms[t]];
-        const double tol = 8.0 * kU * __longlong_as_double((long long)S.tolb[t]) * prm.tol_scale;
-        if (q > qs && fabs(S.D[k] - S.D[S.nnPos[q - 1]]) <= tol) continue;  // not a head
-        S.surv[q] = 1;
-        int prev = k;
-        double dprev_nn = S.D[k];
-        for (int q2 = q + 1; q2 < qe; ++q2) {
-            const int k2 = S.nnPos[q2];
-            const double d2 = S.D[k2];
-            if (fabs(d2 - dprev_nn) > tol) break;
-            dprev_nn = d2;
-            if (fabs(d2 - S.D[prev]) <= tol) {
-                const double zp = S.Z[prev], zq = S.Z[k2];
-                const double r = hyp(zp, zq);
-                const double c = zp / r, s = zq / r;
-                S.Z[prev] = r;
-                S.Z[k2] = 0.0;
-                double xp = S.R0[prev], xq = S.R0[k2];
-                S.R0[prev] = c * xp + s * xq;
-                S.R0[k2] = c * xq - s * xp;
-                xp = S.R1[prev]; xq = S.R1[k2];
-                S.R1[prev] = c * xp + s * xq;
-                S.R1[k2] = c * xq - s * xp;
-                S.surv[q2] = 0;
-            } else {
-                S.surv[q2] = 1;
-                prev = k2;
+    // (group rotation chains from prefix sums, k_segment_walk's arithmetic;
+    // member prefixes go to the dead input slots, members finish in parallel)
+    {
+        double* pQ = lamIn;
+        double* pS0 = bloIn;
+        double* pS1 = bhiIn;
+        for (int q = tid; q < NN; q += kFuseThreads) {
+            const int k = S.nnPos[q];
+            const int t = upper_index(S.mo, cnt, k);
+            const int qs = S.nnPre[S.mo[t]], qe = S.nnPre[S.mo[t] + S.ms[t]];
+            const double tol = 8.0 * kU * __longlong_as_double((long long)S.tolb[t]) * prm.tol_scale;
+            if (q > qs && fabs(S.D[k] - S.D[S.nnPos[q - 1]]) <= tol) continue;  // not a head
+            S.surv[q] = 1;
+            int prev = k, nmem = 0;
+            double dp = S.D[k];
+            const double zs = S.Z[k];
+            double Q = zs * zs, S0 = zs * S.R0[k], S1 = zs * S.R1[k];
+            double dprev_nn = dp;
+            for (int q2 = q + 1; q2 < qe; ++q2) {
+                const int k2 = S.nnPos[q2];
+                const double d2 = S.D[k2];
+                if (fabs(d2 - dprev_nn) > tol) break;
+                dprev_nn = d2;
+                const double zq = S.Z[k2];
+                if (fabs(d2 - dp) <= tol) {
+                    pQ[k2] = Q;
+                    pS0[k2] = S0;
+                    pS1[k2] = S1;
+                    Q = Q + zq * zq;
+                    S0 = S0 + zq * S.R0[k2];
+                    S1 = S1 + zq * S.R1[k2];
+                    ++nmem;
+                    S.surv[q2] = 0;
+                } else {
+                    if (nmem) {
+                        const double R = sqrt(Q), iR = 1.0 / R;
+                        S.Z[prev] = R; S.R0[prev] = S0 * iR; S.R1[prev] = S1 * iR;
+                    }
+                    S.surv[q2] = 1;
+                    prev = k2; dp = d2; nmem = 0;
+                    Q = zq * zq; S0 = zq * S.R0[k2]; S1 = zq * S.R1[k2];
+                }
             }
+            if (nmem) {
+                const double R = sqrt(Q), iR = 1.0 / R;
+                S.Z[prev] = R; S.R0[prev] = S0 * iR; S.R1[prev] = S1 * iR;
+            }
+        }
+        __syncthreads();
+        for (int q = tid; q < NN; q += kFuseThreads) {
+            if (S.surv[q]) continue;
+            const int k = S.nnPos[q];
+            double x0 = S.R0[k], x1 = S.R1[k];
+            group_member(pQ[k], pS0[k], pS1[k], S.Z[k], x0, x1);
+            S.R0[k] = x0;
+            S.R1[k] = x1;
+            S.Z[k] = 0.0;
         }
     }
     __syncthreads();

@@ -395,12 +395,16 @@ __global__ void __launch_bounds__(kScanBlock) k_nn_scan(Work w, LevelDev L, int 
     if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= n) w.nnPre[n] = base + tot;
 }
 
-// Close-pole deflation (deflate.cpp:76-95).  A segment is a maximal run of
-// consecutive non-negligible sorted poles whose neighbour gaps are <= tol; its
-// first pole is always a survivor (its gap to any earlier survivor exceeds
-// tol), so segments are independent.  The segment head walks its run with the
-// reference's rule (rotate into the last survivor when |d - d_prev| <= tol),
-// applying each rotation to z and the two selected rows in record order.
+// Close-pole deflation (deflate.cpp:76-95, 109-140).  A segment is a maximal
+// run of consecutive non-negligible sorted poles whose neighbour gaps are
+// <= tol; its first pole is always a survivor (its gap to any earlier survivor
+// exceeds tol), so segments are independent.  The segment head walks its run
+// with the reference's rule (a pole within tol of the last survivor is
+// absorbed by it) and evaluates each group's rotation chain from prefix sums
+// (the checker's deflate_walk / group_member): the walk carries only
+// Q = sum z^2, S0/S1 = sum z x -- one add per member on the dependency chain --
+// and records each member's prefix (Q, S0, S1) at its position in the free
+// lam/blo/bhi slots; k_surv_scan finishes the members in parallel.
 __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int NN = w.nnPre[n];
@@ -412,41 +416,63 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     const double tol = merge_tol(L, m, tol_scale);
     if (q > qs && fabs(w.D[k] - w.D[w.nnPos[q - 1]]) <= tol) return;  // not a head
     w.survFlag[q] = 1;
-    // the current survivor lives in registers; the next entry is prefetched so a
-    // long cluster (glued Wilkinson: runs of ~700) is a compute chain, not a
-    // chain of dependent L2 round trips
-    int prev = k;
-    double dp = w.D[k], zp = w.Z[k], x0p = w.R0[k], x1p = w.R1[k];
+    int prev = k, nmem = 0;
+    double dp = w.D[k];
+    const double zs = w.Z[k];
+    double Q = zs * zs, S0 = zs * w.R0[k], S1 = zs * w.R1[k];
     double dprev_nn = dp;
-    int q2 = q + 1;
-    int k2 = q2 < qe ? w.nnPos[q2] : 0;
-    double d2 = 0.0, zq = 0.0, x0q = 0.0, x1q = 0.0;
-    if (q2 < qe) { d2 = w.D[k2]; zq = w.Z[k2]; x0q = w.R0[k2]; x1q = w.R1[k2]; }
-    for (; q2 < qe; ++q2) {
-        if (fabs(d2 - dprev_nn) > tol) break;  // next segment head
-        // prefetch the next entry (only this walker ever touches it) while this step computes
-        const int kn = q2 + 1 < qe ? w.nnPos[q2 + 1] : 0;
-        double dn = 0.0, zn = 0.0, x0n = 0.0, x1n = 0.0;
-        if (q2 + 1 < qe) { dn = w.D[kn]; zn = w.Z[kn]; x0n = w.R0[kn]; x1n = w.R1[kn]; }
-        dprev_nn = d2;
-        if (fabs(d2 - dp) <= tol) {
-            const double r = hyp(zp, zq);
-            const double c = zp / r, sn = zq / r;
-            w.Z[k2] = 0.0;
-            w.R0[k2] = c * x0q - sn * x0p;
-            w.R1[k2] = c * x1q - sn * x1p;
-            zp = r;
-            x0p = c * x0p + sn * x0q;
-            x1p = c * x1p + sn * x1q;
-            w.survFlag[q2] = 0;
-        } else {
-            w.Z[prev] = zp; w.R0[prev] = x0p; w.R1[prev] = x1p;  // retire the survivor
-            w.survFlag[q2] = 1;
-            prev = k2; dp = d2; zp = zq; x0p = x0q; x1p = x1q;
+    // Batches of 8 NN entries: the 8 positions are loaded at once, then their
+    // data, so a long cluster (glued Wilkinson: runs of ~10^4) costs two
+    // dependent L2 round trips per 8 entries instead of per entry.  A segment of
+    // length 1 (the common case) exits after its first probe.
+    if (q + 1 < qe && fabs(w.D[w.nnPos[q + 1]] - dp) <= tol) {
+        bool done = false;
+        for (int qb = q + 1; !done && qb < qe; qb += 8) {
+            int kb[8];
+            double db[8], zb[8], x0b[8], x1b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) kb[u] = w.nnPos[min(qb + u, qe - 1)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                db[u] = w.D[kb[u]];
+                zb[u] = w.Z[kb[u]];
+                x0b[u] = w.R0[kb[u]];
+                x1b[u] = w.R1[kb[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int q2 = qb + u;
+                if (done || q2 >= qe) { done = true; continue; }
+                const double d2 = db[u];
+                if (fabs(d2 - dprev_nn) > tol) { done = true; continue; }  // next segment head
+                dprev_nn = d2;
+                const int k2 = kb[u];
+                const double zq = zb[u];
+                if (fabs(d2 - dp) <= tol) {  // member of prev's group
+                    w.lam[k2] = Q;
+                    w.blo[k2] = S0;
+                    w.bhi[k2] = S1;
+                    Q = Q + zq * zq;
+                    S0 = S0 + zq * x0b[u];
+                    S1 = S1 + zq * x1b[u];
+                    ++nmem;
+                    w.survFlag[q2] = 0;
+                } else {
+                    if (nmem) {  // retire the survivor
+                        const double R = sqrt(Q), iR = 1.0 / R;
+                        w.Z[prev] = R; w.R0[prev] = S0 * iR; w.R1[prev] = S1 * iR;
+                    }
+                    w.survFlag[q2] = 1;
+                    prev = k2; dp = d2; nmem = 0;
+                    Q = zq * zq; S0 = zq * x0b[u]; S1 = zq * x1b[u];
+                }
+            }
         }
-        k2 = kn; d2 = dn; zq = zn; x0q = x0n; x1q = x1n;
     }
-    w.Z[prev] = zp; w.R0[prev] = x0p; w.R1[prev] = x1p;
+    if (nmem) {
+        const double R = sqrt(Q), iR = 1.0 / R;
+        w.Z[prev] = R; w.R0[prev] = S0 * iR; w.R1[prev] = S1 * iR;
+    }
 }
 
 // survivor prefix over NN indices + compacted active problem (deflate.cpp:100-105),
@@ -461,6 +487,14 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, in
     if (tile > 0 && tile * kScanBlock >= NN) return;  // uniform per CTA
     const int q = tile * kScanBlock + threadIdx.x;
     const int f = q < NN ? w.survFlag[q] : 0;
+    if (q < NN && !f) {  // group member: rotation-chain update from its prefix (k_segment_walk)
+        const int k = w.nnPos[q];
+        double x0 = w.R0[k], x1 = w.R1[k];
+        group_member(w.lam[k], w.blo[k], w.bhi[k], w.Z[k], x0, x1);
+        w.R0[k] = x0;
+        w.R1[k] = x1;
+        w.Z[k] = 0.0;
+    }
     int tot;
     const int ex = block_exclusive_scan<kScanBlock>(f, tot);
     const int base = cta_lookback(state, tile, tot, &s_pref);
