@@ -43,11 +43,12 @@ void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
                    const unsigned long long* sbits, double* lam, int* launches, Prof* prof);
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
                        int nruns, int* launches, Prof* prof);
-void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups,
+void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
                         const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
                         int* launches, Prof* prof);
 void init_fused_attributes();
 constexpr int kFuseMaxElems = 1024;
+constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
 constexpr int kFuseMaxMergesHost = 128;
 
 void init_kernel_attributes();
@@ -82,6 +83,7 @@ struct LevelHost {
     int tile0;   // offset of this level's tileFirst table
     bool fused;  // all merges <= kFuseMaxElems: one fused SMEM launch (fused.cu)
     int g0, G;   // groups of the fused launch
+    int cap;     // group capacity (elements): 512 (small shape) or 1024
 };
 
 struct Plan {
@@ -243,6 +245,7 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         int maxSize = 0;
         for (int q = 0; q < L.M; ++q) maxSize = std::max(maxSize, p->mSize[L.m0 + q]);
         L.fused = fuse && maxSize <= kFuseMaxElems;
+        L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
         L.G = 0;
         if (L.fused) {
@@ -251,7 +254,7 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
                 int c = 1, tot = p->mSize[L.m0 + q];
                 while (q + c < L.M && c < kFuseMaxMergesHost &&
                        p->mOff[L.m0 + q + c] == p->mOff[L.m0 + q + c - 1] + p->mSize[L.m0 + q + c - 1] &&
-                       tot + p->mSize[L.m0 + q + c] <= kFuseMaxElems) {
+                       tot + p->mSize[L.m0 + q + c] <= L.cap) {
                     tot += p->mSize[L.m0 + q + c];
                     ++c;
                 }
@@ -497,7 +500,7 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
         L.tileFirst = p->d_tileFirst + lh.tile0;
         L.M = lh.M;
         if (lh.fused) {
-            launch_level_fused(s, h->w, L, lh.G, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
+            launch_level_fused(s, h->w, L, lh.G, lh.cap, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
                                h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
         } else {
             launch_level(s, h->w, L, n, prm, launches, prof);

@@ -21,10 +21,12 @@
 
 namespace brgpu {
 
-constexpr int kFuseThreads = 256;
-constexpr int kFuseMax = 1024;        // elements per group
 constexpr int kFuseMaxMerges = 128;   // merges per group
 
+// Two shapes: groups of <= 1024 elements on 256 threads (merges of 513..1024,
+// two CTAs per SM) and groups of <= 512 on 128 threads (merges <= 512, four
+// CTAs per SM, so one CTA's root-queue tail overlaps the others' work).
+template <int kFuseMax, int kFuseThreads>
 struct FuseSmem {
     // sorted merge arrays (local positions)
     double D[kFuseMax];
@@ -57,6 +59,7 @@ struct FuseSmem {
     unsigned long long evals, terms;
 };
 
+template <int kFuseThreads>
 __device__ __forceinline__ int cta_excl_scan(int v, int& total, int* warp_tot) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     constexpr int NW = kFuseThreads / 32;
@@ -85,6 +88,7 @@ __device__ __forceinline__ int cta_excl_scan(int v, int& total, int* warp_tot) {
 }
 
 // exclusive prefix of flags[0..E) into pre[0..E]; each thread scans a contiguous chunk
+template <int kFuseThreads>
 __device__ __forceinline__ int cta_scan_flags(const unsigned char* flags, int E, int* pre, int* warp_tot) {
     const int per = (E + kFuseThreads - 1) / kFuseThreads;
     const int i0 = threadIdx.x * per;
@@ -94,7 +98,7 @@ __device__ __forceinline__ int cta_scan_flags(const unsigned char* flags, int E,
         if (i < E) local += flags[i];
     }
     int tot;
-    int run = cta_excl_scan(local, tot, warp_tot);
+    int run = cta_excl_scan<kFuseThreads>(local, tot, warp_tot);
     for (int k = 0; k < per; ++k) {
         const int i = i0 + k;
         if (i < E) {
@@ -117,11 +121,13 @@ __device__ __forceinline__ int upper_index(const int* a, int cnt, int x) {
     return lo;
 }
 
-__global__ void __launch_bounds__(kFuseThreads, 2)
+template <int kFuseMax, int kFuseThreads>
+__global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
 k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
               SolveParams prm, int* __restrict__ traceOut) {
     extern __shared__ __align__(16) unsigned char fuse_raw[];
-    FuseSmem& S = *reinterpret_cast<FuseSmem*>(fuse_raw);
+    using Smem = FuseSmem<kFuseMax, kFuseThreads>;
+    Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
     const int tid = threadIdx.x;
     const int m0 = gFirst[blockIdx.x];
     const int cnt = gCount[blockIdx.x];
@@ -217,7 +223,7 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
         S.flag[i] = fabs(S.Z[i]) > tol;
     }
     __syncthreads();
-    const int NN = cta_scan_flags(S.flag, E, S.nnPre, S.scan);
+    const int NN = cta_scan_flags<kFuseThreads>(S.flag, E, S.nnPre, S.scan);
     for (int i = tid; i < E; i += kFuseThreads)
         if (S.flag[i]) S.nnPos[S.nnPre[i]] = i;
     __syncthreads();
@@ -285,7 +291,7 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     __syncthreads();
 
     // ---- survivor compaction: active (d, z^2) pairs, z, rows ----------------
-    const int T = cta_scan_flags(S.surv, NN, S.survPre, S.scan);
+    const int T = cta_scan_flags<kFuseThreads>(S.surv, NN, S.survPre, S.scan);
     double2* pairs = reinterpret_cast<double2*>(S.in);   // aliases lam/blo inputs (dead)
     double* zA = S.in + 2 * kFuseMax;                     // aliases bhi input (dead)
     for (int q = tid; q < NN; q += kFuseThreads) {
@@ -472,19 +478,27 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     }
 }
 
-void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups,
+void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
                         const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
                         int* launches, Prof* prof) {
-    k_level_fused<<<ngroups, kFuseThreads, sizeof(FuseSmem), s>>>(w, L, gFirst, gCount, prm, traceOut);
+    if (cap <= 512)
+        k_level_fused<512, 128><<<ngroups, 128, sizeof(FuseSmem<512, 128>), s>>>(w, L, gFirst, gCount, prm,
+                                                                                 traceOut);
+    else
+        k_level_fused<1024, 256><<<ngroups, 256, sizeof(FuseSmem<1024, 256>), s>>>(w, L, gFirst, gCount, prm,
+                                                                                   traceOut);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
 }
 
-size_t fused_smem_bytes() { return sizeof(FuseSmem); }
-static_assert(sizeof(FuseSmem) <= 113 * 1024, "two fused CTAs must fit one SM (227 KB)");
+static_assert(sizeof(FuseSmem<1024, 256>) <= 113 * 1024, "two fused CTAs must fit one SM (227 KB)");
+static_assert(sizeof(FuseSmem<512, 128>) <= 56 * 1024, "four small fused CTAs must fit one SM");
 
 void init_fused_attributes() {
-    cudaFuncSetAttribute(k_level_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FuseSmem));
+    cudaFuncSetAttribute(k_level_fused<1024, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(FuseSmem<1024, 256>));
+    cudaFuncSetAttribute(k_level_fused<512, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(FuseSmem<512, 128>));
 }
 
 }  // namespace brgpu
