@@ -14,6 +14,7 @@
 #include <nccl.h>  // types only: libnccl is dlopen'ed (torch's copy when already loaded)
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -49,6 +50,7 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 void init_fused_attributes();
 constexpr int kFuseMaxElems = 1024;
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
+constexpr int kSplitMinSizeHost = 8192;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
 constexpr int kFuseMaxMergesHost = 128;
 
 void init_kernel_attributes();
@@ -84,6 +86,7 @@ struct LevelHost {
     bool fused;  // all merges <= kFuseMaxElems: one fused SMEM launch (fused.cu)
     int g0, G;   // groups of the fused launch
     int cap;     // group capacity (elements): 512 (small shape) or 1024
+    int minSize; // smallest merge of the level
 };
 
 struct Plan {
@@ -242,8 +245,12 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         }
         L.M = (int)(j - i);
         p->maxM = std::max(p->maxM, L.M);
-        int maxSize = 0;
-        for (int q = 0; q < L.M; ++q) maxSize = std::max(maxSize, p->mSize[L.m0 + q]);
+        int maxSize = 0, minSize = INT32_MAX;
+        for (int q = 0; q < L.M; ++q) {
+            maxSize = std::max(maxSize, p->mSize[L.m0 + q]);
+            minSize = std::min(minSize, p->mSize[L.m0 + q]);
+        }
+        L.minSize = minSize;
         L.fused = fuse && maxSize <= kFuseMaxElems;
         L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
@@ -499,6 +506,7 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
         L.mTol = h->mTol;
         L.tileFirst = p->d_tileFirst + lh.tile0;
         L.M = lh.M;
+        L.allSplit = lh.minSize > kSplitMinSizeHost ? 1 : 0;
         if (lh.fused) {
             launch_level_fused(s, h->w, L, lh.G, lh.cap, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
                                h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);

@@ -66,6 +66,7 @@ struct LevelDev {
     unsigned long long* mTol;  // max(|D|,|z|) bits per merge (atomicMax)
     const int* tileFirst;      // ceil(n/kTile)+1 entries
     int M;
+    int allSplit;              // every merge of the level is larger than kSplitMinSize (warp tier only)
 };
 
 // Optional per-kernel profiling (brgpu_profile_kernels): the launchers call

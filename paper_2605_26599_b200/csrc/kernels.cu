@@ -770,6 +770,7 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
         const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + ks, K, lam);
         p = off + pos;
         w.lam[p] = lam;
+        w.tau[g] = lam;  // tau is dead after this read: k_deflated_out searches the root values
         if (L.mFlags[m] & kMergeRoot) act = false;
     }
     double nn = 0.0, s0 = 0.0, s1 = 0.0;
@@ -833,11 +834,12 @@ __global__ void k_deflated_out(Work w, LevelDev L, int n) {
     const int K = ke - ks;
     const int t = (k - off) - (w.survPre[q] - ks);
     const double v = w.D[k];
-    // #{roots j: lambda_j < v}; roots ascend (interlacing)
+    // #{roots j: lambda_j < v}; roots ascend (interlacing); the rows kernels
+    // left lambda_j = d[org_j] + tau_j in tau[j]
     int lo = 0, hi = K;
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        const double lj = w.dA[ks + w.org[ks + mid]] + w.tau[ks + mid];
+        const double lj = w.tau[ks + mid];
         if (lj < v) lo = mid + 1; else hi = mid;
     }
     const int p = off + t + lo;
@@ -982,25 +984,32 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
     PMARK(BRGPU_K_WALK);
     k_surv_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, st2, tk + 1);
     PMARK(BRGPU_K_SURVWRITE);
-    cudaMemsetAsync(w.levelModes, 0, sizeof(int), s);
-    k_level_modes<<<cdiv(L.M, 256), 256, 0, s>>>(w, L);
-    k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
-    launch_secular_tiled(s, w, L, n, prm);
+    // levels whose merges are all larger than kSplitMinSize run only the
+    // warp-per-root tier (known from the plan: no mode pass, no lane-tier launches)
+    const bool lane_tier = !L.allSplit;
+    int nl = 4;  // scatter, nn_scan, walk, surv_scan
+    if (lane_tier) {
+        cudaMemsetAsync(w.levelModes, 0, sizeof(int), s);
+        k_level_modes<<<cdiv(L.M, 256), 256, 0, s>>>(w, L);
+        k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
+        launch_secular_tiled(s, w, L, n, prm);
+        nl += 3;
+    }
     launch_secular_warp(s, w, L, n, prm);
     PMARK(BRGPU_K_SECULAR);
-    int nl = 8;  // scatter, nn_scan, walk, surv_scan, modes + 3 secular tiers
+    nl += 1;
     if (prm.zhat) {
-        k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
+        if (lane_tier) k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
         launch_zhat_warp(s, w, L, n, prm);
         PMARK(BRGPU_K_ZHAT);
-        nl += 2;
+        nl += lane_tier ? 2 : 1;
     }
-    k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
+    if (lane_tier) k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
     launch_rows_warp(s, w, L, n, prm);
     PMARK(BRGPU_K_ROWS);
     k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
     PMARK(BRGPU_K_DEFLATED);
-    *launches += nl + 3;  // rows, rows_warp, deflated_out
+    *launches += nl + (lane_tier ? 3 : 2);  // rows (lane), rows_warp, deflated_out
 }
 
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,

@@ -40,7 +40,7 @@ __device__ __forceinline__ int strided_start(int lo, int ks, int lane) {
 __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelDev L, int n, int patched) {
     __shared__ double2 s_tile[2][kWarpTile];
     __shared__ int s_next;
-    if (!(*w.levelModes & 2)) return;
+    if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int G = (int)gridDim.x;
     const int R = max(kWarpThreads / 32, (T + G - 1) / G);
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, int n) {
     __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
-    if (!(*w.levelModes & 2)) return;
+    if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {  // uniform per CTA
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
     __shared__ double s_d[kWarpTile], s_zh[kWarpTile], s_r0[kWarpTile], s_r1[kWarpTile];
-    if (!(*w.levelModes & 2)) return;
+    if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {
@@ -281,7 +281,10 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
                 const double lam = dorg + tau;
                 const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + ks, K, lam);
                 p = off + pos;
-                if (lane == 0) w.lam[p] = lam;
+                if (lane == 0) {
+                    w.lam[p] = lam;
+                    w.tau[g] = lam;  // dead after the read above: k_deflated_out searches root values
+                }
                 rows = !(L.mFlags[m] & kMergeRoot);
             }
         }
