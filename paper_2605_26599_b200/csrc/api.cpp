@@ -442,7 +442,8 @@ int ensure_work(Handle* h, int64_t n) {
     w.dA = dbl + 9 * c; w.zA = dbl + 10 * c; w.z2A = dbl + 11 * c; w.r0A = dbl + 12 * c;
     w.r1A = dbl + 13 * c; w.tau = dbl + 14 * c;
     const int64_t ntiles = (c + 1023) / 1024 + 1;
-    const int64_t ni = 5 * c + 2 + 2 * ntiles + 8 + 2 * (2 * ntiles + 4);
+    // look-back states: merge tiles (256 positions) + scan tiles (1024) + tickets
+    const int64_t ni = 5 * c + 2 + 2 * ntiles + 8 + 2 * (6 * ntiles + 8);
     int* ib = nullptr;
     CUDA_TRY(h, cudaMalloc(&ib, sizeof(int) * ni));
     w.nnPre = ib; w.nnPos = ib + c + 1; w.survPre = ib + 2 * c + 1; w.aMerge = ib + 3 * c + 2;

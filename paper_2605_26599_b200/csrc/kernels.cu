@@ -287,55 +287,41 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __r
 // ---------------------------------------------------------------------------
 // level pipeline
 // ---------------------------------------------------------------------------
-// Stable merge of the two sorted children (== std::stable_sort of the
-// concatenation by '<', deflate.cpp:62-66), z = (sign*bhi_L, blo_R), and the
-// per-merge deflation scale max(|D|, |z|) (deflate.cpp:55-60; order-free max,
-// segmented warp reduction + one atomicMax per merge segment).
-__global__ void k_merge_scatter(Work w, LevelDev L, int n) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int m = p < n ? find_merge(L, p) : -1;
-    unsigned long long bits = 0ULL;
-    if (m >= 0) {
-        const int off = L.mOff[m], nl = L.mNL[m], nr = L.mSize[m] - nl;
-        const double v = w.lam[p];
-        int sp;
-        double z, r0, r1;
-        if (p < off + nl) {
-            sp = p + count_less(w.lam + off + nl, nr, v);
-            const double em = w.ew[off + nl - 1];
-            const double b = w.bhi[p];
-            z = em < 0 ? -b : b;
-            r0 = w.blo[p];
-            r1 = 0.0;
-        } else {
-            sp = (p - nl) + count_leq(w.lam + off, nl, v);
-            z = w.blo[p];
-            r0 = 0.0;
-            r1 = w.bhi[p];
-        }
-        w.D[sp] = v;
-        w.Z[sp] = z;
-        w.R0[sp] = r0;
-        w.R1[sp] = r1;
-        bits = (unsigned long long)__double_as_longlong(fmax(fabs(v), fabs(z)));
-    }
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const unsigned long long b2 = __shfl_down_sync(0xffffffffu, bits, off);
-        const int m2 = __shfl_down_sync(0xffffffffu, m, off);
-        if (lane + off < 32 && m2 == m && b2 > bits) bits = b2;
-    }
-    const int mp = __shfl_up_sync(0xffffffffu, m, 1);
-    if (m >= 0 && (lane == 0 || mp != m)) atomicMax(&L.mTol[m], bits);
-}
-
 // ---------------------------------------------------------------------------
 // single-pass compaction scans (decoupled look-back).  Tile states are packed
 // 64-bit words: bits 62-63 status (1 aggregate, 2 inclusive), low 32 the count;
 // tiles are taken in ticket order so every predecessor is resident or done.
 // ---------------------------------------------------------------------------
 constexpr unsigned long long kTileAgg = 1ULL << 62, kTileInc = 2ULL << 62;
+
+// Warp 0 only: publish the tile aggregate, look back, return the exclusive
+// prefix (valid in every lane of warp 0).
+__device__ __forceinline__ int warp_lookback(unsigned long long* state, int tile, int aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0)
+        atomicExch(&state[tile], ((tile == 0 ? 2ULL : 1ULL) << 62) | (unsigned)aggregate);
+    int prefix = 0;
+    if (tile > 0) {
+        int j = tile - 1;
+        for (;;) {
+            const int idx = j - lane;
+            unsigned long long v = idx >= 0 ? *(volatile unsigned long long*)&state[idx] : (2ULL << 62);
+            while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+                if ((v >> 62) == 0) v = *(volatile unsigned long long*)&state[idx];
+            }
+            const unsigned incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+            const int k = incl ? __ffs(incl) - 1 : 31;
+            int c = lane <= k ? (int)(unsigned)(v & 0xffffffffULL) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            prefix += c;
+            if (incl) break;
+            j -= 32;
+        }
+        if (lane == 0) atomicExch(&state[tile], kTileInc | (unsigned)(prefix + aggregate));
+    }
+    return prefix;
+}
 
 __device__ __forceinline__ int cta_lookback(unsigned long long* state, int tile, int aggregate,
                                             int* s_bcast) {
@@ -370,29 +356,215 @@ __device__ __forceinline__ int cta_lookback(unsigned long long* state, int tile,
     return *s_bcast;
 }
 
-// non-negligible flags |z| > tol (deflate.cpp:72), their exclusive prefix over
-// positions and the NN list (sorted positions), in one pass
-__global__ void __launch_bounds__(kScanBlock) k_nn_scan(Work w, LevelDev L, int n, double tol_scale,
-                                                        unsigned long long* state, int* ticket) {
+// Number of left-child elements among the first d outputs of the stable merge
+// of sorted a[0..nl) (left) and b[0..nr) (right): left element i precedes
+// right element j iff a_i <= b_j (std::stable_sort of the concatenation by
+// '<', deflate.cpp:62-66).  Warp-cooperative 32-ary search (all lanes call it
+// with the same arguments): about log32 of the child size dependent L2 round
+// trips instead of log2.
+__device__ __forceinline__ int warp_merge_split(const double* __restrict__ a, int nl,
+                                                const double* __restrict__ b, int nr, int d) {
+    const int lane = threadIdx.x & 31;
+    int lo = max(0, d - nr), hi = min(d, nl);  // answer in [lo, hi]; pred(i) holds for i <= answer
+    while (hi > lo) {
+        const int span = hi - lo;
+        const int step = (span + 31) >> 5;
+        const int c = min(lo + (lane + 1) * step, hi);
+        const bool pred = (d - c >= nr) || !(b[d - c] < a[c - 1]);  // a[c-1] is within the first d
+        const unsigned bal = __ballot_sync(0xffffffffu, pred);
+        const int k = __popc(bal);  // candidates are monotone: the first k hold
+        if (step == 1) { lo = min(lo + k, hi); break; }  // capped duplicates of hi may add to k
+        const int nlo = k ? min(lo + k * step, hi) : lo;
+        hi = min(hi, lo + (k + 1) * step - 1);
+        lo = nlo;
+    }
+    return lo;
+}
+
+constexpr int kMergeTile = 256;
+constexpr int kPrepVec = 4;  // merge tiles per k_merge_prep CTA: the whole level is one wave
+
+// Merge preparation over kPrepVec merge tiles per CTA (one pass, one wave):
+//  * the per-merge deflation scale max(|D|, |z|) (deflate.cpp:55-60), an
+//    order-free max: segmented warp reduction, then one atomicMax per merge
+//    segment of each tile (a tile inside one merge reduces through shared
+//    memory first);
+//  * the merge-path diagonal split at each tile's first position (warp k for
+//    tile k, 32-ary search), kept in split[tile] for k_merge_nn.
+__global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w, LevelDev L, int n, int* __restrict__ split) {
+    __shared__ unsigned long long s_max[kPrepVec][kMergeTile / 32];
+    __shared__ int s_m[kPrepVec][kMergeTile / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int tile0 = blockIdx.x * kPrepVec;
+    int mk[kPrepVec];
+    unsigned long long bk[kPrepVec];
+#pragma unroll
+    for (int k = 0; k < kPrepVec; ++k) {  // independent loads of the CTA's positions
+        const int p = (tile0 + k) * kMergeTile + threadIdx.x;
+        const int m = p < n ? find_merge(L, p) : -1;
+        mk[k] = m;
+        bk[k] = 0ULL;
+        if (m >= 0) {
+            const int off = L.mOff[m], nl = L.mNL[m];
+            const double zs = p < off + nl ? w.bhi[p] : w.blo[p];
+            bk[k] = (unsigned long long)__double_as_longlong(fmax(fabs(w.lam[p]), fabs(zs)));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kPrepVec; ++k) {
+        const int m = mk[k];
+        unsigned long long bits = bk[k];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long b2 = __shfl_down_sync(0xffffffffu, bits, o);
+            const int m2 = __shfl_down_sync(0xffffffffu, m, o);
+            if (lane + o < 32 && m2 == m && b2 > bits) bits = b2;
+        }
+        const int m31 = __shfl_sync(0xffffffffu, m, 31);
+        const bool whole = __all_sync(0xffffffffu, m == m31) && m31 >= 0;
+        if (lane == 0) {
+            s_m[k][wid] = whole ? m : -2;
+            s_max[k][wid] = bits;
+        }
+        bk[k] = bits;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPrepVec; ++k) {
+        bool tile_whole = true;
+#pragma unroll
+        for (int q = 0; q < kMergeTile / 32; ++q) tile_whole = tile_whole && s_m[k][q] == s_m[k][0] && s_m[k][q] >= 0;
+        if (tile_whole) {
+            if (threadIdx.x == 0) {
+                unsigned long long b = s_max[k][0];
+#pragma unroll
+                for (int q = 1; q < kMergeTile / 32; ++q) b = s_max[k][q] > b ? s_max[k][q] : b;
+                atomicMax(&L.mTol[s_m[k][0]], b);
+            }
+        } else {
+            const int m = mk[k];
+            const int mp = __shfl_up_sync(0xffffffffu, m, 1);
+            if (m >= 0 && (lane == 0 || mp != m)) atomicMax(&L.mTol[m], bk[k]);
+        }
+    }
+    if (wid < kPrepVec) {
+        const int tile = tile0 + wid;
+        const int p0 = tile * kMergeTile;
+        const int m0 = p0 < n ? find_merge(L, p0) : -1;
+        if (m0 >= 0) {
+            const int off = L.mOff[m0], nl = L.mNL[m0], nr = L.mSize[m0] - nl;
+            const double* la = w.lam + off;
+            const int sp = warp_merge_split(la, nl, la + nl, nr, p0 - off);
+            if (lane == 0) split[tile] = sp;
+        }
+    }
+}
+
+// Stable merge of the sorted children (merge path), z = (sign*bhi_L, blo_R)
+// and the non-negligible flags |z| > tol (deflate.cpp:31-41, 62-72) with their
+// single-pass prefix (nnPre) and list (nnPos).  A CTA owns kMergeTile output
+// positions; the diagonal splits bounding each merge segment's inputs come
+// from k_merge_prep (tile start) or are the merge's ends, so the inputs are
+// loaded coalesced at once, placed by searches in shared memory and written
+// back coalesced in merged order.  The tile's flag count (order-free: the same
+// elements) is published before the placement so the look-back overlaps it.
+__global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int n, double tol_scale,
+                                                         const int* __restrict__ split,
+                                                         unsigned long long* state, int* ticket) {
+    // inputs (lam, blo, bhi), then the merged tile (D, Z, R0 alias them; R1)
+    __shared__ double s_v[kMergeTile], s_b0[kMergeTile], s_b1[kMergeTile], s_R1[kMergeTile];
+    double* s_D = s_v;
+    double* s_Z = s_b0;
+    double* s_R0 = s_b1;
+    __shared__ int s_red[kMergeTile / 32];
     __shared__ int s_tile, s_pref;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
     __syncthreads();
     const int tile = s_tile;
-    const int k = tile * kScanBlock + threadIdx.x;
-    int f = 0;
-    if (k < n) {
-        const int m = find_merge(L, k);
-        if (m >= 0) f = fabs(w.Z[k]) > merge_tol(L, m, tol_scale);
-        w.nnFlag[k] = (uint8_t)f;
+    const int t = threadIdx.x;
+    const int lane = t & 31, wid = t >> 5;
+    const int p0 = tile * kMergeTile;
+    const int p = p0 + t;
+    const int m = p < n ? find_merge(L, p) : -1;
+    int off = 0, nl = 0, q0 = 0, q1 = 0, i0 = 0, j0 = 0, la = 0, u = 0, f = 0;
+    double tol = 0.0;
+    if (m >= 0) {
+        off = L.mOff[m];
+        nl = L.mNL[m];
+        const int size = L.mSize[m];
+        q0 = max(p0, off);
+        q1 = min(min(p0 + kMergeTile, n), off + size);
+        i0 = q0 == off ? 0 : split[tile];                      // a segment starting mid-tile starts its merge
+        const int i1 = q1 == off + size ? nl : split[tile + 1];  // ... and one ending mid-tile ends it
+        la = i1 - i0;
+        j0 = (q0 - off) - i0;
+        u = p - q0;
+        const bool left = u < la;
+        const int src = left ? off + i0 + u : off + nl + j0 + (u - la);
+        const double b0 = w.blo[src], b1 = w.bhi[src];
+        s_v[t] = w.lam[src];
+        s_b0[t] = b0;
+        s_b1[t] = b1;
+        tol = merge_tol(L, m, tol_scale);
+        f = fabs(left ? b1 : b0) > tol;  // |z| (the sign does not matter)
     }
+    // tile flag count: published before the placement so the look-back overlaps it
+    int c = __reduce_add_sync(0xffffffffu, f);
+    if (lane == 0) s_red[wid] = c;
+    __syncthreads();
+    if (wid == 0) {
+        c = lane < kMergeTile / 32 ? s_red[lane] : 0;
+        c = __reduce_add_sync(0xffffffffu, c);
+        const int pref = warp_lookback(state, tile, c);
+        if (lane == 0) s_pref = pref;
+    }
+    int o = -1;
+    double v = 0.0, z = 0.0, r0 = 0.0, r1 = 0.0;
+    if (m >= 0) {
+        const int h = q0 - p0;
+        v = s_v[t];
+        int sp;  // merge-local output index
+        if (u < la) {  // left element i0+u: right elements before it are b[0..j0) + local ones < v
+            sp = (i0 + u) + j0 + count_less(s_v + h + la, (q1 - q0) - la, v);
+            const double em = w.ew[off + nl - 1];
+            const double b = s_b1[t];
+            z = em < 0 ? -b : b;
+            r0 = s_b0[t];
+            r1 = 0.0;
+        } else {       // right element j0+u-la: left elements before it are a[0..i0) + local ones <= v
+            sp = (j0 + u - la) + i0 + count_leq(s_v + h, la, v);
+            z = s_b0[t];
+            r0 = 0.0;
+            r1 = s_b1[t];
+        }
+        o = off + sp - p0;
+    }
+    __syncthreads();  // every search is done: the input slots become the merged tile
+    if (o >= 0) {
+        s_D[o] = v;
+        s_Z[o] = z;
+        s_R0[o] = r0;
+        s_R1[o] = r1;
+    }
+    __syncthreads();
+    f = 0;
+    if (m >= 0) {
+        z = s_Z[t];
+        w.D[p] = s_D[t];
+        w.Z[p] = z;
+        w.R0[p] = s_R0[t];
+        w.R1[p] = s_R1[t];
+        f = fabs(z) > tol;
+    }
+    if (p < n) w.nnFlag[p] = (uint8_t)f;
     int tot;
-    const int ex = block_exclusive_scan<kScanBlock>(f, tot);
-    const int base = cta_lookback(state, tile, tot, &s_pref);
-    if (k < n) {
-        w.nnPre[k] = base + ex;
-        if (f) w.nnPos[base + ex] = k;
+    const int ex = block_exclusive_scan<kMergeTile>(f, tot);
+    const int base = s_pref;
+    if (p < n) {
+        w.nnPre[p] = base + ex;
+        if (f) w.nnPos[base + ex] = p;
     }
-    if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= n) w.nnPre[n] = base + tot;
+    if (t == kMergeTile - 1 && (tile + 1) * kMergeTile >= n) w.nnPre[n] = base + tot;
 }
 
 // Close-pole deflation (deflate.cpp:76-95, 109-140).  A segment is a maximal
@@ -970,15 +1142,16 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
 void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                   const SolveParams& prm, int* launches, Prof* prof) {
     const int ntiles = cdiv(n, kScanBlock);
+    const int mtiles = cdiv(n, kMergeTile);  // >= ntiles
     cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
-    // tile states + tickets of the two single-pass scans (2*ntiles + 2 words)
-    cudaMemsetAsync(w.scanState, 0, sizeof(unsigned long long) * (size_t)(2 * ntiles + 2), s);
+    // tile states + tickets of the two single-pass scans (mtiles + ntiles + 2 words)
+    cudaMemsetAsync(w.scanState, 0, sizeof(unsigned long long) * (size_t)(mtiles + ntiles + 2), s);
     unsigned long long* st1 = w.scanState;
-    unsigned long long* st2 = w.scanState + ntiles;
-    int* tk = reinterpret_cast<int*>(w.scanState + 2 * ntiles);
-    k_merge_scatter<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+    unsigned long long* st2 = w.scanState + mtiles;
+    int* tk = reinterpret_cast<int*>(w.scanState + mtiles + ntiles);
+    k_merge_prep<<<cdiv(mtiles, kPrepVec), kMergeTile, 0, s>>>(w, L, n, w.org);  // org: free until the secular pass
     PMARK(BRGPU_K_SCATTER);
-    k_nn_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, prm.tol_scale, st1, tk);
+    k_merge_nn<<<mtiles, kMergeTile, 0, s>>>(w, L, n, prm.tol_scale, w.org, st1, tk);
     PMARK(BRGPU_K_NNFLAG);
     k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
     PMARK(BRGPU_K_WALK);
