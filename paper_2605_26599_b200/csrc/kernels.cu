@@ -4,10 +4,10 @@
 //
 // Level pipeline (grid tier; one launch per step covers ALL merges of a
 // level, positions are level-global so no host round trip is needed):
-//   k_merge_scatter  stable merge of the sorted children deflate.cpp:62-66, build_z deflate.cpp:31-41,
-//                    + per-merge max(|D|,|z|)            deflate.cpp:55-60
-//   k_nn_scan        small-z flags + compaction, 1 pass  deflate.cpp:70-75
-//   k_segment_walk   close-pole Givens walk per segment  deflate.cpp:76-95, 109-140
+//   k_merge_prep     per-merge max(|D|,|z|) + merge-path splits  deflate.cpp:55-60
+//   k_merge_nn       stable merge of the sorted children deflate.cpp:62-66, build_z deflate.cpp:31-41,
+//                    small-z flags + compaction, 1 pass  deflate.cpp:70-75
+//   k_segment_walk   close-pole groups per segment       deflate.cpp:76-95, 109-140
 //   k_surv_scan      survivor compaction, 1 pass         deflate.cpp:100-105
 //   k_secular        lane-per-root RootSM + CTA queue    secular.cpp:80-241 (tiled.cu, warp.cu: other tiers)
 //   k_zhat           refreshed weights, one pole/thread  secular.cpp:288-313
