@@ -21,6 +21,7 @@ OPT_USE_GRAPH = 4
 OPT_SUBTREE = 5
 OPT_VIRTUAL_RANKS = 6
 OPT_EXACT_PASSES = 7
+OPT_ROOT_SPLIT = 8
 
 
 class Stats(C.Structure):

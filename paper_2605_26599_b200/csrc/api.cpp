@@ -38,6 +38,9 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
                    const int* tFlags, const Work& w, int* launches, Prof* prof);
 void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
                   int* launches, Prof* prof);
+void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
+                       int part, int* launches, Prof* prof);
+int level_exchange_arrays(const SolveParams& prm, int part);
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
                         int* launches, Prof* prof);
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
@@ -168,6 +171,8 @@ struct Handle {
     int nranks = 1, rank = 0;
     ncclComm_t comm = nullptr;
     int virt = 1;
+    int root_split = 1;  // split the roots of shared top merges across ranks (BRGPU_OPT_ROOT_SPLIT)
+    int xerr = 0;        // first exchange error of the current solve (run_plan returns it)
     std::vector<std::unique_ptr<Handle>> subs;
 };
 
@@ -437,6 +442,8 @@ int ensure_work(Handle* h, int64_t n) {
     CUDA_TRY(h, cudaMalloc(&dbl, sizeof(double) * nd));
     Work& w = h->w;
     w.exact = h->exact;
+    w.own_P = 1;
+    w.own_r = 0;
     w.dw = dbl; w.ew = dbl + c; w.lam = dbl + 2 * c; w.blo = dbl + 3 * c; w.bhi = dbl + 4 * c;
     w.D = dbl + 5 * c; w.Z = dbl + 6 * c; w.R0 = dbl + 7 * c; w.R1 = dbl + 8 * c;
     w.dA = dbl + 9 * c; w.zA = dbl + 10 * c; w.z2A = dbl + 11 * c; w.r0A = dbl + 12 * c;
@@ -494,25 +501,72 @@ int status_message(Handle* h, int st) {
     }
 }
 
-void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* launches, Prof* prof) {
+LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh) {
+    LevelDev L;
+    L.mOff = p->d_mOff + lh.m0;
+    L.mSize = p->d_mSize + lh.m0;
+    L.mNL = p->d_mNL + lh.m0;
+    L.mFlags = p->d_mFlags + lh.m0;
+    L.mTol = h->mTol;
+    L.tileFirst = p->d_tileFirst + lh.tile0;
+    L.M = lh.M;
+    L.allSplit = lh.minSize > kSplitMinSizeHost ? 1 : 0;
+    return L;
+}
+
+SolveParams solve_params(Handle* h, int n) {
+    SolveParams prm{};
+    prm.n = n;
+    prm.zhat = h->zhat;
+    prm.patched = h->patched;
+    prm.tol_scale = h->tol_scale;
+    prm.sec_grid = h->sec_grid;
+    return prm;
+}
+
+// Root-range split of the shared top merges: rank r of P
+// owns active indices g = k*P + r, k < c; results travel through the gather
+// buffers (the dead dw and Z arrays of phase 2) in slot r.
+struct SplitCfg {
+    int P = 1, r = 0, c = 0;
+};
+
+// chunk per rank, or 0 when the gather buffers (capacity cap) cannot hold P*c
+int split_chunk(const Handle* h, int n, int P) {
+    const int c = (n + P - 1) / P;
+    return (int64_t)c * P <= h->cap ? c : 0;
+}
+
+void set_split(Handle* h, const SplitCfg* sc, SolveParams& prm) {
+    h->w.own_P = sc ? sc->P : 1;
+    h->w.own_r = sc ? sc->r : 0;
+    prm.xsplit = sc ? 1 : 0;
+    prm.xc = sc ? sc->c : 0;
+    prm.xA = h->w.dw;
+    prm.xB = h->w.Z;
+}
+
+int exchange_allgather(Handle* h, const SplitCfg& sc, int arrays);
+
+void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* launches, Prof* prof,
+                const SplitCfg* sc = nullptr) {
     cudaStream_t s = h->stream;
     const int n = p->n;
-    SolveParams prm{n, h->zhat, h->patched, h->tol_scale, h->sec_grid};
+    SolveParams prm = solve_params(h, n);
     for (const LevelHost& lh : levels) {
-        LevelDev L;
-        L.mOff = p->d_mOff + lh.m0;
-        L.mSize = p->d_mSize + lh.m0;
-        L.mNL = p->d_mNL + lh.m0;
-        L.mFlags = p->d_mFlags + lh.m0;
-        L.mTol = h->mTol;
-        L.tileFirst = p->d_tileFirst + lh.tile0;
-        L.M = lh.M;
-        L.allSplit = lh.minSize > kSplitMinSizeHost ? 1 : 0;
+        const LevelDev L = level_dev(h, p, lh);
         if (lh.fused) {
+            set_split(h, nullptr, prm);
             launch_level_fused(s, h->w, L, lh.G, lh.cap, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
                                h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
         } else {
-            launch_level(s, h->w, L, n, prm, launches, prof);
+            set_split(h, sc, prm);
+            for (int part = 0; part < 4; ++part) {
+                launch_level_part(s, h->w, L, n, prm, part, launches, prof);
+                if (const int k = level_exchange_arrays(prm, part))
+                    if (const int e = exchange_allgather(h, *sc, k)) h->xerr = h->xerr ? h->xerr : e;
+            }
+            set_split(h, nullptr, prm);
             if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
         }
     }
@@ -531,12 +585,22 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     run_levels(h, p, p->levels, launches, prof);
 }
 
-// Stage B: shared top merges, rescale, cross-block merge passes.
+// Stage B: shared top merges (roots split across ranks when enabled),
+// rescale, cross-block merge passes.
+void finish_stage_b(Handle* h, Plan* p, int* launches, Prof* prof);
 void run_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
+    SplitCfg sc;
+    const bool split = p->nranks > 1 && h->root_split && (sc.c = split_chunk(h, p->n, p->nranks)) > 0;
+    sc.P = p->nranks;
+    sc.r = p->rank;
+    run_levels(h, p, p->levels2, launches, prof, split ? &sc : nullptr);
+    finish_stage_b(h, p, launches, prof);
+}
+
+void finish_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
     cudaStream_t s = h->stream;
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
-    run_levels(h, p, p->levels2, launches, prof);
     launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
     double* src = h->w.lam;
     double* dst = h->w.D;
@@ -551,13 +615,14 @@ void run_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
 int exchange_nccl(Handle* h, Plan* p);
 
 int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
+    h->xerr = 0;
     run_stage_a(h, p, launches, prof);
     if (p->nranks > 1) {
         const int r = exchange_nccl(h, p);
         if (r) return r;
     }
     run_stage_b(h, p, launches, prof);
-    return BRGPU_OK;
+    return h->xerr;
 }
 
 // ---------------------------------------------------------------------------
@@ -569,6 +634,7 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -584,10 +650,11 @@ NcclApi& nccl_api() {
         a.CommInitRank = (decltype(a.CommInitRank))dlsym(lib, "ncclCommInitRank");
         a.CommDestroy = (decltype(a.CommDestroy))dlsym(lib, "ncclCommDestroy");
         a.Broadcast = (decltype(a.Broadcast))dlsym(lib, "ncclBroadcast");
+        a.AllGather = (decltype(a.AllGather))dlsym(lib, "ncclAllGather");
         a.GroupStart = (decltype(a.GroupStart))dlsym(lib, "ncclGroupStart");
         a.GroupEnd = (decltype(a.GroupEnd))dlsym(lib, "ncclGroupEnd");
         a.GetErrorString = (decltype(a.GetErrorString))dlsym(lib, "ncclGetErrorString");
-        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Broadcast && a.GroupStart &&
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Broadcast && a.AllGather && a.GroupStart &&
                a.GroupEnd && a.GetErrorString;
         return a;
     }();
@@ -614,6 +681,22 @@ int exchange_nccl(Handle* h, Plan* p) {
     return BRGPU_OK;
 }
 
+// In-place all-gather of the split exchange buffers (slot r of c doubles per
+// rank): one grouped call per array.  Virtual ranks copy between workspaces
+// instead (solve_virtual).
+int exchange_allgather(Handle* h, const SplitCfg& sc, int arrays) {
+    NcclApi& N = nccl_api();
+    if (!h->comm || !N.ok) return fail(h, BRGPU_ERR_NCCL, "root-range split without an NCCL communicator");
+    double* bufs[2] = {h->w.dw, h->w.Z};
+    ncclResult_t r = N.GroupStart();
+    for (int k = 0; k < arrays && r == ncclSuccess; ++k)
+        r = N.AllGather(bufs[k] + (size_t)sc.r * sc.c, bufs[k], (size_t)sc.c, ncclDouble, h->comm, h->stream);
+    const ncclResult_t r2 = N.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(h, BRGPU_ERR_NCCL, std::string("ncclAllGather: ") + N.GetErrorString(r != ncclSuccess ? r : r2));
+    return BRGPU_OK;
+}
+
 int ensure_buf_sizes(Handle* h, Plan* p);
 
 // P virtual ranks on this device (test mode): each runs its own phase-1 plan
@@ -636,6 +719,7 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
         u->leaf_cutoff = h->leaf_cutoff; u->zhat = h->zhat; u->patched = h->patched;
         u->use_graph = 0; u->subtree = h->subtree; u->trace = 0; u->exact = h->exact; u->w.exact = h->exact; u->tol_scale = h->tol_scale;
         u->sec_grid = h->sec_grid;
+        u->root_split = h->root_split;
         if (int r = ensure_work(u, n)) return fail(h, r, u->err);
         u->w.status = h->w.status;
         u->w.counters = h->w.counters;
@@ -660,7 +744,48 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
                 CUDA_TRY(h, cudaMemcpyAsync(b->w.bhi + rg.first, a->w.bhi + rg.first, bytes, cudaMemcpyDeviceToDevice, s));
             }
     int launches = 0;
-    run_stage_b(h->subs[0].get(), plans[0].get(), &launches, nullptr);
+    const int c = split_chunk(h->subs[0].get(), n, P);
+    if (h->root_split && c > 0) {
+        // phase 2 with the roots split across the P virtual ranks, in lockstep;
+        // the all-gathers are device copies of each rank's slot
+        const auto& L2 = plans[0]->levels2;
+        for (size_t li = 0; li < L2.size(); ++li) {
+            if (L2[li].fused) {
+                for (int k = 0; k < P; ++k) {
+                    Handle* u = h->subs[(size_t)k].get();
+                    run_levels(u, plans[(size_t)k].get(), {plans[(size_t)k]->levels2[li]}, &launches, nullptr);
+                }
+                continue;
+            }
+            for (int part = 0; part < 4; ++part) {
+                int arrays = 0;
+                for (int k = 0; k < P; ++k) {
+                    Handle* u = h->subs[(size_t)k].get();
+                    Plan* pk = plans[(size_t)k].get();
+                    SolveParams prm = solve_params(u, n);
+                    SplitCfg sc;
+                    sc.P = P; sc.r = k; sc.c = c;
+                    set_split(u, &sc, prm);
+                    launch_level_part(s, u->w, level_dev(u, pk, pk->levels2[li]), n, prm, part, &launches, nullptr);
+                    arrays = level_exchange_arrays(prm, part);
+                    set_split(u, nullptr, prm);
+                }
+                for (int k = 0; k < P && arrays; ++k)
+                    for (int j = 0; j < P; ++j) {
+                        if (j == k) continue;
+                        Handle* a = h->subs[(size_t)k].get();
+                        Handle* b = h->subs[(size_t)j].get();
+                        const size_t off = (size_t)k * c, bytes = sizeof(double) * (size_t)c;
+                        CUDA_TRY(h, cudaMemcpyAsync(b->w.dw + off, a->w.dw + off, bytes, cudaMemcpyDeviceToDevice, s));
+                        if (arrays > 1)
+                            CUDA_TRY(h, cudaMemcpyAsync(b->w.Z + off, a->w.Z + off, bytes, cudaMemcpyDeviceToDevice, s));
+                    }
+            }
+        }
+        finish_stage_b(h->subs[0].get(), plans[0].get(), &launches, nullptr);
+    } else {
+        run_stage_b(h->subs[0].get(), plans[0].get(), &launches, nullptr);
+    }
     CUDA_TRY(h, cudaMemcpyAsync(h->w.lam, h->subs[0]->w.lam, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     CUDA_TRY(h, cudaEventRecord(h->tev[3], s));
     CUDA_TRY(h, cudaGetLastError());
@@ -938,6 +1063,10 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
             h->w.exact = h->exact;
             if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
             return BRGPU_OK;
+        case BRGPU_OPT_ROOT_SPLIT:
+            h->root_split = v != 0;
+            if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
+            return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -957,6 +1086,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_USE_GRAPH: *v = h->use_graph; return BRGPU_OK;
         case BRGPU_OPT_SUBTREE: *v = h->subtree; return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS: *v = h->virt; return BRGPU_OK;
+        case BRGPU_OPT_ROOT_SPLIT: *v = h->root_split; return BRGPU_OK;
         case BRGPU_OPT_EXACT_PASSES: *v = h->exact; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }

@@ -55,6 +55,10 @@ struct Work {
     int* levelModes;  // bit0: level has lane-per-root merges, bit1: warp-per-root merges
     unsigned long long* counters;  // [0] evals
     int exact;       // test hook (BRGPU_OPT_EXACT_PASSES): every pole pass takes the exact path
+    // root-range split of the shared top merges: this rank
+    // solves the roots (and refreshed weights, boundary rows) of the active
+    // indices g with g % own_P == own_r; 1/0 outside split levels
+    int own_P, own_r;
 };
 
 // One level's merges (device pointers into the plan arrays).
@@ -80,6 +84,12 @@ struct SolveParams {
     int patched;
     double tol_scale;
     int sec_grid;  // CTAs of the secular kernel (fills the GPU; chunks adapt to the root count)
+    // root-range split exchange: results of owned indices are packed into slot
+    // own_r (xc entries) of the gather buffers xA/xB, which are all-gathered in place
+    int xsplit;
+    int xc;
+    double* xA;
+    double* xB;
 };
 
 }  // namespace brgpu

@@ -772,6 +772,7 @@ __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, L
         while (g < 0 && !exhausted) {
             const int q = atomicAdd(&s_next, 1);
             if (c0 + q >= c1) { exhausted = true; break; }
+            if (!owns(w, c0 + q)) continue;  // another rank's root (root-range split)
             const int m = w.aMerge[c0 + q];
             int ke;
             active_range(w, L, m, ks, ke);
@@ -861,7 +862,7 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
         const int m = w.aMerge[g];
         int ke;
         active_range(w, L, m, ks, ke);
-        if ((L.mFlags[m] & kMergeRoot) || split_mode(L.mSize[m], ke - ks)) act = false;
+        if ((L.mFlags[m] & kMergeRoot) || split_mode(L.mSize[m], ke - ks) || !owns(w, g)) act = false;
         K = ke - ks;
         i = g - ks;
         di = w.dA[g];
@@ -942,8 +943,9 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
         const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + ks, K, lam);
         p = off + pos;
         w.lam[p] = lam;
-        w.tau[g] = lam;  // tau is dead after this read: k_deflated_out searches the root values
-        if (L.mFlags[m] & kMergeRoot) act = false;
+        w.tau[g] = lam;  // tau, org are dead after these reads: k_deflated_out searches the
+        w.org[g] = p;    // root values, the root-range split exchange finds the position
+        if ((L.mFlags[m] & kMergeRoot) || !owns(w, g)) act = false;
     }
     double nn = 0.0, s0 = 0.0, s1 = 0.0;
     if (!__syncthreads_or(act)) return;
@@ -1139,50 +1141,126 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
     PMARK(BRGPU_K_LEAF);
 }
 
+// Root-range split exchange: a rank packs the results of the
+// active indices it owns (g = k*P + r) into slot r of the gather buffers, the
+// buffers are all-gathered in place (NCCL, or device copies for virtual
+// ranks), and every rank unpacks the other slots.  kind 0: roots (tau, org);
+// 1: refreshed weights; 2: boundary rows (at the parent position in org).
+__global__ void k_xpack(Work w, int n, int kind, int c, double* __restrict__ xA, double* __restrict__ xB) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int T = w.survPre[w.nnPre[n]];
+    const int g = k * w.own_P + w.own_r;
+    if (k >= c || g >= T) return;
+    const int slot = w.own_r * c + k;
+    if (kind == 0) {
+        xA[slot] = w.tau[g];
+        xB[slot] = (double)w.org[g];
+    } else if (kind == 1) {
+        xA[slot] = w.zA[g];
+    } else {
+        const int p = w.org[g];
+        xA[slot] = w.blo[p];
+        xB[slot] = w.bhi[p];
+    }
+}
+
+__global__ void k_xunpack(Work w, int n, int kind, int c, const double* __restrict__ xA,
+                          const double* __restrict__ xB) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int P = w.own_P;
+    if (idx >= P * c) return;
+    const int rr = idx / c, k = idx - rr * c;
+    const int T = w.survPre[w.nnPre[n]];
+    const int g = k * P + rr;
+    if (rr == w.own_r || g >= T) return;
+    if (kind == 0) {
+        w.tau[g] = xA[idx];
+        w.org[g] = (int)xB[idx];
+    } else if (kind == 1) {
+        w.zA[g] = xA[idx];
+    } else {
+        const int p = w.org[g];
+        w.blo[p] = xA[idx];
+        w.bhi[p] = xB[idx];
+    }
+}
+
+// One level of the grid tier, in four parts separated by the points where a
+// root-range split exchanges results (prm.xsplit): 0 deflation + secular roots,
+// 1 refreshed weights, 2 boundary rows + root placement, 3 deflated placement.
+// Without a split the parts run back to back.
+void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
+                       int part, int* launches, Prof* prof) {
+    const bool lane_tier = !L.allSplit;  // all merges > kSplitMinSize: warp tier only
+    const bool x = prm.xsplit != 0;
+    const int xg = cdiv(prm.xc, 256), xu = cdiv(prm.xc * w.own_P, 256);
+    int nl = 0;
+    if (part == 0) {
+        const int ntiles = cdiv(n, kScanBlock);
+        const int mtiles = cdiv(n, kMergeTile);  // >= ntiles
+        cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
+        // tile states + tickets of the two single-pass scans (mtiles + ntiles + 2 words)
+        cudaMemsetAsync(w.scanState, 0, sizeof(unsigned long long) * (size_t)(mtiles + ntiles + 2), s);
+        unsigned long long* st1 = w.scanState;
+        unsigned long long* st2 = w.scanState + mtiles;
+        int* tk = reinterpret_cast<int*>(w.scanState + mtiles + ntiles);
+        k_merge_prep<<<cdiv(mtiles, kPrepVec), kMergeTile, 0, s>>>(w, L, n, w.org);  // org: free until the secular pass
+        PMARK(BRGPU_K_SCATTER);
+        k_merge_nn<<<mtiles, kMergeTile, 0, s>>>(w, L, n, prm.tol_scale, w.org, st1, tk);
+        PMARK(BRGPU_K_NNFLAG);
+        k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
+        PMARK(BRGPU_K_WALK);
+        k_surv_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, st2, tk + 1);
+        PMARK(BRGPU_K_SURVWRITE);
+        nl += 4;
+        if (lane_tier) {
+            cudaMemsetAsync(w.levelModes, 0, sizeof(int), s);
+            k_level_modes<<<cdiv(L.M, 256), 256, 0, s>>>(w, L);
+            k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
+            launch_secular_tiled(s, w, L, n, prm);
+            nl += 3;
+        }
+        launch_secular_warp(s, w, L, n, prm);
+        nl += 1;
+        if (x) { k_xpack<<<xg, 256, 0, s>>>(w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
+        PMARK(BRGPU_K_SECULAR);
+    } else if (part == 1) {
+        if (x) { k_xunpack<<<xu, 256, 0, s>>>(w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
+        if (prm.zhat) {
+            if (lane_tier) { k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n); ++nl; }
+            launch_zhat_warp(s, w, L, n, prm);
+            ++nl;
+            if (x) { k_xpack<<<xg, 256, 0, s>>>(w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
+            PMARK(BRGPU_K_ZHAT);
+        }
+    } else if (part == 2) {
+        if (x && prm.zhat) { k_xunpack<<<xu, 256, 0, s>>>(w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
+        if (lane_tier) { k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n); ++nl; }
+        launch_rows_warp(s, w, L, n, prm);
+        ++nl;
+        if (x) { k_xpack<<<xg, 256, 0, s>>>(w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
+        PMARK(BRGPU_K_ROWS);
+    } else {
+        if (x) { k_xunpack<<<xu, 256, 0, s>>>(w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
+        k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+        ++nl;
+        PMARK(BRGPU_K_DEFLATED);
+    }
+    *launches += nl;
+}
+
+// Does a split level exchange after `part` (and which arrays: 1 = xA, 2 = xA + xB)?
+int level_exchange_arrays(const SolveParams& prm, int part) {
+    if (!prm.xsplit) return 0;
+    if (part == 0) return 2;             // roots: tau, org
+    if (part == 1) return prm.zhat ? 1 : 0;  // refreshed weights
+    if (part == 2) return 2;             // rows: blo, bhi
+    return 0;
+}
+
 void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                   const SolveParams& prm, int* launches, Prof* prof) {
-    const int ntiles = cdiv(n, kScanBlock);
-    const int mtiles = cdiv(n, kMergeTile);  // >= ntiles
-    cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
-    // tile states + tickets of the two single-pass scans (mtiles + ntiles + 2 words)
-    cudaMemsetAsync(w.scanState, 0, sizeof(unsigned long long) * (size_t)(mtiles + ntiles + 2), s);
-    unsigned long long* st1 = w.scanState;
-    unsigned long long* st2 = w.scanState + mtiles;
-    int* tk = reinterpret_cast<int*>(w.scanState + mtiles + ntiles);
-    k_merge_prep<<<cdiv(mtiles, kPrepVec), kMergeTile, 0, s>>>(w, L, n, w.org);  // org: free until the secular pass
-    PMARK(BRGPU_K_SCATTER);
-    k_merge_nn<<<mtiles, kMergeTile, 0, s>>>(w, L, n, prm.tol_scale, w.org, st1, tk);
-    PMARK(BRGPU_K_NNFLAG);
-    k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
-    PMARK(BRGPU_K_WALK);
-    k_surv_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, st2, tk + 1);
-    PMARK(BRGPU_K_SURVWRITE);
-    // levels whose merges are all larger than kSplitMinSize run only the
-    // warp-per-root tier (known from the plan: no mode pass, no lane-tier launches)
-    const bool lane_tier = !L.allSplit;
-    int nl = 4;  // scatter, nn_scan, walk, surv_scan
-    if (lane_tier) {
-        cudaMemsetAsync(w.levelModes, 0, sizeof(int), s);
-        k_level_modes<<<cdiv(L.M, 256), 256, 0, s>>>(w, L);
-        k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
-        launch_secular_tiled(s, w, L, n, prm);
-        nl += 3;
-    }
-    launch_secular_warp(s, w, L, n, prm);
-    PMARK(BRGPU_K_SECULAR);
-    nl += 1;
-    if (prm.zhat) {
-        if (lane_tier) k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
-        launch_zhat_warp(s, w, L, n, prm);
-        PMARK(BRGPU_K_ZHAT);
-        nl += lane_tier ? 2 : 1;
-    }
-    if (lane_tier) k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n);
-    launch_rows_warp(s, w, L, n, prm);
-    PMARK(BRGPU_K_ROWS);
-    k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
-    PMARK(BRGPU_K_DEFLATED);
-    *launches += nl + (lane_tier ? 3 : 2);  // rows (lane), rows_warp, deflated_out
+    for (int part = 0; part < 4; ++part) launch_level_part(s, w, L, n, prm, part, launches, prof);
 }
 
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,

@@ -65,6 +65,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
         while (g < 0 && !exhausted) {
             const int q = atomicAdd(&s_next, 1);
             if (c0 + q >= c1) { exhausted = true; break; }
+            if (!owns(w, c0 + q)) continue;  // another rank's root (root-range split)
             const int m = w.aMerge[c0 + q];
             int ke;
             const int off = L.mOff[m];

@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
             q = __shfl_sync(0xffffffffu, q, 0);
             if (c0 + q >= c1) { exhausted = true; break; }
             const int gg = c0 + q;
+            if (!owns(w, gg)) continue;  // another rank's root (root-range split)
             const int m = w.aMerge[gg];
             int ke;
             merge_active(w, L, m, ks, ke);
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
             const int m = w.aMerge[g];
             int ke;
             merge_active(w, L, m, ks, ke);
-            act = split_mode(L.mSize[m], ke - ks) && !(L.mFlags[m] & kMergeRoot);
+            act = split_mode(L.mSize[m], ke - ks) && !(L.mFlags[m] & kMergeRoot) && owns(w, g);
             K = ke - ks;
             i = g - ks;
             di = w.dA[g];
@@ -283,9 +284,10 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
                 p = off + pos;
                 if (lane == 0) {
                     w.lam[p] = lam;
-                    w.tau[g] = lam;  // dead after the read above: k_deflated_out searches root values
+                    w.tau[g] = lam;  // dead after the reads above: k_deflated_out searches root
+                    w.org[g] = p;    // values, the root-range split exchange finds the position
                 }
-                rows = !(L.mFlags[m] & kMergeRoot);
+                rows = !(L.mFlags[m] & kMergeRoot) && owns(w, g);
             }
         }
         if (!__syncthreads_or(rows)) continue;
