@@ -53,7 +53,10 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 void init_fused_attributes();
 constexpr int kFuseMaxElems = 1024;
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
-constexpr int kSplitMinSizeHost = 8192;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
+#ifndef BRGPU_SPLIT_MIN_SIZE
+#define BRGPU_SPLIT_MIN_SIZE 8192
+#endif
+constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
 constexpr int kFuseMaxMergesHost = 128;
 
 void init_kernel_attributes();
