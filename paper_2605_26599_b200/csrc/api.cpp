@@ -50,6 +50,8 @@ void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, co
 void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
                         const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
                         int* launches, Prof* prof);
+void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int ngroups, const int2* tab,
+                         const SolveParams& prm, int* launches, Prof* prof);
 void init_fused_attributes();
 constexpr int kFuseMaxElems = 1024;
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
@@ -106,6 +108,12 @@ struct Plan {
     std::vector<int> mOff, mSize, mNL, mFlags, mLevel;
     std::vector<int> tileFirst;
     std::vector<int> gFirst, gCount;  // fused groups (level-local first merge, count)
+    // runs of consecutive small-shape fused levels launched as one kernel:
+    // (first level index in `levels`, level count, groups, offset in mlTab)
+    struct MultiRun { int lev0, nlev, G, tab0; };
+    std::vector<MultiRun> multi;
+    std::vector<int> mlTab;           // (first, count) per (group, level), level-local
+    int2* d_mlTab = nullptr;
     std::vector<LevelHost> levels;    // phase 1: merges owned by this rank (all, when nranks == 1)
     std::vector<LevelHost> levels2;   // phase 2: top merges shared by all ranks (after the exchange)
     int nranks = 1, rank = 0;
@@ -291,6 +299,54 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
     }
 }
 
+// Runs of >= 2 consecutive small-shape fused levels in which every group of
+// the run's top level is exactly tiled by whole merges at each lower level
+// (true for complete trees such as n = 2^k; otherwise the levels stay
+// separate launches): one k_levels_fused launch per run.
+void plan_fused_runs(Plan* p) {
+    auto& lv = p->levels;
+    size_t i = 0;
+    while (i < lv.size()) {
+        size_t j = i;
+        while (j < lv.size() && lv[j].fused && lv[j].cap == kFuseSmallElems &&
+               (j == i || lv[j].level == lv[j - 1].level + 1) && j - i < (size_t)kMaxFusedRun)
+            ++j;
+        if (j - i < 2) { i = std::max(j, i + 1); continue; }
+        const LevelHost& top = lv[j - 1];
+        const int nlev = (int)(j - i);
+        std::vector<int> tab;
+        std::vector<int> covered(j - i, 0);  // every merge of every level of the run must be in a group
+        bool ok = true;
+        for (int q = 0; q < top.G && ok; ++q) {
+            const int gf = p->gFirst[(size_t)top.g0 + q], gc = p->gCount[(size_t)top.g0 + q];
+            const int a = top.m0 + gf, z = top.m0 + gf + gc - 1;
+            const int start = p->mOff[(size_t)a], end = p->mOff[(size_t)z] + p->mSize[(size_t)z];
+            for (size_t l = i; l < j && ok; ++l) {
+                const LevelHost& L = lv[l];
+                const int* mo = p->mOff.data() + L.m0;
+                const int* ms = p->mSize.data() + L.m0;
+                const int first = (int)(std::lower_bound(mo, mo + L.M, start) - mo);
+                int pos = start, c = 0;
+                while (first + c < L.M && mo[first + c] < end) {
+                    if (mo[first + c] != pos) { ok = false; break; }
+                    pos += ms[first + c];
+                    ++c;
+                }
+                ok = ok && pos == end && c >= 1 && c <= kFuseMaxMergesHost;
+                covered[l - i] += c;
+                tab.push_back(first);
+                tab.push_back(c);
+            }
+        }
+        for (size_t l = i; l < j && ok; ++l) ok = covered[l - i] == lv[l].M;
+        if (ok) {
+            p->multi.push_back({(int)i, nlev, top.G, (int)p->mlTab.size() / 2});
+            p->mlTab.insert(p->mlTab.end(), tab.begin(), tab.end());
+        }
+        i = j;
+    }
+}
+
 // Plan of rank `rank` out of `nranks` (1: the whole solve).  Blocks of at
 // least 2^D * 2(cutoff+1) elements (D = floor(log2 nranks)) are split by
 // subtree; smaller blocks go to ranks in contiguous chunks of the total size.
@@ -358,6 +414,7 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
     }
     add_levels(p.get(), mine, fuse, p->levels);
     add_levels(p.get(), top, fuse, p->levels2);
+    plan_fused_runs(p.get());
     // final merge passes: runs = blocks, merged pairwise inside each segment;
     // a segment with an odd run count gets an empty partner so that pairs
     // (2k, 2k+1) of a pass table never straddle segments.
@@ -400,6 +457,7 @@ int upload_plan(Handle* h, Plan* p) {
     const size_t oTile = put(p->tileFirst);
     const size_t oB = put(p->bstart);
     const size_t oGF = put(p->gFirst), oGC = put(p->gCount);
+    const size_t oML = put(p->mlTab);  // int2 pairs: 8-byte aligned (offsets are multiples of 4 ints)
     std::vector<size_t> oRuns;
     for (auto& rp : p->runPasses) oRuns.push_back(put(rp));
     p->devInts = buf.size();
@@ -410,6 +468,7 @@ int upload_plan(Handle* h, Plan* p) {
     p->d_mOff = p->dev + oMOff; p->d_mSize = p->dev + oMSize; p->d_mNL = p->dev + oMNL;
     p->d_mFlags = p->dev + oMF; p->d_tileFirst = p->dev + oTile; p->d_bstart = p->dev + oB;
     p->d_gFirst = p->dev + oGF; p->d_gCount = p->dev + oGC;
+    p->d_mlTab = reinterpret_cast<int2*>(p->dev + oML);
     for (size_t o : oRuns) p->d_runs.push_back(p->dev + o);
     return BRGPU_OK;
 }
@@ -556,7 +615,25 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
     cudaStream_t s = h->stream;
     const int n = p->n;
     SolveParams prm = solve_params(h, n);
-    for (const LevelHost& lh : levels) {
+    const bool phase1 = &levels == &p->levels;
+    size_t mr = 0;
+    for (size_t li = 0; li < levels.size(); ++li) {
+        const LevelHost& lh = levels[li];
+        if (phase1 && mr < p->multi.size() && p->multi[mr].lev0 == (int)li) {
+            const Plan::MultiRun& run = p->multi[mr++];
+            FusedRun fr{};
+            fr.nlev = run.nlev;
+            for (int l = 0; l < run.nlev; ++l) {
+                const LevelHost& ll = levels[li + (size_t)l];
+                fr.L[l] = level_dev(h, p, ll);
+                fr.trace[l] = h->trace ? h->traceBuf + 2 * ll.m0 : nullptr;
+            }
+            set_split(h, nullptr, prm);
+            launch_levels_fused(s, h->w, fr, run.G, p->d_mlTab + run.tab0, prm,
+                                launches, prof);
+            li += (size_t)run.nlev - 1;
+            continue;
+        }
         const LevelDev L = level_dev(h, p, lh);
         if (lh.fused) {
             set_split(h, nullptr, prm);

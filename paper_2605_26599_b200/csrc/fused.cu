@@ -130,16 +130,13 @@ __device__ __forceinline__ int upper_index(const int* a, int cnt, int x) {
     return lo;
 }
 
+// One group of merges of one level: merges m0 .. m0+cnt-1 (level-local
+// indices) tile a contiguous range; state in and out through w.lam/blo/bhi.
 template <int kFuseMax, int kFuseThreads>
-__global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
-k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
-              SolveParams prm, int* __restrict__ traceOut) {
-    extern __shared__ __align__(16) unsigned char fuse_raw[];
-    using Smem = FuseSmem<kFuseMax, kFuseThreads>;
-    Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
+__device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, const int m0, const int cnt,
+                                            const SolveParams& prm, int* __restrict__ traceOut,
+                                            FuseSmem<kFuseMax, kFuseThreads>& S) {
     const int tid = threadIdx.x;
-    const int m0 = gFirst[blockIdx.x];
-    const int cnt = gCount[blockIdx.x];
     const int base = L.mOff[m0];
 
     // ---- metadata + inputs -------------------------------------------------
@@ -487,6 +484,35 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
     }
 }
 
+template <int kFuseMax, int kFuseThreads>
+__global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
+k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
+              SolveParams prm, int* __restrict__ traceOut) {
+    extern __shared__ __align__(16) unsigned char fuse_raw[];
+    using Smem = FuseSmem<kFuseMax, kFuseThreads>;
+    Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
+    fused_group<kFuseMax, kFuseThreads>(w, L, gFirst[blockIdx.x], gCount[blockIdx.x], prm, traceOut, S);
+}
+
+// Several consecutive levels in one launch: CTA b owns one group of the top
+// level and, below it, the merges of every lower level of the run that tile
+// the same range (tab[b*nlev + l] = (first, count)); a level's outputs are
+// the next level's inputs, so the CTA moves from level to level with a block
+// barrier instead of a grid-wide kernel boundary (the data stays in L1/L2),
+// and different CTAs' root-queue tails overlap across levels.
+template <int kFuseMax, int kFuseThreads>
+__global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
+k_levels_fused(Work w, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
+    extern __shared__ __align__(16) unsigned char fuse_raw[];
+    using Smem = FuseSmem<kFuseMax, kFuseThreads>;
+    Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
+    for (int l = 0; l < run.nlev; ++l) {
+        const int2 fc = tab[blockIdx.x * run.nlev + l];
+        fused_group<kFuseMax, kFuseThreads>(w, run.L[l], fc.x, fc.y, prm, run.trace[l], S);
+        __syncthreads();
+    }
+}
+
 void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
                         const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
                         int* launches, Prof* prof) {
@@ -500,6 +526,14 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
 }
 
+void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int ngroups, const int2* tab,
+                         const SolveParams& prm, int* launches, Prof* prof) {
+    k_levels_fused<512, kSmallThreads><<<ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s>>>(
+        w, run, tab, prm);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
+}
+
 static_assert(sizeof(FuseSmem<1024, kBigThreads>) <= 113 * 1024, "two fused CTAs must fit one SM (227 KB)");
 static_assert(sizeof(FuseSmem<512, kSmallThreads>) <= 56 * 1024, "four small fused CTAs must fit one SM");
 
@@ -507,6 +541,8 @@ void init_fused_attributes() {
     cudaFuncSetAttribute(k_level_fused<1024, kBigThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(FuseSmem<1024, kBigThreads>));
     cudaFuncSetAttribute(k_level_fused<512, kSmallThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(FuseSmem<512, kSmallThreads>));
+    cudaFuncSetAttribute(k_levels_fused<512, kSmallThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(FuseSmem<512, kSmallThreads>));
 }
 

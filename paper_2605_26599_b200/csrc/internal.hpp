@@ -73,6 +73,14 @@ struct LevelDev {
     int allSplit;              // every merge of the level is larger than kSplitMinSize (warp tier only)
 };
 
+// A run of consecutive fused levels launched as one kernel (k_levels_fused).
+constexpr int kMaxFusedRun = 8;
+struct FusedRun {
+    LevelDev L[kMaxFusedRun];
+    int* trace[kMaxFusedRun];
+    int nlev;
+};
+
 // Optional per-kernel profiling (brgpu_profile_kernels): the launchers call
 // prof_mark after every launch; api.cpp records a CUDA event per mark.
 struct Prof;
