@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "internal.hpp"
+#include "launch.cuh"
 #include "numerics.cuh"
 
 namespace brgpu {
@@ -488,6 +489,7 @@ template <int kFuseMax, int kFuseThreads>
 __global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
 k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
               SolveParams prm, int* __restrict__ traceOut) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char fuse_raw[];
     using Smem = FuseSmem<kFuseMax, kFuseThreads>;
     Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
@@ -503,6 +505,7 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
 template <int kFuseMax, int kFuseThreads>
 __global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
 k_levels_fused(Work w, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char fuse_raw[];
     using Smem = FuseSmem<kFuseMax, kFuseThreads>;
     Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
@@ -517,10 +520,10 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
                         const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
                         int* launches, Prof* prof) {
     if (cap <= 512)
-        k_level_fused<512, kSmallThreads><<<ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s>>>(w, L, gFirst, gCount, prm,
+        launch_pdl(k_level_fused<512, kSmallThreads>, ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s, w, L, gFirst, gCount, prm,
                                                                                  traceOut);
     else
-        k_level_fused<1024, kBigThreads><<<ngroups, kBigThreads, sizeof(FuseSmem<1024, kBigThreads>), s>>>(w, L, gFirst, gCount, prm,
+        launch_pdl(k_level_fused<1024, kBigThreads>, ngroups, kBigThreads, sizeof(FuseSmem<1024, kBigThreads>), s, w, L, gFirst, gCount, prm,
                                                                                    traceOut);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
@@ -528,7 +531,7 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 
 void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int ngroups, const int2* tab,
                          const SolveParams& prm, int* launches, Prof* prof) {
-    k_levels_fused<512, kSmallThreads><<<ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s>>>(
+    launch_pdl(k_levels_fused<512, kSmallThreads>, ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s, 
         w, run, tab, prm);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);

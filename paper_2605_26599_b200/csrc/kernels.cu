@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "internal.hpp"
+#include "launch.cuh"
 #include "numerics.cuh"
 
 namespace brgpu {
@@ -173,6 +174,7 @@ __device__ __forceinline__ int find_block(const int* __restrict__ bstart, int nb
 __global__ void k_block_scale(int n, const double* __restrict__ d, const double* __restrict__ e,
                               const int* __restrict__ bstart, int nblk,
                               unsigned long long* __restrict__ sbits) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int b = (i < n && nblk > 1) ? find_block(bstart, nblk, i) : 0;
     double v = 0.0;
@@ -206,6 +208,7 @@ __device__ __forceinline__ double block_scale_of(unsigned long long bits) {
 __global__ void k_apply_scale(int n, const int* __restrict__ bstart, int nblk,
                               const unsigned long long* __restrict__ sbits,
                               double* __restrict__ dw, double* __restrict__ ew) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
@@ -219,6 +222,7 @@ __global__ void k_apply_scale(int n, const int* __restrict__ bstart, int nblk,
 // the cuts commute: one thread per internal node, bitwise equal to pre-order.
 __global__ void k_cuts(int ncut, const int* __restrict__ cutPos, const double* __restrict__ ew,
                        double* __restrict__ dw) {
+    pdl_entry();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ncut) return;
     const int m = cutPos[t];
@@ -251,6 +255,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __r
                                                        double* __restrict__ blo,
                                                        double* __restrict__ bhi,
                                                        int* __restrict__ status) {
+    pdl_entry();
     extern __shared__ double leaf_sm[];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntask) return;
@@ -392,6 +397,7 @@ constexpr int kPrepVec = 4;  // merge tiles per k_merge_prep CTA: the whole leve
 //  * the merge-path diagonal split at each tile's first position (warp k for
 //    tile k, 32-ary search), kept in split[tile] for k_merge_nn.
 __global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w, LevelDev L, int n, int* __restrict__ split) {
+    pdl_entry();
     __shared__ unsigned long long s_max[kPrepVec][kMergeTile / 32];
     __shared__ int s_m[kPrepVec][kMergeTile / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -471,6 +477,7 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w, LevelDev L, i
 __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int n, double tol_scale,
                                                          const int* __restrict__ split,
                                                          unsigned long long* state, int* ticket) {
+    pdl_entry();
     // inputs (lam, blo, bhi), then the merged tile (D, Z, R0 alias them; R1)
     __shared__ double s_v[kMergeTile], s_b0[kMergeTile], s_b1[kMergeTile], s_R1[kMergeTile];
     double* s_D = s_v;
@@ -578,6 +585,7 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int
 // and records each member's prefix (Q, S0, S1) at its position in the free
 // lam/blo/bhi slots; k_surv_scan finishes the members in parallel.
 __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
+    pdl_entry();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int NN = w.nnPre[n];
     if (q >= NN) return;
@@ -651,6 +659,7 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
 // one pass; tile 0 always runs so survPre[NN] is written even when NN == 0
 __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, int n,
                                                           unsigned long long* state, int* ticket) {
+    pdl_entry();
     __shared__ int s_tile, s_pref;
     const int NN = w.nnPre[n];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -687,9 +696,21 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, in
     if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= NN) w.survPre[NN] = base + tot;
 }
 
+// Start of a grid-tier level: zero the per-merge scale words, the look-back
+// tile states + tickets and the tier-mode word.
+__global__ void k_level_zero(unsigned long long* __restrict__ mTol, int M, unsigned long long* __restrict__ st,
+                             int words, int* __restrict__ modes) {
+    pdl_entry();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < M) mTol[i] = 0ULL;
+    if (i < words) st[i] = 0ULL;
+    if (i == 0) *modes = 0;
+}
+
 // Which secular tiers a level needs (merges with K > 0): bit0 lane-per-root,
 // bit1 warp-per-root.  Kernels of an absent tier exit on their first load.
 __global__ void k_level_modes(Work w, LevelDev L) {
+    pdl_entry();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     int bits = 0;
     if (m < L.M) {
@@ -745,6 +766,7 @@ constexpr int kSecWinQ = BRGPU_SEC_WIN;
 // as soon as its root converges.  Evaluations are branch-free pole loops over
 // shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
 __global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, LevelDev L, int n, int patched) {
+    pdl_entry();
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ double2 s_snap[kSecBlock];
     __shared__ int s_next;
@@ -848,6 +870,7 @@ __global__ void k_selftest_rcp(long long count, unsigned long long seed, unsigne
 // tiles of kWin covering the CTA's window (one tile when it fits), in root
 // order, so the product order is the checker's.
 __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
+    pdl_entry();
     __shared__ double s_dorg[kWin], s_tau[kWin], s_dj[kWin];
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -913,6 +936,7 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
 // plus placement of lambda_j in the parent's ascending order.  Poles (d, zhat,
 // r0, r1) stream through shared memory in tiles, in pole order.
 __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
+    pdl_entry();
     __shared__ double s_d[kWin], s_zh[kWin], s_r0[kWin], s_r1[kWin];
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -996,6 +1020,7 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
 
 // deflated columns: parent position t + #{roots < D}
 __global__ void k_deflated_out(Work w, LevelDev L, int n) {
+    pdl_entry();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int m = find_merge(L, k);
@@ -1026,6 +1051,7 @@ __global__ void k_deflated_out(Work w, LevelDev L, int n) {
 
 // per-merge (nn, K) for the trace
 __global__ void k_level_trace(Work w, LevelDev L, int* __restrict__ out) {
+    pdl_entry();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= L.M) return;
     const int off = L.mOff[m], end = off + L.mSize[m];
@@ -1039,6 +1065,7 @@ __global__ void k_level_trace(Work w, LevelDev L, int* __restrict__ out) {
 // ---------------------------------------------------------------------------
 __global__ void k_rescale(int n, const int* __restrict__ bstart, int nblk,
                           const unsigned long long* __restrict__ sbits, double* __restrict__ lam) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
@@ -1049,6 +1076,7 @@ __global__ void k_rescale(int n, const int* __restrict__ bstart, int nblk,
 // one pass of a bottom-up stable merge sort over runs [rs[r], rs[r+1])
 __global__ void k_merge_runs(int n, const double* __restrict__ src, double* __restrict__ dst,
                              const int* __restrict__ rs, int nruns) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int r = find_block(rs, nruns, i);
@@ -1110,11 +1138,11 @@ void launch_scan_input_batched(cudaStream_t s, int batch, int n, const double* d
 
 void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned long long* sbits,
                     double* dw, double* ew, int ncut, const int* cutPos, int* launches, Prof* prof) {
-    k_block_scale<<<cdiv(n, 256), 256, 0, s>>>(n, dw, ew, bstart, nblk, sbits);
-    k_apply_scale<<<cdiv(n, 256), 256, 0, s>>>(n, bstart, nblk, sbits, dw, ew);
+    launch_pdl(k_block_scale, cdiv(n, 256), 256, 0, s, n, dw, ew, bstart, nblk, sbits);
+    launch_pdl(k_apply_scale, cdiv(n, 256), 256, 0, s, n, bstart, nblk, sbits, dw, ew);
     *launches += 2;
     if (ncut > 0) {
-        k_cuts<<<cdiv(ncut, 256), 256, 0, s>>>(ncut, cutPos, ew, dw);
+        launch_pdl(k_cuts, cdiv(ncut, 256), 256, 0, s, ncut, cutPos, ew, dw);
         *launches += 1;
     }
     PMARK(BRGPU_K_PREPARE);
@@ -1126,15 +1154,15 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
     const int grid = cdiv(ntask, kLeafThreads);
     if (maxm <= 16) {
         const size_t sm = leaf_smem_bytes<16>();
-        k_leaf<16><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+        launch_pdl(k_leaf<16>, grid, kLeafThreads, sm, s, ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
     } else if (maxm <= 26) {
         const size_t sm = leaf_smem_bytes<26>();
-        k_leaf<26><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+        launch_pdl(k_leaf<26>, grid, kLeafThreads, sm, s, ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
     } else {
         const size_t sm = leaf_smem_bytes<32>();
-        k_leaf<32><<<grid, kLeafThreads, sm, s>>>(ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
+        launch_pdl(k_leaf<32>, grid, kLeafThreads, sm, s, ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
                                                   w.blo, w.bhi, w.status);
     }
     *launches += 1;
@@ -1147,6 +1175,7 @@ void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const i
 // ranks), and every rank unpacks the other slots.  kind 0: roots (tau, org);
 // 1: refreshed weights; 2: boundary rows (at the parent position in org).
 __global__ void k_xpack(Work w, int n, int kind, int c, double* __restrict__ xA, double* __restrict__ xB) {
+    pdl_entry();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int T = w.survPre[w.nnPre[n]];
     const int g = k * w.own_P + w.own_r;
@@ -1166,6 +1195,7 @@ __global__ void k_xpack(Work w, int n, int kind, int c, double* __restrict__ xA,
 
 __global__ void k_xunpack(Work w, int n, int kind, int c, const double* __restrict__ xA,
                           const double* __restrict__ xB) {
+    pdl_entry();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     const int P = w.own_P;
     if (idx >= P * c) return;
@@ -1198,55 +1228,56 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
     if (part == 0) {
         const int ntiles = cdiv(n, kScanBlock);
         const int mtiles = cdiv(n, kMergeTile);  // >= ntiles
-        cudaMemsetAsync(L.mTol, 0, sizeof(unsigned long long) * (size_t)L.M, s);
-        // tile states + tickets of the two single-pass scans (mtiles + ntiles + 2 words)
-        cudaMemsetAsync(w.scanState, 0, sizeof(unsigned long long) * (size_t)(mtiles + ntiles + 2), s);
+        // per-merge scales, tile states + tickets of the two single-pass scans
+        // (mtiles + ntiles + 2 words) and the mode word: zeroed by a kernel so the
+        // level's launches form one programmatic-dependency chain
+        launch_pdl(k_level_zero, cdiv(max(L.M, mtiles + ntiles + 2), 256), 256, 0, s, L.mTol, L.M, w.scanState,
+                   mtiles + ntiles + 2, w.levelModes);
         unsigned long long* st1 = w.scanState;
         unsigned long long* st2 = w.scanState + mtiles;
         int* tk = reinterpret_cast<int*>(w.scanState + mtiles + ntiles);
-        k_merge_prep<<<cdiv(mtiles, kPrepVec), kMergeTile, 0, s>>>(w, L, n, w.org);  // org: free until the secular pass
+        launch_pdl(k_merge_prep, cdiv(mtiles, kPrepVec), kMergeTile, 0, s, w, L, n, w.org);  // org: free until the secular pass
         PMARK(BRGPU_K_SCATTER);
-        k_merge_nn<<<mtiles, kMergeTile, 0, s>>>(w, L, n, prm.tol_scale, w.org, st1, tk);
+        launch_pdl(k_merge_nn, mtiles, kMergeTile, 0, s, w, L, n, prm.tol_scale, w.org, st1, tk);
         PMARK(BRGPU_K_NNFLAG);
-        k_segment_walk<<<cdiv(n, 256), 256, 0, s>>>(w, L, n, prm.tol_scale);
+        launch_pdl(k_segment_walk, cdiv(n, 256), 256, 0, s, w, L, n, prm.tol_scale);
         PMARK(BRGPU_K_WALK);
-        k_surv_scan<<<ntiles, kScanBlock, 0, s>>>(w, L, n, st2, tk + 1);
+        launch_pdl(k_surv_scan, ntiles, kScanBlock, 0, s, w, L, n, st2, tk + 1);
         PMARK(BRGPU_K_SURVWRITE);
         nl += 4;
         if (lane_tier) {
-            cudaMemsetAsync(w.levelModes, 0, sizeof(int), s);
-            k_level_modes<<<cdiv(L.M, 256), 256, 0, s>>>(w, L);
-            k_secular<<<prm.sec_grid, kSecBlock, 0, s>>>(w, L, n, prm.patched);
+            launch_pdl(k_level_modes, cdiv(L.M, 256), 256, 0, s, w, L);
+            launch_pdl(k_secular, prm.sec_grid, kSecBlock, 0, s, w, L, n, prm.patched);
             launch_secular_tiled(s, w, L, n, prm);
             nl += 3;
         }
         launch_secular_warp(s, w, L, n, prm);
         nl += 1;
-        if (x) { k_xpack<<<xg, 256, 0, s>>>(w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
+        if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
         PMARK(BRGPU_K_SECULAR);
     } else if (part == 1) {
-        if (x) { k_xunpack<<<xu, 256, 0, s>>>(w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
+        if (x) { launch_pdl(k_xunpack, xu, 256, 0, s, w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
         if (prm.zhat) {
-            if (lane_tier) { k_zhat<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n); ++nl; }
+            if (lane_tier) { launch_pdl(k_zhat, cdiv(n, kSecBlock), kSecBlock, 0, s, w, L, n); ++nl; }
             launch_zhat_warp(s, w, L, n, prm);
             ++nl;
-            if (x) { k_xpack<<<xg, 256, 0, s>>>(w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
+            if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
             PMARK(BRGPU_K_ZHAT);
         }
     } else if (part == 2) {
-        if (x && prm.zhat) { k_xunpack<<<xu, 256, 0, s>>>(w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
-        if (lane_tier) { k_rows<<<cdiv(n, kSecBlock), kSecBlock, 0, s>>>(w, L, n); ++nl; }
+        if (x && prm.zhat) { launch_pdl(k_xunpack, xu, 256, 0, s, w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
+        if (lane_tier) { launch_pdl(k_rows, cdiv(n, kSecBlock), kSecBlock, 0, s, w, L, n); ++nl; }
         launch_rows_warp(s, w, L, n, prm);
         ++nl;
-        if (x) { k_xpack<<<xg, 256, 0, s>>>(w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
+        if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
         PMARK(BRGPU_K_ROWS);
     } else {
-        if (x) { k_xunpack<<<xu, 256, 0, s>>>(w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
-        k_deflated_out<<<cdiv(n, 256), 256, 0, s>>>(w, L, n);
+        if (x) { launch_pdl(k_xunpack, xu, 256, 0, s, w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
+        launch_pdl(k_deflated_out, cdiv(n, 256), 256, 0, s, w, L, n);
         ++nl;
         PMARK(BRGPU_K_DEFLATED);
     }
-    *launches += nl;
+    *launches += nl + (part == 0 ? 1 : 0);  // + k_level_zero
 }
 
 // Does a split level exchange after `part` (and which arrays: 1 = xA, 2 = xA + xB)?
@@ -1266,21 +1297,21 @@ void launch_level(cudaStream_t s, const Work& w, const LevelDev& L, int n,
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
                         int* launches, Prof* prof) {
     (void)n;
-    k_level_trace<<<cdiv(L.M, 128), 128, 0, s>>>(w, L, out);
+    launch_pdl(k_level_trace, cdiv(L.M, 128), 128, 0, s, w, L, out);
     *launches += 1;
     PMARK(BRGPU_K_TRACE);
 }
 
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
                    const unsigned long long* sbits, double* lam, int* launches, Prof* prof) {
-    k_rescale<<<cdiv(n, 256), 256, 0, s>>>(n, bstart, nblk, sbits, lam);
+    launch_pdl(k_rescale, cdiv(n, 256), 256, 0, s, n, bstart, nblk, sbits, lam);
     *launches += 1;
     PMARK(BRGPU_K_FINISH);
 }
 
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
                        int nruns, int* launches, Prof* prof) {
-    k_merge_runs<<<cdiv(n, 256), 256, 0, s>>>(n, src, dst, rs, nruns);
+    launch_pdl(k_merge_runs, cdiv(n, 256), 256, 0, s, n, src, dst, rs, nruns);
     *launches += 1;
     PMARK(BRGPU_K_FINISH);
 }

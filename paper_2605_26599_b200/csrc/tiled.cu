@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "internal.hpp"
+#include "launch.cuh"
 #include "numerics.cuh"
 
 namespace brgpu {
@@ -31,6 +32,7 @@ __device__ __forceinline__ void tile_load(double2* dst, const double* __restrict
 
 __global__ void __launch_bounds__(kTiledThreads, 2)
 k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
+    pdl_entry();
     __shared__ double2 s_tile[2][kTile2];
     __shared__ double2 s_snap[kTiledThreads];
     __shared__ int s_next;
@@ -163,7 +165,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
 
 void launch_secular_tiled(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                           const SolveParams& prm) {
-    k_secular_tiled<<<prm.sec_grid, kTiledThreads, 0, s>>>(w, L, n, prm.patched, prm.sec_grid);
+    launch_pdl(k_secular_tiled, prm.sec_grid, kTiledThreads, 0, s, w, L, n, prm.patched, prm.sec_grid);
 }
 
 }  // namespace brgpu

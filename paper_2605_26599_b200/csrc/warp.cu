@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "internal.hpp"
+#include "launch.cuh"
 #include "numerics.cuh"
 
 namespace brgpu {
@@ -38,6 +39,7 @@ __device__ __forceinline__ int strided_start(int lo, int ks, int lane) {
 // secular roots, one warp per root
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelDev L, int n, int patched) {
+    pdl_entry();
     __shared__ double2 s_tile[2][kWarpTile];
     __shared__ int s_next;
     if (!L.allSplit && !(*w.levelModes & 2)) return;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
 // refreshed weights, one warp per pole (product over roots, split by lane)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, int n) {
+    pdl_entry();
     __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
 // boundary rows + placement, one warp per root
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
+    pdl_entry();
     __shared__ double s_d[kWarpTile], s_zh[kWarpTile], s_r0[kWarpTile], s_r1[kWarpTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -344,13 +348,13 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
 }
 
 void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    k_secular_warp<<<prm.sec_grid, kWarpThreads, 0, s>>>(w, L, n, prm.patched);
+    launch_pdl(k_secular_warp, prm.sec_grid, kWarpThreads, 0, s, w, L, n, prm.patched);
 }
 void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    k_zhat_warp<<<prm.sec_grid, kWarpThreads, 0, s>>>(w, L, n);
+    launch_pdl(k_zhat_warp, prm.sec_grid, kWarpThreads, 0, s, w, L, n);
 }
 void launch_rows_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    k_rows_warp<<<prm.sec_grid, kWarpThreads, 0, s>>>(w, L, n);
+    launch_pdl(k_rows_warp, prm.sec_grid, kWarpThreads, 0, s, w, L, n);
 }
 
 }  // namespace brgpu
