@@ -583,6 +583,7 @@ SolveParams solve_params(Handle* h, int n) {
     prm.patched = h->patched;
     prm.tol_scale = h->tol_scale;
     prm.sec_grid = h->sec_grid;
+    prm.sms = h->sms;
     return prm;
 }
 

@@ -92,6 +92,7 @@ struct SolveParams {
     int patched;
     double tol_scale;
     int sec_grid;  // CTAs of the secular kernel (fills the GPU; chunks adapt to the root count)
+    int sms;       // SM count (grid sizing of the warp tier)
     // root-range split exchange: results of owned indices are packed into slot
     // own_r (xc entries) of the gather buffers xA/xB, which are all-gathered in place
     int xsplit;

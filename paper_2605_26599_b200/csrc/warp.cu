@@ -347,14 +347,26 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
     }
 }
 
+// Grids of the warp tier (CTAs per SM, times the SM count): the secular kernel
+// takes chunks of roots per CTA, the z-hat / rows kernels stride over roots.
+#ifndef BRGPU_WARP_SEC_PER_SM
+#define BRGPU_WARP_SEC_PER_SM 16
+#endif
+#ifndef BRGPU_WARP_ROW_PER_SM
+#define BRGPU_WARP_ROW_PER_SM 24
+#endif
+constexpr int kWarpSecPerSm = BRGPU_WARP_SEC_PER_SM;
+constexpr int kWarpRowPerSm = BRGPU_WARP_ROW_PER_SM;
+static int warp_grid(const SolveParams& prm, int per_sm) { return prm.sms * per_sm; }
+
 void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    launch_pdl(k_secular_warp, prm.sec_grid, kWarpThreads, 0, s, w, L, n, prm.patched);
+    launch_pdl(k_secular_warp, warp_grid(prm, kWarpSecPerSm), kWarpThreads, 0, s, w, L, n, prm.patched);
 }
 void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    launch_pdl(k_zhat_warp, prm.sec_grid, kWarpThreads, 0, s, w, L, n);
+    launch_pdl(k_zhat_warp, warp_grid(prm, kWarpRowPerSm), kWarpThreads, 0, s, w, L, n);
 }
 void launch_rows_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    launch_pdl(k_rows_warp, prm.sec_grid, kWarpThreads, 0, s, w, L, n);
+    launch_pdl(k_rows_warp, warp_grid(prm, kWarpRowPerSm), kWarpThreads, 0, s, w, L, n);
 }
 
 }  // namespace brgpu
