@@ -238,6 +238,7 @@ __global__ void k_cuts(int ncut, const int* __restrict__ cutPos, const double* _
 // sweeps are a serial chain of dependent loads/stores, so they must hit SMEM
 // latency, not L1-thrashing local memory (4 x MAXM doubles per thread).
 constexpr int kLeafThreads = 64;
+constexpr int kLeafSpreadWarps = 148 * 4;  // warps to spread a small leaf set over
 // per-thread SMEM doubles: d[MAXM], e[MAXM-1] (e[m-1] is never read), r0, r1.
 // At MAXM = 16 this is 63 doubles = 32256 B per 64-thread CTA, so 7 CTAs fit in
 // one SM (7 x (32256 + 1024 reserved) <= 233472 B) and the 65536 leaves of an
@@ -254,10 +255,15 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __r
                                                        double* __restrict__ lam,
                                                        double* __restrict__ blo,
                                                        double* __restrict__ bhi,
-                                                       int* __restrict__ status) {
+                                                       int* __restrict__ status, int per_warp) {
     pdl_entry();
     extern __shared__ double leaf_sm[];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    // per_warp leaves per warp (lanes >= per_warp idle): 32 packs the machine
+    // when there are many leaves; fewer shorten the latency of small solves,
+    // where one warp's divergent leaves would otherwise run back to back
+    const int lane = threadIdx.x & 31;
+    if (lane >= per_warp) return;
+    const int t = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * per_warp + lane;
     if (t >= ntask) return;
     const int off = tOff[t], m = tSize[t];
     const bool values_only = tFlags[t] & 1;
@@ -1151,19 +1157,23 @@ void launch_prepare(cudaStream_t s, int n, const int* bstart, int nblk, unsigned
 void launch_leaves(cudaStream_t s, int ntask, int maxm, const int* tOff, const int* tSize,
                    const int* tFlags, const Work& w, int* launches, Prof* prof) {
     if (ntask <= 0) return;
-    const int grid = cdiv(ntask, kLeafThreads);
+    // leaves per warp: fill ~4 warps per SM first, then pack up to 32 per warp
+    int per_warp = 1;
+    while (per_warp < 32 && (long long)ntask > (long long)per_warp * kLeafSpreadWarps) per_warp <<= 1;
+    const int warps = cdiv(ntask, per_warp);
+    const int grid = cdiv(warps * 32, kLeafThreads);
     if (maxm <= 16) {
         const size_t sm = leaf_smem_bytes<16>();
         launch_pdl(k_leaf<16>, grid, kLeafThreads, sm, s, ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
-                                                  w.blo, w.bhi, w.status);
+                                                  w.blo, w.bhi, w.status, per_warp);
     } else if (maxm <= 26) {
         const size_t sm = leaf_smem_bytes<26>();
         launch_pdl(k_leaf<26>, grid, kLeafThreads, sm, s, ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
-                                                  w.blo, w.bhi, w.status);
+                                                  w.blo, w.bhi, w.status, per_warp);
     } else {
         const size_t sm = leaf_smem_bytes<32>();
         launch_pdl(k_leaf<32>, grid, kLeafThreads, sm, s, ntask, tOff, tSize, tFlags, w.dw, w.ew, w.lam,
-                                                  w.blo, w.bhi, w.status);
+                                                  w.blo, w.bhi, w.status, per_warp);
     }
     *launches += 1;
     PMARK(BRGPU_K_LEAF);
