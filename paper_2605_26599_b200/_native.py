@@ -52,6 +52,7 @@ EXPORTS = [
     "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_profile_kernels_batched",
     "brgpu_kernel_class_name", "brgpu_selftest_rcp",
     "brgpu_nccl_unique_id", "brgpu_create_distributed", "brgpu_plan_owned", "brgpu_version",
+    "brgpu_phase_cycles",
 ]
 
 NCLASS = 17

@@ -921,7 +921,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     }
     if (int r = ensure_buf_sizes(h, p)) return r;
     CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
-    CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 4, s));
+    CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 8, s));
     int launches = 0;
     const bool want_graph = h->use_graph != 0 && h->prof == nullptr;
     CUDA_TRY(h, cudaEventRecord(h->tev[2], s));
@@ -1279,6 +1279,14 @@ int brgpu_eigvals_batched(brgpu_handle* hh, int64_t batch, int64_t n, const doub
 int brgpu_get_stats(const brgpu_handle* hh, brgpu_stats* out) {
     if (!hh || !out) return BRGPU_ERR_INVALID_ARGUMENT;
     *out = hh->h.stats;
+    return BRGPU_OK;
+}
+
+int brgpu_phase_cycles(brgpu_handle* hh, uint64_t* out4) {
+    if (!hh || !out4) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (!h->w.counters) { for (int k = 0; k < 4; ++k) out4[k] = 0; return BRGPU_OK; }
+    CUDA_TRY(h, cudaMemcpy(out4, h->w.counters + 4, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost));
     return BRGPU_OK;
 }
 

@@ -139,6 +139,21 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
                                             FuseSmem<kFuseMax, kFuseThreads>& S) {
     const int tid = threadIdx.x;
     const int base = L.mOff[m0];
+#ifdef BRGPU_PHASE_PROF
+    // phase cycle accounting (profiling builds only): deflation / secular /
+    // refreshed weights / rows + placement, summed over CTAs in counters[4..7]
+    long long ph_t = clock64();
+#define PHASE_MARK(k)                                                              \
+    do {                                                                           \
+        if (tid == 0) {                                                            \
+            const long long t_ = clock64();                                        \
+            atomicAdd(&w.counters[4 + (k)], (unsigned long long)(t_ - ph_t));      \
+            ph_t = t_;                                                             \
+        }                                                                          \
+    } while (0)
+#else
+#define PHASE_MARK(k) do {} while (0)
+#endif
 
     // ---- metadata + inputs -------------------------------------------------
     if (tid < cnt) {
@@ -313,6 +328,7 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
     if (tid <= cnt) S.kS[tid] = S.survPre[S.nnPre[tid < cnt ? S.mo[tid] : E]];
     __syncthreads();
 
+    PHASE_MARK(0);
     // ---- secular roots: per-lane RootSM, CTA queue --------------------------
     {
         // per-thread prefix snapshot slot; S.Z is dead between compaction and sDorg
@@ -381,6 +397,7 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
     }
     __syncthreads();
 
+    PHASE_MARK(1);
     // ---- Gu-Eisenstat refreshed weights (non-root merges) --------------------
     if (prm.zhat) {
         for (int g = tid; g < T; g += kFuseThreads) {
@@ -412,6 +429,7 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
         __syncthreads();
     }
 
+    PHASE_MARK(2);
     // ---- roots: boundary rows + placement; deflated columns: placement -------
     for (int g = tid; g < T; g += kFuseThreads) {
         const int t = upper_index(S.kS, cnt, g);
@@ -478,6 +496,11 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
         }
     }
 
+#ifdef BRGPU_PHASE_PROF
+    __syncthreads();
+#endif
+    PHASE_MARK(3);
+#undef PHASE_MARK
     // ---- stats / trace -------------------------------------------------------
     if (traceOut && tid < cnt) {
         traceOut[2 * (m0 + tid)] = S.nnPre[S.mo[tid] + S.ms[tid]] - S.nnPre[S.mo[tid]];
