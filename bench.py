@@ -53,9 +53,16 @@ CONFIGS = {
 # bracket's sign split) = 11; refreshed-weight term 3 DADD + 5 DFMA + 2 DMUL = 10;
 # boundary-row term 2 DADD + 5 DFMA + 1 DMUL + 3 DFMA = 11.
 OPS_PER_TERM = {"secular": 11, "zhat": 10, "rows": 11}
-# algorithmic bytes per element per level of the memory-bound classes
-BYTES_PER_ELEM = {"merge_tol": 16, "merge_scatter": 56, "nn_flag": 9, "nn_write": 5,
-                  "deflated_out": 53, "segment_walk": 0, "surv_count": 1, "surv_write": 0}
+# algorithmic bytes per element per grid-tier level of the memory-bound classes
+# (kernel class names of brgpu_kernel_class_name):
+#   merge_scatter = k_merge_prep: read lam + the z source            16 B
+#   nn_flag       = k_merge_nn: read lam, blo, bhi (24), write D, Z,
+#                   R0, R1 (32), flag (1), prefix (4)                  61 B
+#   deflated_out  : read D, R0, R1 (24), flag + prefix (5), survivor
+#                   flag + prefix (5), write lam, blo, bhi (24)        58 B
+#   surv_write    = k_surv_scan over the NN list (counted per element: 1 B)
+BYTES_PER_ELEM = {"merge_scatter": 16, "nn_flag": 61, "deflated_out": 58, "surv_write": 1,
+                  "segment_walk": 0}
 
 
 def traffic_bytes(config: str, kernel: str):
@@ -334,6 +341,17 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
                 roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hb, "unit": "GB/s",
                         "frac": ach / hb, "traffic": traffic_bytes(args.config, dom), "launches": dom_launch,
                         "avg_launch_ms": dom_ms / dom_launch}
+        # --- memory-bound grid-tier kernels: achieved GB/s on algorithmic bytes
+        hbm = {}
+        if prof:
+            hb = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0) \
+                if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+            glev = prof.get("nn_flag", (0.0, 0))[1]  # one k_merge_nn launch per grid-tier level
+            for k in ("merge_scatter", "nn_flag", "deflated_out"):
+                if k in prof and prof[k][0] > 0 and glev:
+                    gbs = BYTES_PER_ELEM[k] * N * glev / (prof[k][0] * 1e-3) / 1e9
+                    hbm[k] = {"ms": prof[k][0], "levels": glev, "gbs": gbs, "frac_of_hbm": gbs / hb,
+                              "note": "per-level working set is L2-resident at n <= 2^20"}
         # --- CPU baseline: the reference composition on this box's host cores
         import oracle as O
         cores = os.cpu_count() or 1
@@ -361,6 +379,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
                     "d2h_bytes_per_step": 8 * N},
             "roofline": roof,
             "fp64_kernels": fp64 if prof else None,
+            "hbm_kernels": hbm if prof else None,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches * args.steps,
