@@ -71,6 +71,8 @@ def bro() -> C.CDLL:
         lib.bro_refreshed_weights.argtypes = [C.c_int, _dp, _dp, _ip, _dp, C.c_int, _dp]
         lib.bro_sturm_count.argtypes = [C.c_int64, _dp, _dp, C.c_double]
         lib.bro_sturm_count.restype = C.c_int64
+        lib.bro_set_merge_dump.argtypes = [_dp, C.c_int64]
+        lib.bro_merge_dump_used.restype = C.c_int64
         _bro = lib
     return _bro
 
@@ -301,3 +303,29 @@ def tolerance(d, e) -> float:
         row[:-1] += e
         row[1:] += e
     return 8.0 * len(d) * 2.0 ** -52 * float(row.max())
+
+
+def merge_inputs(d, e, **kw) -> list[tuple[int, int, int, np.ndarray, np.ndarray]]:
+    """Per merge (offset, size, n_left, D, z): the merged child eigenvalues and
+    z = (sign*bhi_L, blo_R) that each BR merge hands to deflation (Theorem 1
+    check; single-threaded so the records come in tree order per level)."""
+    d = _f64(d)
+    n = len(d)
+    cap = 64 * n + 1024
+    for _ in range(2):
+        buf = np.zeros(cap)
+        bro().bro_set_merge_dump(_p(buf), cap)
+        try:
+            eigvals(d, e, threads=1, **kw)
+        finally:
+            used = bro().bro_merge_dump_used()
+            bro().bro_set_merge_dump(None, 0)
+        if used <= cap:
+            break
+        cap = used
+    out, at = [], 0
+    while at < used:
+        off, size, nl = int(buf[at]), int(buf[at + 1]), int(buf[at + 2])
+        out.append((off, size, nl, buf[at + 3:at + 3 + size].copy(), buf[at + 3 + size:at + 3 + 2 * size].copy()))
+        at += 3 + 2 * size
+    return out

@@ -884,6 +884,12 @@ typedef struct {
 
 /* lam/blo/bhi hold both children at [off, off+size); replaced by the parent.
  * par != 0 allows OpenMP inside the merge. */
+/* Merge-input dump for the Theorem 1 test (test infrastructure): records
+ * (offset, size, n_left, D[size], z[size]) per merge while buf is set. */
+static struct { double* buf; int64_t cap, used; } g_dump;
+void bro_set_merge_dump(double* buf, int64_t cap) { g_dump.buf = buf; g_dump.cap = cap; g_dump.used = 0; }
+int64_t bro_merge_dump_used(void) { return g_dump.used; }
+
 static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, int64_t size,
                             double rho, int sign, int is_root, const bro_opts* o, int par) {
     merge_out mo;
@@ -930,6 +936,18 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
                 R1[k] = bhi[p];
                 ++b;
             }
+        }
+    }
+    /* test hook (Theorem 1 check): merged poles and z of every merge, before deflation */
+    if (g_dump.buf) {
+        int64_t at;
+#pragma omp atomic capture
+        { at = g_dump.used; g_dump.used += 3 + 2 * (int64_t)n; }
+        if (at + 3 + 2 * (int64_t)n <= g_dump.cap) {
+            double* q = g_dump.buf + at;
+            q[0] = (double)off; q[1] = (double)n; q[2] = (double)nL;
+            memcpy(q + 3, D, sizeof(double) * (size_t)n);
+            memcpy(q + 3 + n, Z, sizeof(double) * (size_t)n);
         }
     }
     defl_info info;

@@ -116,6 +116,12 @@ int bro_deflate(int n, const double* d, const double* z, double tol_scale, int r
 int bro_refreshed_weights(int k, const double* d, const double* z, const int* origin,
                           const double* tau, int ref_arith, double* zhat);
 
+/* Test hook: record (offset, size, n_left, D[size], z[size]) of every merge --
+ * merged child eigenvalues and z = (sign*bhi_L, blo_R) before deflation -- into
+ * buf (doubles); NULL disables.  bro_merge_dump_used: doubles written/needed. */
+void bro_set_merge_dump(double* buf, int64_t cap);
+int64_t bro_merge_dump_used(void);
+
 /* Sturm count: number of eigenvalues of T strictly less than x. */
 int64_t bro_sturm_count(int64_t n, const double* d, const double* e, double x);
 
