@@ -242,6 +242,25 @@ class Solver:
             self._fail(rc)
         return w
 
+    def eigvals_dense_device(self, A, w=None, stream: int | None = None):
+        """Dense symmetric torch.cuda float64 matrix (n x n, lower triangle used, OVERWRITTEN):
+        cuSOLVER dsytrd to tridiagonal, then the BR solve (the paper's "reduced dense"
+        family).  Returns ascending eigenvalues."""
+        import torch
+        if A.dtype != torch.float64 or not A.is_cuda or A.dim() != 2 or A.shape[0] != A.shape[1]:
+            raise InvalidArgument("eigvals_dense_device: square cuda float64 matrix required")
+        n = A.shape[0]
+        if not A.is_contiguous():
+            raise InvalidArgument("eigvals_dense_device: contiguous matrix required")
+        if w is None:
+            w = torch.empty(n, dtype=torch.float64, device=A.device)
+        s = stream if stream is not None else torch.cuda.current_stream(A.device).cuda_stream
+        # row-major contiguous storage of a symmetric matrix == its column-major storage
+        rc = self._lib.brgpu_eigvals_dense_device(self._h, n, A.data_ptr(), n, w.data_ptr(), s)
+        if rc:
+            self._fail(rc)
+        return w
+
     def eigvals_batched(self, d, e) -> np.ndarray:
         """d (batch, n), e (batch, n-1) host arrays -> (batch, n) ascending per matrix."""
         d = np.ascontiguousarray(d, dtype=np.float64)

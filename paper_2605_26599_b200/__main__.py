@@ -4,8 +4,9 @@
     python -m paper_2605_26599_b200 --family file --input T.txt --out lam.txt
 
 Families: the paper's uniform / normal / toeplitz (d=2, e=0.25) / clustered (SPEC.md:562,
-PAPER.md:1916) plus BASELINE's sym-uniform / toeplitz121 / wilkinson, and `file` (the
-reference's text format, src/tridiagonal.cpp:60-91).  The solver is this repository's
+PAPER.md:1916) plus BASELINE's sym-uniform / toeplitz121 / wilkinson, `reduced` (a dense
+symmetric Gaussian matrix reduced on the GPU by cuSOLVER dsytrd, the paper's reduced-dense
+family) and `file` (the reference's text format, src/tridiagonal.cpp:60-91).  The solver is this repository's
 sm_100a BR solver (`--solver br`); the SPEC's `qrql` / `reference` CPU solvers are not part of
 the product and are refused.  Accuracy: e_fwd = |lam - lam_ref|_inf /
 max(1, |lam_ref|_inf), e_bwd = |lam - lam_ref|_inf / max(1, |T|_inf) against LAPACK
@@ -64,7 +65,7 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2605_26599_b200", description=__doc__.split("\n")[0])
     ap.add_argument("--family", default="uniform",
                     choices=["uniform", "normal", "toeplitz", "clustered", "sym-uniform", "toeplitz121",
-                             "wilkinson", "file"])
+                             "wilkinson", "reduced", "file"])
     ap.add_argument("--n", type=int, nargs="+", default=[4096])
     ap.add_argument("--solver", default="br", choices=["br", "qrql", "reference"])
     ap.add_argument("--threads", type=int, default=1, help="recorded only (one GPU)")
@@ -91,25 +92,48 @@ def main(argv=None) -> int:
         for n in sizes:
             rec = dict(family=a.family, n=n, solver="br", threads=a.threads)
             try:
+                A = None
                 if a.family == "file":
                     T = read_tridiagonal(a.input)
                     d, e = T.d, T.e
+                elif a.family == "reduced":  # dense symmetric -> cuSOLVER dsytrd -> BR
+                    import torch
+                    M = np.random.default_rng(G.seed_for("normal", n)).standard_normal((n, n))
+                    A = (M + M.T) / 2
+                    d = np.zeros(n)
+                    e = np.zeros(n - 1)
                 else:
                     d, e = G.generate(a.family, n)
                 rec["n"] = len(d)
                 R = a.repeat or (5 if len(d) <= 8192 else 1)
                 best, lam = math.inf, None
+                def run_once():
+                    if A is None:
+                        return s.eigvals(d, e)
+                    At = torch.tensor(A, device=f"cuda:{a.device}")  # overwritten by the reduction
+                    torch.cuda.synchronize()
+                    t = time.perf_counter()
+                    out = s.eigvals_dense_device(At).cpu().numpy()
+                    return out, time.perf_counter() - t
+
                 for _ in range(a.warmup):
-                    s.eigvals(d, e)
+                    run_once()
                 if a.trace_merges:
                     s.set_trace(True)
                 for _ in range(R):
                     t0 = time.perf_counter()
-                    lam = s.eigvals(d, e)
-                    best = min(best, time.perf_counter() - t0)
+                    lam = run_once()
+                    dt = time.perf_counter() - t0
+                    if A is not None:
+                        lam, dt = lam  # reduction + solve, excluding the host-to-device copy of A
+                    best = min(best, dt)
                 led = s.ledger()
-                ref, kind = reference_spectrum(a.reference, a.family, d, e)
-                tn = float(np.max(np.abs(d) + np.r_[np.abs(e), 0] + np.r_[0, np.abs(e)]))
+                if A is not None:
+                    ref = np.linalg.eigvalsh(A) if (a.reference != "none" and n <= 8192) else None
+                    tn = float(np.max(np.sum(np.abs(A), axis=1)))
+                else:
+                    ref, kind = reference_spectrum(a.reference, a.family, d, e)
+                    tn = float(np.max(np.abs(d) + np.r_[np.abs(e), 0] + np.r_[0, np.abs(e)]))
                 ef, eb = accuracy(lam, ref, tn) if ref is not None else (None, None)
                 rec.update(time_ms=best * 1e3, e_fwd=ef, e_bwd=eb, ws_doubles_peak=led.peak_doubles,
                            ws_ints_peak=led.peak_ints, checksum_sum=float(np.sum(lam)),

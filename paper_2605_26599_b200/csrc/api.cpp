@@ -1228,6 +1228,84 @@ int brgpu_eigvals_device(brgpu_handle* hh, int64_t n, const double* d, const dou
     return solve_device(h, n, d, e, w, false);
 }
 
+// ---------------------------------------------------------------------------
+// Upstream neighbour ("reduced dense"):
+// dense symmetric -> tridiagonal by cuSOLVER dsytrd (library call, dlopen'ed so
+// the product has no link-time dependency), then the BR solve.
+// ---------------------------------------------------------------------------
+struct CusolverApi {
+    bool ok = false;
+    using H = void*;
+    int (*Create)(H*) = nullptr;
+    int (*Destroy)(H) = nullptr;
+    int (*SetStream)(H, cudaStream_t) = nullptr;
+    int (*BufSize)(H, int, int, const double*, int, const double*, const double*, const double*, int*) = nullptr;
+    int (*Sytrd)(H, int, int, double*, int, double*, double*, double*, double*, int, int*) = nullptr;
+};
+
+CusolverApi& cusolver_api() {
+    static CusolverApi api = [] {
+        CusolverApi a;
+        void* lib = dlopen("libcusolver.so.11", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libcusolver.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) return a;
+        a.Create = (decltype(a.Create))dlsym(lib, "cusolverDnCreate");
+        a.Destroy = (decltype(a.Destroy))dlsym(lib, "cusolverDnDestroy");
+        a.SetStream = (decltype(a.SetStream))dlsym(lib, "cusolverDnSetStream");
+        a.BufSize = (decltype(a.BufSize))dlsym(lib, "cusolverDnDsytrd_bufferSize");
+        a.Sytrd = (decltype(a.Sytrd))dlsym(lib, "cusolverDnDsytrd");
+        a.ok = a.Create && a.Destroy && a.SetStream && a.BufSize && a.Sytrd;
+        return a;
+    }();
+    return api;
+}
+
+int brgpu_eigvals_dense_device(brgpu_handle* hh, int64_t n64, double* A, int64_t lda, double* w, void* stream) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (n64 <= 0 || n64 >= (int64_t)1 << 31 || !A || !w || lda < n64)
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "dense: order must be positive and lda >= n");
+    CusolverApi& C = cusolver_api();
+    if (!C.ok) return fail(h, BRGPU_ERR_CUDA, "dense: libcusolver not available");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    const int n = (int)n64;
+    cudaStream_t user = (cudaStream_t)stream;
+    if (user) {
+        cudaEvent_t ev = nullptr;
+        CUDA_TRY(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaEventRecord(ev, user));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    void* sh = nullptr;
+    if (C.Create(&sh) != 0) return fail(h, BRGPU_ERR_CUDA, "dense: cusolverDnCreate failed");
+    C.SetStream(sh, h->stream);
+    double *buf = nullptr;
+    int* info = nullptr;
+    int lwork = 0;
+    constexpr int kLower = 0;  // CUBLAS_FILL_MODE_LOWER
+    int rc = BRGPU_OK;
+    if (C.BufSize(sh, kLower, n, A, (int)lda, nullptr, nullptr, nullptr, &lwork) != 0) {
+        rc = fail(h, BRGPU_ERR_CUDA, "dense: dsytrd_bufferSize failed");
+    } else if (cudaMalloc(&buf, sizeof(double) * ((size_t)3 * n + (size_t)lwork)) != cudaSuccess ||
+               cudaMalloc(&info, sizeof(int)) != cudaSuccess) {
+        rc = fail(h, BRGPU_ERR_CUDA, "dense: workspace allocation failed");
+    } else {
+        double* d = buf;
+        double* e = buf + n;
+        double* tau = buf + 2 * (size_t)n;
+        double* work = buf + 3 * (size_t)n;
+        if (C.Sytrd(sh, kLower, n, A, (int)lda, d, e, tau, work, lwork, info) != 0)
+            rc = fail(h, BRGPU_ERR_CUDA, "dense: dsytrd failed");
+        else
+            rc = solve_device(h, n, d, e, w, false);  // synchronises the handle stream
+    }
+    cudaFree(buf);
+    cudaFree(info);
+    C.Destroy(sh);
+    return rc;
+}
+
 int brgpu_eigvals_batched_device(brgpu_handle* hh, int64_t batch, int64_t n, const double* d,
                                  const double* e, double* w, void* stream) {
     if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;

@@ -92,3 +92,12 @@ def test_cli_records(tmp_path):
     rows = r.stdout.strip().splitlines()
     assert rows[0].split(",")[:3] == ["family", "n", "solver"] and len(rows) == 3
     assert all(float(x.split(",")[5]) <= 1e-12 for x in rows[1:])  # e_fwd vs analytic
+
+
+@pytest.mark.gpu
+def test_cli_reduced_dense():
+    r = subprocess.run([sys.executable, "-m", "paper_2605_26599_b200", "--family", "reduced", "--n", "500"],
+                       cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rec = json.loads(r.stdout.strip().splitlines()[-1])
+    assert rec["status"] == "ok" and rec["e_bwd"] <= 1e-12
