@@ -69,6 +69,8 @@ def bro() -> C.CDLL:
                                        _dp, _ip]
         lib.bro_deflate.argtypes = [C.c_int, _dp, _dp, C.c_double, C.c_int, _dp, _dp, _dp, _ip, _ip, _dp]
         lib.bro_refreshed_weights.argtypes = [C.c_int, _dp, _dp, _ip, _dp, C.c_int, _dp]
+        lib.bro_eigvals_rows.argtypes = [C.c_int64, _dp, _dp, _dp, C.c_int64, C.POINTER(C.c_int64), _dp,
+                                         C.POINTER(BroOpts)]
         lib.bro_sturm_count.argtypes = [C.c_int64, _dp, _dp, C.c_double]
         lib.bro_sturm_count.restype = C.c_int64
         lib.bro_set_merge_dump.argtypes = [_dp, C.c_int64]
@@ -145,6 +147,24 @@ def eigvals(d, e, *, leaf_cutoff=25, zhat=True, patched=True, ref_arith=False, t
             t = tr[i]
             recs.append((t.level, t.is_root, t.offset, t.size, t.nn, t.k))
     return Result(w, stats, recs)
+
+
+def eigvals_rows(d, e, rows, *, leaf_cutoff=25, zhat=True, patched=True, ref_arith=False, threads=0):
+    """Eigenvalues and the requested eigenvector rows (Algorithm 1's sigma,
+    SPEC.md:317-337): returns (w, R) with R[r, j] = Q[rows[r], j], the columns in
+    the order of w.  0-based row indices; duplicates and any order allowed."""
+    d = _f64(d)
+    n = len(d)
+    e = _f64(e) if n > 1 else np.zeros(1)
+    sel = np.ascontiguousarray(rows, dtype=np.int64).reshape(-1)
+    w = np.empty(n)
+    R = np.empty((len(sel), n))
+    o = BroOpts(leaf_cutoff, int(zhat), int(patched), int(ref_arith), int(threads), 1.0)
+    rc = bro().bro_eigvals_rows(n, _p(d), _p(e), _p(w), len(sel),
+                                sel.ctypes.data_as(C.POINTER(C.c_int64)), _p(R), C.byref(o))
+    if rc:
+        raise OracleError(rc)
+    return w, R
 
 
 def eigvals_batched(d, e, batch: int, n: int, **kw) -> np.ndarray:

@@ -670,6 +670,25 @@ static int root_rows(int k, const double* d, const double* zh, const double* r0,
     return BRO_OK;
 }
 
+/* One selected row's entry for root (org, tau): R_parent(i, j) = R_child(i,:) y_j
+ * (Algorithm 1, "(Q_v)_sigma = (Q_L + Q_R)_sigma S_v").
+ * GPU arithmetic: one sequential pass in pole order, fused multiply-adds for
+ * ||y||^2 and the dot product (the non-split root_rows order). */
+static int sigma_root_row(int k, const double* d, const double* zh, const double* x, int org,
+                          double tau, int ref, double* out) {
+    const double dorg = d[org];
+    double nn = 0.0, s = 0.0;
+    for (int i = 0; i < k; ++i) {
+        const double del = (d[i] - dorg) - tau;
+        if (del == 0.0) return BRO_ZERO_DENOMINATOR;
+        const double y = ref ? zh[i] / del : zh[i] * (1.0 / del);
+        if (ref) { nn += y * y; s += x[i] * y; }
+        else { nn = fma(y, y, nn); s = fma(x[i], y, s); }
+    }
+    *out = ref ? s / sqrt(nn) : s * (1.0 / sqrt(nn));
+    return BRO_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* deflation: deflate.cpp:43-107 (walk) + 109-140 (row replay, fused)         */
 /* ------------------------------------------------------------------------- */
@@ -702,7 +721,8 @@ static void group_member(double Qp, double S0p, double S1p, double zk, double* x
  * act[K]: sorted positions of survivors.  defl[n-K]: sorted positions of the
  * deflated poles in walk order.  R0/R1 may be NULL (root-only merge). */
 static void deflate_walk(int n, const double* D, double* Z, double* R0, double* R1, double tol,
-                         int ref, int* act, int* defl, defl_info* info) {
+                         int ref, int* act, int* defl, defl_info* info, int nx, double* X, double* SX) {
+    /* X: nx extra selected rows (stride n, merged order), SX: nx group sums */
     int prev = -1, K = 0, nd = 0, nn = 0, nrot = 0;
     /* GPU arithmetic: running group sums of the current survivor */
     int L = 0;
@@ -714,6 +734,8 @@ static void deflate_walk(int n, const double* D, double* Z, double* R0, double* 
             Z[prev] = R_;                                          \
             if (R0) R0[prev] = S0 * iR_;                           \
             if (R1) R1[prev] = S1 * iR_;                           \
+            for (int x_ = 0; x_ < nx; ++x_)                        \
+                X[(int64_t)x_ * n + prev] = SX[x_] * iR_;          \
         }                                                          \
     } while (0)
     for (int k = 0; k < n; ++k) {
@@ -728,10 +750,22 @@ static void deflate_walk(int n, const double* D, double* Z, double* R0, double* 
                 Z[k] = 0.0;
                 if (R0) { double xp = R0[prev], xq = R0[k]; R0[prev] = c * xp + s * xq; R0[k] = c * xq - s * xp; }
                 if (R1) { double xp = R1[prev], xq = R1[k]; R1[prev] = c * xp + s * xq; R1[k] = c * xq - s * xp; }
+                for (int x = 0; x < nx; ++x) {
+                    double* Xr = X + (int64_t)x * n;
+                    double xp = Xr[prev], xq = Xr[k];
+                    Xr[prev] = c * xp + s * xq;
+                    Xr[k] = c * xq - s * xp;
+                }
             } else {
                 const double zk = Z[k];
                 const double x0 = R0 ? R0[k] : 0.0, x1 = R1 ? R1[k] : 0.0;
                 group_member(Q, S0, S1, zk, R0 ? &R0[k] : NULL, R1 ? &R1[k] : NULL);
+                for (int x = 0; x < nx; ++x) {  /* same per-row arithmetic as R0/R1 */
+                    double* Xr = X + (int64_t)x * n;
+                    const double xk = Xr[k];
+                    group_member(Q, SX[x], SX[x], zk, &Xr[k], NULL);
+                    SX[x] = SX[x] + zk * xk;
+                }
                 Q = Q + zk * zk;
                 S0 = S0 + zk * x0;
                 S1 = S1 + zk * x1;
@@ -751,6 +785,7 @@ static void deflate_walk(int n, const double* D, double* Z, double* R0, double* 
             Q = zs * zs;
             S0 = R0 ? zs * R0[k] : 0.0;
             S1 = R1 ? zs * R1[k] : 0.0;
+            for (int x = 0; x < nx; ++x) SX[x] = zs * X[(int64_t)x * n + k];
         }
     }
     GROUP_CLOSE();
@@ -780,7 +815,7 @@ int bro_deflate(int n, const double* d, const double* z, double tol_scale, int r
     }
     for (int k = 0; k < n; ++k) { D[k] = d[perm[k]]; Z[k] = z[perm[k]]; }
     defl_info info;
-    deflate_walk(n, D, Z, NULL, NULL, tol, ref, act, defl, &info);
+    deflate_walk(n, D, Z, NULL, NULL, tol, ref, act, defl, &info, 0, NULL, NULL);
     for (int a = 0; a < info.K; ++a) { d_active[a] = D[act[a]]; z_active[a] = Z[act[a]]; }
     for (int t = 0; t < n - info.K; ++t) deflated[t] = D[defl[t]];
     *k_out = info.K;
@@ -890,8 +925,18 @@ static struct { double* buf; int64_t cap, used; } g_dump;
 void bro_set_merge_dump(double* buf, int64_t cap) { g_dump.buf = buf; g_dump.cap = cap; g_dump.used = 0; }
 int64_t bro_merge_dump_used(void) { return g_dump.used; }
 
+/* Selected rows sigma (global row indices) of the whole solve: S holds, per
+ * requested row r, the row sel[r] of the current node's eigenvector matrix at
+ * that node's positions (stride N), in the node's ascending eigenvalue order. */
+typedef struct {
+    int64_t nsel, N;
+    const int64_t* sel;
+    double* S;
+} sigma_t;
+
 static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, int64_t size,
-                            double rho, int sign, int is_root, const bro_opts* o, int par) {
+                            double rho, int sign, int is_root, const bro_opts* o, int par,
+                            const sigma_t* sg) {
     merge_out mo;
     memset(&mo, 0, sizeof(mo));
     const int n = (int)size, nL = (int)(size / 2), nR = n - nL;
@@ -906,6 +951,22 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
     double *dA = buf + 4 * n, *zA = buf + 5 * n, *r0A = buf + 6 * n, *r1A = buf + 7 * n;
     double *tau = buf + 8 * n, *zh = buf + 9 * n, *outb = buf + 10 * n;
     int *act = ibuf, *defl = ibuf + n, *org = ibuf + 2 * n;
+    /* selected rows inside this node (split_row_request: the
+     * child that holds a row contributes it, the other child's columns are 0) */
+    int nx = 0;
+    int64_t* xr = NULL;
+    double *X = NULL, *XA = NULL, *XO = NULL, *SX = NULL;
+    if (sg && sg->nsel) {
+        xr = (int64_t*)malloc(sizeof(int64_t) * (size_t)sg->nsel);
+        for (int64_t r = 0; r < sg->nsel; ++r)
+            if (sg->sel[r] >= off && sg->sel[r] < off + size) xr[nx++] = r;
+        if (nx) {
+            X = (double*)malloc(sizeof(double) * (size_t)n * (size_t)nx * 3);
+            SX = (double*)malloc(sizeof(double) * (size_t)nx);
+            XA = X + (size_t)n * nx;
+            XO = XA + (size_t)n * nx;
+        }
+    }
 
     /* tol: deflate.cpp:55-60 over D = lam_L ++ lam_R and z = (sign*bhi_L, blo_R) */
     double dmax = 0.0, zmax = 0.0;
@@ -927,6 +988,8 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
                 Z[k] = sign < 0 ? -bhi[p] : bhi[p];
                 R0[k] = blo[p];
                 R1[k] = 0.0;
+                for (int x = 0; x < nx; ++x)
+                    X[(int64_t)x * n + k] = sg->sel[xr[x]] < off + nL ? sg->S[xr[x] * sg->N + p] : 0.0;
                 ++a;
             } else {
                 const int64_t p = off + nL + b;
@@ -934,6 +997,8 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
                 Z[k] = blo[p];
                 R0[k] = 0.0;
                 R1[k] = bhi[p];
+                for (int x = 0; x < nx; ++x)
+                    X[(int64_t)x * n + k] = sg->sel[xr[x]] >= off + nL ? sg->S[xr[x] * sg->N + p] : 0.0;
                 ++b;
             }
         }
@@ -951,7 +1016,7 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
         }
     }
     defl_info info;
-    deflate_walk(n, D, Z, is_root ? NULL : R0, is_root ? NULL : R1, tol, ref, act, defl, &info);
+    deflate_walk(n, D, Z, is_root ? NULL : R0, is_root ? NULL : R1, tol, ref, act, defl, &info, nx, X, SX);
     const int K = info.K;
     mo.K = K; mo.nn = info.nn; mo.nrot = info.nrot;
     if (!ref && K > BRO_SPLIT_MIN_K) split = 1;
@@ -959,6 +1024,7 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
         dA[a] = D[act[a]];
         zA[a] = Z[act[a]];
         if (!is_root) { r0A[a] = R0[act[a]]; r1A[a] = R1[act[a]]; }
+        for (int x = 0; x < nx; ++x) XA[(int64_t)x * n + a] = X[(int64_t)x * n + act[a]];
     }
 
     /* secular roots (secular.cpp:80-241), independent per root */
@@ -1029,6 +1095,14 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
             free(ybuf);
         }
         if (st_all) { mo.status = st_all; goto done; }
+        /* selected rows: R_parent(sigma, j) = R_child(sigma, :) y_j */
+        for (int x = 0; x < nx; ++x)
+            for (int j = 0; j < K; ++j) {
+                int st = sigma_root_row(K, dA, zh, XA + (int64_t)x * n, org[j], tau[j], ref,
+                                        &XO[(int64_t)x * n + j]);
+                if (st) st_all = st;
+            }
+        if (st_all) { mo.status = st_all; goto done; }
     }
 
     /* parent order: stable merge of deflated list (walk order) then roots */
@@ -1046,11 +1120,13 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
             if (take_root) {
                 lam[p] = lr;
                 if (!is_root) { blo[p] = outb[b]; bhi[p] = zA[b]; }
+                for (int x = 0; x < nx; ++x) sg->S[xr[x] * sg->N + p] = XO[(int64_t)x * n + b];
                 ++b;
             } else {
                 const int s = defl[a];
                 lam[p] = D[s];
                 if (!is_root) { blo[p] = R0[s]; bhi[p] = R1[s]; }
+                for (int x = 0; x < nx; ++x) sg->S[xr[x] * sg->N + p] = X[(int64_t)x * n + s];
                 ++a;
             }
         }
@@ -1058,6 +1134,9 @@ static merge_out merge_node(double* lam, double* blo, double* bhi, int64_t off, 
 done:
     free(buf);
     free(ibuf);
+    free(xr);
+    free(X);
+    free(SX);
     return mo;
 }
 
@@ -1075,13 +1154,17 @@ void bro_default_opts(bro_opts* o) {
 
 static int solve_impl(int64_t n, const double* d, const double* e, double* w, const bro_opts* o,
                       bro_stats* st, bro_trace* trace, int64_t trace_cap, int64_t* trace_len,
-                      int allow_par) {
+                      int allow_par, int64_t nsel, const int64_t* sel, double* rows) {
     if (n <= 0 || !d || (!e && n > 1) || !w) return BRO_INVALID_ARGUMENT;
     for (int64_t i = 0; i < n; ++i) if (!isfinite(d[i])) return BRO_INVALID_ARGUMENT;
     for (int64_t i = 0; i + 1 < n; ++i) if (!isfinite(e[i])) return BRO_INVALID_ARGUMENT;
     if (o->leaf_cutoff < 5 || o->leaf_cutoff > 64) return BRO_INVALID_ARGUMENT;
     const int cutoff = o->leaf_cutoff;
     int status = BRO_OK;
+    for (int64_t r = 0; r < nsel; ++r)
+        if (sel[r] < 0 || sel[r] >= n) return BRO_INVALID_ARGUMENT;
+    sigma_t sg = {nsel, n, sel, NULL};
+    int64_t* pos = NULL;
 
     /* irreducible blocks: tridiagonal.cpp:45-58 with tol = u */
     int64_t nblk = 0;
@@ -1095,7 +1178,8 @@ static int solve_impl(int64_t n, const double* d, const double* e, double* w, co
     t.cap = 2 * (n / ((cutoff + 1) / 2) + 1) + 2 * n / 8 + 16;
     t.count = 0;
     t.nodes = (node_t*)malloc(sizeof(node_t) * (size_t)t.cap);
-    if (!bstart || !scale || !dw || !ew || !blo || !bhi || !t.nodes) { status = BRO_OUT_OF_MEMORY; goto out; }
+    if (nsel) sg.S = (double*)calloc((size_t)(nsel * n), sizeof(double));
+    if (!bstart || !scale || !dw || !ew || !blo || !bhi || !t.nodes || (nsel && !sg.S)) { status = BRO_OUT_OF_MEMORY; goto out; }
 
     bstart[nblk++] = 0;
     for (int64_t i = 0; i + 1 < n; ++i)
@@ -1168,6 +1252,28 @@ static int solve_impl(int64_t n, const double* d, const double* e, double* w, co
             memcpy(w + off, lam, sizeof(double) * (size_t)sz);
         }
         (void)nleaf;
+        /* selected rows of the leaves (and of blocks <= cutoff): the leaf QL/QR
+         * tracking row sel-off instead of the boundary rows (inc/qrql.hpp:38-42) */
+        for (int64_t r = 0; r < nsel && !lerr; ++r) {
+            const int64_t i = sel[r];
+            int64_t off = -1, sz = 0;
+            for (int64_t q = 0; q < t.count; ++q)
+                if (t.nodes[q].left < 0 && t.nodes[q].off <= i && i < t.nodes[q].off + t.nodes[q].size) {
+                    off = t.nodes[q].off; sz = t.nodes[q].size;
+                    break;
+                }
+            if (off < 0)
+                for (int64_t b = 0; b < nblk; ++b)
+                    if (bstart[b] <= i && i < bstart[b + 1]) { off = bstart[b]; sz = bstart[b + 1] - off; break; }
+            double lam[64], ee[64], x[64];
+            memcpy(lam, dw + off, sizeof(double) * (size_t)sz);
+            if (sz > 1) memcpy(ee, ew + off, sizeof(double) * (size_t)(sz - 1));
+            for (int64_t k = 0; k < sz; ++k) x[k] = k == i - off ? 1.0 : 0.0;
+            int rr = steqr(sz, lam, ee, x, NULL, o->ref_arith);
+            if (rr) lerr = rr;
+            stable_sort_rows((int)sz, lam, x, NULL);
+            memcpy(sg.S + r * n + off, x, sizeof(double) * (size_t)sz);
+        }
         if (lerr) { status = lerr; goto out; }
     }
 
@@ -1196,10 +1302,11 @@ static int solve_impl(int64_t n, const double* d, const double* e, double* w, co
                 const int64_t m = nd->off + nd->size / 2 - 1;
                 const double rho = fabs(ew[m]);
                 const int sign = ew[m] < 0 ? -1 : 1;
-                const int is_root = (nd->off == bstart[nd->block]) &&
+                /* root-only mode unless rows are requested */
+                const int is_root = !nsel && (nd->off == bstart[nd->block]) &&
                                     (nd->size == bstart[nd->block + 1] - bstart[nd->block]);
                 merge_out mo = merge_node(w, blo, bhi, nd->off, nd->size, rho, sign, is_root, o,
-                                          par_inside);
+                                          par_inside, nsel ? &sg : NULL);
                 if (mo.status) {
 #pragma omp atomic write
                     lerr = mo.status;
@@ -1232,11 +1339,44 @@ static int solve_impl(int64_t n, const double* d, const double* e, double* w, co
     /* rescale, then global ascending (stable) sort across blocks */
     for (int64_t b = 0; b < nblk; ++b)
         for (int64_t i = bstart[b]; i < bstart[b + 1]; ++i) w[i] *= scale[b];
+    if (nsel) {
+        /* selected rows to the global column order: element i of block b goes
+         * to its stable rank #{j: w_j < w_i} + #{j < i: w_j == w_i} (the order
+         * of the stable cross-block sort below); other blocks' columns are 0 */
+        pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+        if (!pos) { status = BRO_OUT_OF_MEMORY; goto out; }
+        for (int64_t i = 0; i < n; ++i) pos[i] = i;
+        if (nblk > 1) {
+            int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)n * 2);
+            if (!idx) { status = BRO_OUT_OF_MEMORY; goto out; }
+            int64_t* tmp = idx + n;
+            for (int64_t i = 0; i < n; ++i) idx[i] = i;
+            for (int64_t wd = 1; wd < n; wd *= 2) {  /* stable merge sort of indices by value */
+                for (int64_t lo = 0; lo < n; lo += 2 * wd) {
+                    int64_t mid = lo + wd < n ? lo + wd : n, hi = lo + 2 * wd < n ? lo + 2 * wd : n;
+                    int64_t a = lo, b = mid, k = lo;
+                    while (a < mid && b < hi) tmp[k++] = (w[idx[b]] < w[idx[a]]) ? idx[b++] : idx[a++];
+                    while (a < mid) tmp[k++] = idx[a++];
+                    while (b < hi) tmp[k++] = idx[b++];
+                }
+                memcpy(idx, tmp, sizeof(int64_t) * (size_t)n);
+            }
+            for (int64_t k = 0; k < n; ++k) pos[idx[k]] = k;
+            free(idx);
+        }
+        memset(rows, 0, sizeof(double) * (size_t)(nsel * n));
+        for (int64_t r = 0; r < nsel; ++r) {
+            int64_t b = 0;
+            while (bstart[b + 1] <= sel[r]) ++b;
+            for (int64_t i = bstart[b]; i < bstart[b + 1]; ++i) rows[r * n + pos[i]] = sg.S[r * n + i];
+        }
+    }
     if (nblk > 1) stable_sort_values(n, w, dw);
     if (st) { st->height = height; st->blocks = (int32_t)nblk; }
 
 out:
     free(bstart); free(scale); free(dw); free(ew); free(blo); free(bhi); free(t.nodes);
+    free(sg.S); free(pos);
     return status;
 }
 
@@ -1248,11 +1388,32 @@ int bro_eigvals(int64_t n, const double* d, const double* e, double* w, const br
 #ifdef _OPENMP
     int saved = omp_get_max_threads();
     if (o->threads > 0) omp_set_num_threads(o->threads);
-    int r = solve_impl(n, d, e, w, o, st, trace, trace_cap, trace_len, o->threads != 1);
+    int r = solve_impl(n, d, e, w, o, st, trace, trace_cap, trace_len, o->threads != 1, 0, NULL, NULL);
     omp_set_num_threads(saved);
     return r;
 #else
-    return solve_impl(n, d, e, w, o, st, trace, trace_cap, trace_len, 0);
+    return solve_impl(n, d, e, w, o, st, trace, trace_cap, trace_len, 0, 0, NULL, NULL);
+#endif
+}
+
+/* Algorithm 1 with requested rows sigma: eigenvalues w
+ * ascending plus rows[r*n + j] = Q(sel[r], j), Q the eigenvector matrix of T
+ * with columns in the order of w (0-based global row indices, duplicates and
+ * any order allowed).  Every merge, the block root included, propagates the
+ * requested rows; with nsel == 0 this is bro_eigvals. */
+int bro_eigvals_rows(int64_t n, const double* d, const double* e, double* w, int64_t nsel,
+                     const int64_t* sel, double* rows, const bro_opts* o) {
+    bro_opts def;
+    if (!o) { bro_default_opts(&def); o = &def; }
+    if (nsel < 0 || (nsel && (!sel || !rows))) return BRO_INVALID_ARGUMENT;
+#ifdef _OPENMP
+    int saved = omp_get_max_threads();
+    if (o->threads > 0) omp_set_num_threads(o->threads);
+    int r = solve_impl(n, d, e, w, o, NULL, NULL, 0, NULL, o->threads != 1, nsel, sel, rows);
+    omp_set_num_threads(saved);
+    return r;
+#else
+    return solve_impl(n, d, e, w, o, NULL, NULL, 0, NULL, 0, nsel, sel, rows);
 #endif
 }
 
@@ -1272,7 +1433,7 @@ int bro_eigvals_batched(int64_t batch, int64_t n, const double* d, const double*
         bro_stats s1;
         memset(&s1, 0, sizeof(s1));
         int r = solve_impl(n, d + b * n, e + b * (n - 1), w + b * n, o, st ? &s1 : NULL, NULL, 0,
-                           NULL, 0);
+                           NULL, 0, 0, NULL, NULL);
         if (r) {
 #pragma omp atomic write
             status = r;

@@ -95,6 +95,10 @@ int bro_eigvals_batched(int64_t batch, int64_t n, const double* d, const double*
                         double* w, const bro_opts* o, bro_stats* st);
 
 /* Values-only implicit QL/QR (the eigenvalues_qrql shape), ascending. */
+/* Selected rows (Algorithm 1's sigma): rows is nsel x n, rows[r*n+j] = Q(sel[r], j). */
+int bro_eigvals_rows(int64_t n, const double* d, const double* e, double* w, int64_t nsel,
+                     const int64_t* sel, double* rows, const bro_opts* o);
+
 int bro_qrql_values(int64_t n, const double* d, const double* e, double* w, int ref_arith);
 
 /* Leaf solve: eigenvalues ascending plus first/last eigenvector rows. */

@@ -26,7 +26,8 @@ __all__ = [
     "Error", "InvalidArgument", "NoConvergence", "BudgetExceeded", "PoleHit", "ZeroDenominator",
     "MalformedCompactRoot", "DimensionMismatch", "DomainError", "DeviceError",
     "TridiagonalMatrix", "Block", "find_irreducible_blocks", "Solver", "BrOptions", "BrResult",
-    "LedgerSnapshot", "eigenvalues", "br_eigenvalues", "workspace_query",
+    "LedgerSnapshot", "eigenvalues", "br_eigenvalues", "workspace_query", "RowRequest",
+    "split_row_request",
 ]
 
 
@@ -154,6 +155,33 @@ class BrResult:
     lam: np.ndarray
     ledger: LedgerSnapshot
     stats: dict = field(default_factory=dict)
+    selected_rows: np.ndarray | None = None  # |sigma| x n: Q[sigma_r, j], columns in lam's order
+
+
+# ------------------------------------------------- row requests (Algorithm 1)
+@dataclass(frozen=True)
+class RowRequest:
+    """Ordered local row indices sigma (1-based as in SPEC.md; duplicates allowed)."""
+    sigma: tuple[int, ...] = ()
+
+    def validate(self, size: int) -> None:
+        if any(i < 1 or i > size for i in self.sigma):
+            raise InvalidArgument("RowRequest: index outside the node")
+
+
+def split_row_request(sigma, n_left: int, size: int | None = None):
+    """SPEC.md:327-333 (Algorithm 1, "Map sigma_v and split-boundary requests"):
+    sigma_L = the entries <= n_left (order kept) plus the left split-boundary row
+    n_left; sigma_R = the entries > n_left shifted by -n_left (order kept) plus the
+    right boundary row 1.  Returns (sigma_L, sigma_R) as RowRequests, the boundary
+    row last.  The GPU solver realises this mapping positionally (a requested row
+    lives in exactly one child; the other child's columns are zero, sigma.cu)."""
+    sig = tuple(int(i) for i in (sigma.sigma if isinstance(sigma, RowRequest) else sigma))
+    if size is not None:
+        RowRequest(sig).validate(size)
+    left = tuple(i for i in sig if i <= n_left) + (n_left,)
+    right = tuple(i - n_left for i in sig if i > n_left) + (1,)
+    return RowRequest(left), RowRequest(right)
 
 
 def workspace_query(n: int) -> tuple[int, int]:
@@ -223,6 +251,27 @@ class Solver:
         if rc:
             self._fail(rc)
         return w
+
+    def eigvals_rows(self, d, e, rows) -> tuple[np.ndarray, np.ndarray]:
+        """Eigenvalues and requested eigenvector rows (Algorithm 1's sigma): returns
+        (w, R), R[r, j] = Q[rows[r], j] with column j belonging to w[j].  0-based
+        row indices, duplicates and any order allowed (brgpu_eigvals_rows)."""
+        d = np.ascontiguousarray(d, dtype=np.float64).reshape(-1)
+        n = len(d)
+        e = np.ascontiguousarray(e if e is not None else np.zeros(0), dtype=np.float64).reshape(-1)
+        if n == 0:
+            raise InvalidArgument("tridiagonal: order must be positive")
+        if len(e) + 1 != n:
+            raise InvalidArgument("tridiagonal: off-diagonal length != n-1")
+        sel = np.ascontiguousarray(rows, dtype=np.int64).reshape(-1)
+        w = np.empty(n)
+        R = np.empty((len(sel), n))
+        rc = self._lib.brgpu_eigvals_rows(self._h, n, d.ctypes.data, e.ctypes.data if n > 1 else None,
+                                          len(sel), sel.ctypes.data if len(sel) else None, w.ctypes.data,
+                                          R.ctypes.data if len(sel) else None)
+        if rc:
+            self._fail(rc)
+        return w, R
 
     def eigvals_device(self, d, e, w=None, stream: int | None = None):
         """torch.cuda float64 tensors in (resident in HBM), ascending eigenvalues in ``w``."""
@@ -413,11 +462,17 @@ def eigenvalues(T: TridiagonalMatrix) -> np.ndarray:
     return _solver().eigvals(T.d, T.e)
 
 
-def br_eigenvalues(T: TridiagonalMatrix, options: BrOptions | None = None) -> BrResult:
-    """BR eigenvalues plus the workspace ledger snapshot."""
+def br_eigenvalues(T: TridiagonalMatrix, options: BrOptions | None = None,
+                   sigma: RowRequest | None = None) -> BrResult:
+    """BR eigenvalues plus the workspace ledger snapshot, and
+    the requested rows Q[sigma, :] when ``sigma`` (1-based RowRequest) is given."""
     T.validate()
     s = _solver()
     if options is not None:
         s.set_options(options)
+    if sigma is not None and len(sigma.sigma):
+        sigma.validate(T.n)
+        lam, rows = s.eigvals_rows(T.d, T.e, np.asarray(sigma.sigma, dtype=np.int64) - 1)
+        return BrResult(lam, s.ledger(), s.stats(), rows)
     lam = s.eigvals(T.d, T.e)
     return BrResult(lam, s.ledger(), s.stats())

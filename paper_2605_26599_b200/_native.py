@@ -52,7 +52,7 @@ EXPORTS = [
     "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_profile_kernels_batched",
     "brgpu_kernel_class_name", "brgpu_selftest_rcp",
     "brgpu_nccl_unique_id", "brgpu_create_distributed", "brgpu_plan_owned", "brgpu_version",
-    "brgpu_phase_cycles", "brgpu_eigvals_dense_device",
+    "brgpu_phase_cycles", "brgpu_eigvals_dense_device", "brgpu_eigvals_rows",
 ]
 
 NCLASS = 17
@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
     L.brgpu_get_ledger.argtypes = [hp, C.POINTER(Ledger)]
     L.brgpu_eigvals.argtypes = [hp, C.c_int64, _dp, _dp, _dp]
     L.brgpu_eigvals_device.argtypes = [hp, C.c_int64, _dp, _dp, _dp, C.c_void_p]
+    L.brgpu_eigvals_rows.argtypes = [hp, C.c_int64, _dp, _dp, C.c_int64, C.c_void_p, _dp, _dp]
     L.brgpu_eigvals_batched.argtypes = [hp, C.c_int64, C.c_int64, _dp, _dp, _dp]
     L.brgpu_eigvals_dense_device.argtypes = [hp, C.c_int64, _dp, C.c_int64, _dp, C.c_void_p]
     L.brgpu_phase_cycles.argtypes = [hp, C.c_void_p]

@@ -62,6 +62,11 @@ constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (nu
 constexpr int kFuseMaxMergesHost = 128;
 
 void init_kernel_attributes();
+void init_sigma_attributes();
+void launch_sigma_leaves(cudaStream_t s, const SigmaDev& sg, int maxm, const int* taskOf, const int* tOff,
+                         const int* tSize, const Work& w, int* launches);
+void launch_sigma_final(cudaStream_t s, const SigmaDev& sg, const double* lam, const int* bstart, int nblk,
+                        const int* blkOf, int maxBlock, double* out, int n, int* launches);
 int sec_ctas_per_sm();
 int selftest_rcp(long long count, unsigned long long seed, unsigned long long* host_bad);
 
@@ -95,6 +100,7 @@ struct LevelHost {
     int g0, G;   // groups of the fused launch
     int cap;     // group capacity (elements): 512 (small shape) or 1024
     int minSize; // smallest merge of the level
+    int maxSize; // largest merge of the level
 };
 
 struct Plan {
@@ -123,6 +129,7 @@ struct Plan {
     int height = 0;
     int maxM = 0;
     int maxLeaf = 0;
+    bool sigma = false;  // requested-rows plan: grid tier everywhere, no root-only merges
     // device copies
     int* dev = nullptr;  // one int buffer
     size_t devInts = 0;
@@ -185,6 +192,16 @@ struct Handle {
     int root_split = 1;  // split the roots of shared top merges across ranks (BRGPU_OPT_ROOT_SPLIT)
     int xerr = 0;        // first exchange error of the current solve (run_plan returns it)
     std::vector<std::unique_ptr<Handle>> subs;
+    // requested eigenvector rows of the current solve (brgpu_eigvals_rows), or null
+    struct SigmaRun {
+        SigmaDev dev{};
+        std::vector<int> sel;  // host copy of the request
+        int* dTask = nullptr;  // leaf task per request
+        int* dBlk = nullptr;   // block per request
+        int maxBlock = 0;
+        double* out = nullptr; // nsel x n, global column order
+    };
+    SigmaRun* sig = nullptr;
 };
 
 int fail(Handle* h, int code, const std::string& msg) {
@@ -267,6 +284,7 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
             minSize = std::min(minSize, p->mSize[L.m0 + q]);
         }
         L.minSize = minSize;
+        L.maxSize = maxSize;
         L.fused = fuse && maxSize <= kFuseMaxElems;
         L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
@@ -573,6 +591,7 @@ LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh) {
     L.tileFirst = p->d_tileFirst + lh.tile0;
     L.M = lh.M;
     L.allSplit = lh.minSize > kSplitMinSizeHost ? 1 : 0;
+    L.maxSize = lh.maxSize;
     return L;
 }
 
@@ -584,6 +603,7 @@ SolveParams solve_params(Handle* h, int n) {
     prm.tol_scale = h->tol_scale;
     prm.sec_grid = h->sec_grid;
     prm.sms = h->sms;
+    prm.sigma = h->sig ? &h->sig->dev : nullptr;
     return prm;
 }
 
@@ -663,6 +683,8 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
                    p->d_cut, launches, prof);
     launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
                   launches, prof);
+    if (h->sig)
+        launch_sigma_leaves(s, h->sig->dev, p->maxLeaf, h->sig->dTask, p->d_tOff, p->d_tSize, h->w, launches);
     run_levels(h, p, p->levels, launches, prof);
 }
 
@@ -683,6 +705,9 @@ void finish_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
     launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
+    if (h->sig)
+        launch_sigma_final(s, h->sig->dev, h->w.lam, p->d_bstart, nblk, h->sig->dBlk, h->sig->maxBlock,
+                           h->sig->out, n, launches);
     double* src = h->w.lam;
     double* dst = h->w.D;
     for (size_t q = 0; q < p->runPasses.size(); ++q) {
@@ -912,18 +937,43 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     }
     if (h->virt > 1) return solve_virtual(h, n, bstart, segs);
     Plan* p = h->plan.get();
-    if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs) {
+    const bool sig = h->sig != nullptr;
+    if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs ||
+        p->sigma != sig) {
         if (h->plan) free_plan(h->plan.get());
-        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, h->nranks, h->rank);
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0, h->nranks, h->rank);
         p = h->plan.get();
+        if (sig) {  // every merge propagates the requested rows: no root-only mode
+            p->sigma = true;
+            for (int& f : p->mFlags) f &= ~kMergeRoot;
+        }
         int r = upload_plan(h, p);
         if (r) return r;
+    }
+    if (sig) {  // leaf task and block of every requested row
+        Handle::SigmaRun& sr = *h->sig;
+        const int ns = (int)sr.sel.size();
+        std::vector<int> task((size_t)ns, -1), blk((size_t)ns, 0);
+        std::vector<int> byOff((size_t)p->tOff.size());
+        for (size_t t = 0; t < byOff.size(); ++t) byOff[t] = (int)t;
+        std::sort(byOff.begin(), byOff.end(), [&](int a, int b) { return p->tOff[a] < p->tOff[b]; });
+        sr.maxBlock = 0;
+        for (size_t b = 0; b + 1 < bstart.size(); ++b) sr.maxBlock = std::max(sr.maxBlock, bstart[b + 1] - bstart[b]);
+        for (int r = 0; r < ns; ++r) {
+            const int i = sr.sel[(size_t)r];
+            auto it = std::upper_bound(byOff.begin(), byOff.end(), i,
+                                       [&](int v, int t) { return v < p->tOff[t]; });
+            task[(size_t)r] = *(it - 1);
+            blk[(size_t)r] = (int)(std::upper_bound(bstart.begin(), bstart.end(), i) - bstart.begin()) - 1;
+        }
+        CUDA_TRY(h, cudaMemcpy(sr.dTask, task.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+        CUDA_TRY(h, cudaMemcpy(sr.dBlk, blk.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
     }
     if (int r = ensure_buf_sizes(h, p)) return r;
     CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 8, s));
     int launches = 0;
-    const bool want_graph = h->use_graph != 0 && h->prof == nullptr;
+    const bool want_graph = h->use_graph != 0 && h->prof == nullptr && !sig;
     CUDA_TRY(h, cudaEventRecord(h->tev[2], s));
     if (want_graph) {
         if (!p->graph || p->graph_trace != (h->trace != 0) || p->graph_gen != h->bufgen) {
@@ -1088,6 +1138,7 @@ int brgpu_create(brgpu_handle** out, int device) {
     }
     brgpu::init_kernel_attributes();
     brgpu::init_fused_attributes();
+    brgpu::init_sigma_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
     *out = hh;
@@ -1226,6 +1277,68 @@ int brgpu_eigvals_device(brgpu_handle* hh, int64_t n, const double* d, const dou
         cudaEventDestroy(ev);
     }
     return solve_device(h, n, d, e, w, false);
+}
+
+// Eigenvalues plus requested eigenvector rows (Algorithm 1's sigma,
+// SPEC.md:317-337): rows[r*n + j] = Q(sel[r], j), columns in the order of w.
+// The solve runs every level through the grid tier with the sigma kernels
+// (sigma.cu) attached, outside the cached eigenvalue-only graph.
+int brgpu_eigvals_rows(brgpu_handle* hh, int64_t n, const double* d, const double* e, int64_t nsel,
+                       const int64_t* sel, double* w, double* rows) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (n <= 0 || n >= ((int64_t)1 << 31) || !d || !w || (n > 1 && !e))
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be positive (and < 2^31)");
+    if (nsel < 0 || (nsel > 0 && (!sel || !rows)))
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "selected rows: negative count or null pointers");
+    for (int64_t r = 0; r < nsel; ++r)
+        if (sel[r] < 0 || sel[r] >= n)
+            return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "selected rows: row index " + std::to_string(sel[r]) +
+                                                           " outside [0, " + std::to_string(n) + ")");
+    if (nsel == 0) return brgpu_eigvals(hh, n, d, e, w);
+    if (h->nranks > 1 || h->virt > 1)
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "selected rows: single-device handles only");
+    if (nsel > ((int64_t)1 << 30) / std::max<int64_t>(n, 1))
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "selected rows: nsel * n too large");
+    CUDA_TRY(h, cudaSetDevice(h->device));
+    if (int r = ensure_work(h, n)) return r;
+    const int64_t c = h->cap;
+    Handle::SigmaRun sr;
+    sr.sel.assign(sel, sel + nsel);
+    double* dbl = nullptr;
+    int* ib = nullptr;
+    CUDA_TRY(h, cudaMalloc(&dbl, sizeof(double) * (size_t)((3 * nsel + 1) * c + nsel * n)));
+    if (cudaMalloc(&ib, sizeof(int) * (size_t)(3 * nsel)) != cudaSuccess) {
+        cudaFree(dbl);
+        cudaGetLastError();
+        return fail(h, BRGPU_ERR_CUDA, "selected rows: out of device memory");
+    }
+    std::vector<int> s32(sr.sel.begin(), sr.sel.end());
+    int rc = BRGPU_OK;
+    if (cudaMemcpy(ib, s32.data(), sizeof(int) * (size_t)nsel, cudaMemcpyHostToDevice) != cudaSuccess)
+        rc = fail(h, BRGPU_ERR_CUDA, "selected rows: copy of the request failed");
+    sr.dev.nsel = (int)nsel;
+    sr.dev.stride = c;
+    sr.dev.sel = ib;
+    sr.dev.S = dbl;
+    sr.dev.X = dbl + nsel * c;
+    sr.dev.XA = dbl + 2 * nsel * c;
+    sr.dev.Z0 = dbl + 3 * nsel * c;
+    sr.out = dbl + (3 * nsel + 1) * c;
+    sr.dTask = ib + nsel;
+    sr.dBlk = ib + 2 * nsel;
+    if (!rc && cudaMemsetAsync(sr.out, 0, sizeof(double) * (size_t)(nsel * n), h->stream) != cudaSuccess)
+        rc = fail(h, BRGPU_ERR_CUDA, "selected rows: memset failed");
+    if (!rc) {
+        h->sig = &sr;
+        rc = brgpu_eigvals(hh, n, d, e, w);
+        h->sig = nullptr;
+        if (!rc && cudaMemcpy(rows, sr.out, sizeof(double) * (size_t)(nsel * n), cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(h, BRGPU_ERR_CUDA, "selected rows: copy of the rows failed");
+    }
+    cudaFree(dbl);
+    cudaFree(ib);
+    return rc;
 }
 
 // ---------------------------------------------------------------------------

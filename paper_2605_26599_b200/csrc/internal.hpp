@@ -71,6 +71,20 @@ struct LevelDev {
     const int* tileFirst;      // ceil(n/kTile)+1 entries
     int M;
     int allSplit;              // every merge of the level is larger than kSplitMinSize (warp tier only)
+    int maxSize;               // largest merge of the level
+};
+
+// Requested eigenvector rows (Algorithm 1's sigma, sigma.cu).  Per requested
+// row r: S = the row in the current nodes' eigenvalue order (node positions),
+// X = merged order, XA = active order; each nsel x stride doubles.
+struct SigmaDev {
+    int nsel;
+    long long stride;
+    const int* sel;  // global row index per request
+    double* S;
+    double* X;
+    double* XA;
+    double* Z0;      // merged z before the close-pole walk (stride doubles)
 };
 
 // A run of consecutive fused levels launched as one kernel (k_levels_fused).
@@ -99,6 +113,7 @@ struct SolveParams {
     int xc;
     double* xA;
     double* xB;
+    const SigmaDev* sigma;  // requested rows (grid tier only), or null
 };
 
 }  // namespace brgpu

@@ -1229,6 +1229,9 @@ __global__ void k_xunpack(Work w, int n, int kind, int c, const double* __restri
 // root-range split exchanges results (prm.xsplit): 0 deflation + secular roots,
 // 1 refreshed weights, 2 boundary rows + root placement, 3 deflated placement.
 // Without a split the parts run back to back.
+void launch_sigma_stage(cudaStream_t s, const Work& w, const LevelDev& L, const SigmaDev& sg, int maxSize,
+                        int stage, int* launches);
+
 void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
                        int part, int* launches, Prof* prof) {
     const bool lane_tier = !L.allSplit;  // all merges > kSplitMinSize: warp tier only
@@ -1250,10 +1253,12 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         PMARK(BRGPU_K_SCATTER);
         launch_pdl(k_merge_nn, mtiles, kMergeTile, 0, s, w, L, n, prm.tol_scale, w.org, st1, tk);
         PMARK(BRGPU_K_NNFLAG);
+        if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 0, &nl);
         launch_pdl(k_segment_walk, cdiv(n, 256), 256, 0, s, w, L, n, prm.tol_scale);
         PMARK(BRGPU_K_WALK);
         launch_pdl(k_surv_scan, ntiles, kScanBlock, 0, s, w, L, n, st2, tk + 1);
         PMARK(BRGPU_K_SURVWRITE);
+        if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 1, &nl);
         nl += 4;
         if (lane_tier) {
             launch_pdl(k_level_modes, cdiv(L.M, 256), 256, 0, s, w, L);
@@ -1276,6 +1281,8 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         }
     } else if (part == 2) {
         if (x && prm.zhat) { launch_pdl(k_xunpack, xu, 256, 0, s, w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
+        // requested rows need the roots (tau, org) that the rows kernels overwrite
+        if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 2, &nl);
         if (lane_tier) { launch_pdl(k_rows, cdiv(n, kSecBlock), kSecBlock, 0, s, w, L, n); ++nl; }
         launch_rows_warp(s, w, L, n, prm);
         ++nl;
