@@ -79,6 +79,8 @@ struct Ledger {
 struct BrResult {
     std::vector<double> lambda;  // ascending
     Ledger ledger;
+    /// |sigma| x n, row-major: selected_rows[r*n + j] = Q(sigma_r, j); empty if no request
+    std::vector<double> selected_rows;
 };
 
 /// One handle = one device + one stream; use one Solver per host thread.
@@ -114,6 +116,26 @@ public:
     BrResult br_eigenvalues(const TM& t) {
         BrResult r;
         r.lambda = eigenvalues(t.d, t.e);
+        brgpu_ledger l;
+        check(brgpu_get_ledger(h_, &l));
+        r.ledger = Ledger{l.live_doubles, l.peak_doubles, l.live_ints, l.peak_ints, l.limit_doubles,
+                          l.limit_ints};
+        return r;
+    }
+
+    /// Algorithm 1 with a row request: eigenvalues plus rows Q(sigma_r, :) (0-based
+    /// row indices, duplicates and any order allowed).
+    template <class TM>
+    BrResult br_eigenvalues(const TM& t, const std::vector<std::int64_t>& sigma) {
+        if (t.d.empty()) throw InvalidArgument("tridiagonal: order must be positive");
+        if (t.e.size() + 1 != t.d.size()) throw InvalidArgument("tridiagonal: off-diagonal length != n-1");
+        BrResult r;
+        const std::int64_t n = static_cast<std::int64_t>(t.d.size());
+        r.lambda.resize(t.d.size());
+        r.selected_rows.resize(sigma.size() * t.d.size());
+        check(brgpu_eigvals_rows(h_, n, t.d.data(), t.e.empty() ? nullptr : t.e.data(),
+                                 static_cast<std::int64_t>(sigma.size()), sigma.empty() ? nullptr : sigma.data(),
+                                 r.lambda.data(), sigma.empty() ? nullptr : r.selected_rows.data()));
         brgpu_ledger l;
         check(brgpu_get_ledger(h_, &l));
         r.ledger = Ledger{l.live_doubles, l.peak_doubles, l.live_ints, l.peak_ints, l.limit_doubles,

@@ -130,6 +130,7 @@ struct Plan {
     int maxM = 0;
     int maxLeaf = 0;
     bool sigma = false;  // requested-rows plan: grid tier everywhere, no root-only merges
+    std::vector<int> tByOff;  // leaf tasks in offset order (requested-rows plans)
     // device copies
     int* dev = nullptr;  // one int buffer
     size_t devInts = 0;
@@ -202,6 +203,10 @@ struct Handle {
         double* out = nullptr; // nsel x n, global column order
     };
     SigmaRun* sig = nullptr;
+    double* sigDbl = nullptr;  // grow-only buffers of the requested-rows solves (never in a graph)
+    int64_t sigDblCap = 0;
+    int* sigInt = nullptr;
+    int64_t sigIntCap = 0;
 };
 
 int fail(Handle* h, int code, const std::string& msg) {
@@ -954,9 +959,12 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
         Handle::SigmaRun& sr = *h->sig;
         const int ns = (int)sr.sel.size();
         std::vector<int> task((size_t)ns, -1), blk((size_t)ns, 0);
-        std::vector<int> byOff((size_t)p->tOff.size());
-        for (size_t t = 0; t < byOff.size(); ++t) byOff[t] = (int)t;
-        std::sort(byOff.begin(), byOff.end(), [&](int a, int b) { return p->tOff[a] < p->tOff[b]; });
+        std::vector<int>& byOff = p->tByOff;
+        if (byOff.size() != p->tOff.size()) {
+            byOff.resize(p->tOff.size());
+            for (size_t t = 0; t < byOff.size(); ++t) byOff[t] = (int)t;
+            std::sort(byOff.begin(), byOff.end(), [&](int a, int b) { return p->tOff[a] < p->tOff[b]; });
+        }
         sr.maxBlock = 0;
         for (size_t b = 0; b + 1 < bstart.size(); ++b) sr.maxBlock = std::max(sr.maxBlock, bstart[b + 1] - bstart[b]);
         for (int r = 0; r < ns; ++r) {
@@ -1170,6 +1178,8 @@ int brgpu_destroy(brgpu_handle* hh) {
     if (h->hsmall) cudaFreeHost(h->hsmall);
     if (h->hcnt) cudaFreeHost(h->hcnt);
     if (h->dsmall) cudaFree(h->dsmall);
+    if (h->sigDbl) cudaFree(h->sigDbl);
+    if (h->sigInt) cudaFree(h->sigInt);
     for (auto& e : h->tev) if (e) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete hh;
@@ -1305,14 +1315,19 @@ int brgpu_eigvals_rows(brgpu_handle* hh, int64_t n, const double* d, const doubl
     const int64_t c = h->cap;
     Handle::SigmaRun sr;
     sr.sel.assign(sel, sel + nsel);
-    double* dbl = nullptr;
-    int* ib = nullptr;
-    CUDA_TRY(h, cudaMalloc(&dbl, sizeof(double) * (size_t)((3 * nsel + 1) * c + nsel * n)));
-    if (cudaMalloc(&ib, sizeof(int) * (size_t)(3 * nsel)) != cudaSuccess) {
-        cudaFree(dbl);
-        cudaGetLastError();
+    auto grow = [&](auto*& p, int64_t& cap, int64_t need) -> bool {
+        if (need <= cap) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaMalloc(&p, sizeof(*p) * (size_t)need) != cudaSuccess) { cudaGetLastError(); return false; }
+        cap = need;
+        return true;
+    };
+    if (!grow(h->sigDbl, h->sigDblCap, (3 * nsel + 1) * c + nsel * n) || !grow(h->sigInt, h->sigIntCap, 3 * nsel))
         return fail(h, BRGPU_ERR_CUDA, "selected rows: out of device memory");
-    }
+    double* dbl = h->sigDbl;
+    int* ib = h->sigInt;
     std::vector<int> s32(sr.sel.begin(), sr.sel.end());
     int rc = BRGPU_OK;
     if (cudaMemcpy(ib, s32.data(), sizeof(int) * (size_t)nsel, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -1336,8 +1351,6 @@ int brgpu_eigvals_rows(brgpu_handle* hh, int64_t n, const double* d, const doubl
         if (!rc && cudaMemcpy(rows, sr.out, sizeof(double) * (size_t)(nsel * n), cudaMemcpyDeviceToHost) != cudaSuccess)
             rc = fail(h, BRGPU_ERR_CUDA, "selected rows: copy of the rows failed");
     }
-    cudaFree(dbl);
-    cudaFree(ib);
     return rc;
 }
 

@@ -19,4 +19,7 @@ for n, ns in [(1<<20, 2), (1<<20, 16), (1<<16, 64)]:
     t = time.perf_counter()
     for _ in range(3): s.eigvals(d, e)
     t0 = (time.perf_counter() - t) / 3
+    s.eigvals_rows(d, e, sel)
+    tm = s.timing()
+    print(f"n={n} nsel={ns}: device {tm}")
     print(f"n={n} nsel={ns}: rows {t1*1e3:.2f} ms  eigvals-only {t0*1e3:.2f} ms  row-norm err {np.abs((R*R).sum(1)-1).max():.1e}")
