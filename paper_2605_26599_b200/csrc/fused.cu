@@ -404,6 +404,7 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
             const int t = upper_index(S.kS, cnt, g);
             if (S.mf[t] & kMergeRoot) continue;
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
+            if (K == 1) continue;  // a lone pole keeps its z (the checker refreshes only K > 1)
             const double di = pairs[g].x;
             double prod = 1.0;
             const bool fast = !w.exact && zhat_guard(PolesPairs{pairs + ks}, K, i);

@@ -891,7 +891,9 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
         const int m = w.aMerge[g];
         int ke;
         active_range(w, L, m, ks, ke);
-        if ((L.mFlags[m] & kMergeRoot) || split_mode(L.mSize[m], ke - ks) || !owns(w, g)) act = false;
+        // a lone pole keeps its z (the checker refreshes only K > 1)
+        if ((L.mFlags[m] & kMergeRoot) || split_mode(L.mSize[m], ke - ks) || !owns(w, g) || ke - ks == 1)
+            act = false;
         K = ke - ks;
         i = g - ks;
         di = w.dA[g];

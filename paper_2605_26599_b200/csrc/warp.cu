@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
             const int m = w.aMerge[g];
             int ke;
             merge_active(w, L, m, ks, ke);
-            act = split_mode(L.mSize[m], ke - ks) && !(L.mFlags[m] & kMergeRoot) && owns(w, g);
+            // a lone pole keeps its z (the checker refreshes only K > 1)
+            act = split_mode(L.mSize[m], ke - ks) && !(L.mFlags[m] & kMergeRoot) && owns(w, g) && ke - ks > 1;
             K = ke - ks;
             i = g - ks;
             di = w.dA[g];
