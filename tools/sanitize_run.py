@@ -24,3 +24,10 @@ with br.Solver(0, br.BrOptions(use_graph=False, subtree=False)) as s:
     d, e = G.generate("wilkinson", 20000)
     s.eigvals(d, e)
     print("grid-only ok")
+with br.Solver(0) as s:  # requested rows (sigma.cu), incl. the split tier and several blocks
+    for fam, n in [("sym-uniform", 3000 if SMALL else 20000), ("toeplitz121", 2000 if SMALL else 10000)]:
+        d, e = G.generate(fam, n)
+        e[n // 3] = 0.0
+        w, R = s.eigvals_rows(d, e, [0, n // 3, n // 3 + 1, n - 1, 7, 7])
+        assert np.allclose((R * R).sum(1), 1.0, atol=1e-12)
+    print("rows ok")
