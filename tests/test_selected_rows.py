@@ -91,26 +91,35 @@ def test_split_row_request_spec_examples():
 
 
 def test_split_row_request_matches_child_rows():
-    """Merging children's selected rows at original positions reproduces the
-    parent selection (the relative-order lemma of): the rows of the
-    block-diagonal child eigenvector matrix Q_L (+) Q_R for sigma are the child
-    requests' rows, placed in the child's column range."""
+    """Merging the children's selected rows at their original positions
+    reproduces the parent selection: with a zero cut, T =
+    T_L (+) T_R, and each requested row of T is the row its child request
+    returns, placed at the child's eigenvalues in the global order (bitwise:
+    both blocks scale by 1)."""
     from paper_2605_26599_b200 import split_row_request
     rng = np.random.default_rng(3)
     dl, el = rng.uniform(-1, 1, 30), rng.uniform(-1, 1, 29)
     dr, er = rng.uniform(-1, 1, 34), rng.uniform(-1, 1, 33)
     sigma = (31, 2, 30, 64, 2)
     L, R = split_row_request(sigma, 30, size=64)
+    assert L.sigma == (2, 30, 2, 30) and R.sigma == (1, 34, 1)  # boundary rows last
     wl, QL = O.eigvals_rows(dl, el, np.asarray(L.sigma) - 1)
     wr, QR = O.eigvals_rows(dr, er, np.asarray(R.sigma) - 1)
-    li = iter(range(len(L.sigma) - 1))
-    ri = iter(range(len(R.sigma) - 1))
-    for s in sigma:  # every requested row maps into exactly one child request
-        if s <= 30:
-            assert L.sigma[next(li)] == s
+    w, Q = O.eigvals_rows(np.r_[dl, dr], np.r_[el, 0.0, er], np.asarray(sigma) - 1)
+    order = np.argsort(np.r_[wl, wr], kind="stable")
+    assert np.array_equal(w, np.r_[wl, wr][order])
+    inv = np.empty(64, dtype=np.int64)
+    inv[order] = np.arange(64)
+    li = ri = 0
+    for r, s_ in enumerate(sigma):
+        want = np.zeros(64)
+        if s_ <= 30:
+            want[inv[:30]] = QL[li]
+            li += 1
         else:
-            assert R.sigma[next(ri)] == s - 30
-    assert L.sigma[-1] == 30 and R.sigma[-1] == 1  # the split-boundary rows that build z
+            want[inv[30:]] = QR[ri]
+            ri += 1
+        assert np.array_equal(Q[r], want)
 
 
 # ------------------------------------------------------------------------------ GPU
@@ -165,3 +174,30 @@ def test_gpu_rows_errors_and_plan_switch(solver):
     assert np.array_equal(w0, w1) and np.array_equal(w0, w2)
     w3, R3 = solver.eigvals_rows(d, e, [])
     assert np.array_equal(w0, w3) and R3.shape == (0, 500)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("opts,chk", [(dict(zhat=False), dict(zhat=False)),
+                                      (dict(patched_stop=False), dict(patched=False)),
+                                      (dict(leaf_cutoff=8), dict(leaf_cutoff=8)),
+                                      (dict(exact_passes=True), {})])
+def test_gpu_rows_options(opts, chk):
+    import paper_2605_26599_b200 as br
+    d, e = G.generate("sym-uniform", 3000)
+    sel = [0, 1, 1499, 1500, 2999, 1500]
+    with br.Solver(0, br.BrOptions(**opts)) as s:
+        w, R = s.eigvals_rows(d, e, sel)
+    wc, Rc = O.eigvals_rows(d, e, sel, **chk)
+    assert np.array_equal(w, wc) and np.array_equal(R, Rc)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale", [2.0 ** -1040, 2.0 ** 1000])
+def test_gpu_rows_extreme_scales(solver, scale):
+    d, e = G.generate("sym-uniform", 2000)
+    d, e = d * scale, e * scale
+    sel = [3, 1000, 1999]
+    w, R = solver.eigvals_rows(d, e, sel)
+    wc, Rc = O.eigvals_rows(d, e, sel)
+    assert np.array_equal(w, wc) and np.array_equal(R, Rc)
+    assert np.allclose((R * R).sum(1), 1.0, atol=1e-12)
