@@ -62,7 +62,6 @@ constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (nu
 constexpr int kFuseMaxMergesHost = 128;
 
 void init_kernel_attributes();
-void init_sigma_attributes();
 void launch_sigma_leaves(cudaStream_t s, const SigmaDev& sg, int maxm, const int* taskOf, const int* tOff,
                          const int* tSize, const Work& w, int* launches);
 void launch_sigma_final(cudaStream_t s, const SigmaDev& sg, const double* lam, const int* bstart, int nblk,
@@ -1146,7 +1145,6 @@ int brgpu_create(brgpu_handle** out, int device) {
     }
     brgpu::init_kernel_attributes();
     brgpu::init_fused_attributes();
-    brgpu::init_sigma_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
     *out = hh;

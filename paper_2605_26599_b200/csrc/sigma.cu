@@ -215,21 +215,13 @@ void launch_sigma_leaves(cudaStream_t s, const SigmaDev& sg, int maxm, const int
                          const int* tSize, const Work& w, int* launches) {
     if (sg.nsel <= 0) return;
     const int grid = cdiv(sg.nsel, kSigLeafThreads);
-    if (maxm <= 16)
+    if (maxm <= 16)  // leaf cutoff <= 32 (BRGPU_OPT_LEAF_CUTOFF): 32 KiB of SMEM at most
         launch_pdl(k_sig_leaf<16>, grid, kSigLeafThreads, (size_t)4 * 16 * kSigLeafThreads * 8, s, sg, taskOf,
                    tOff, tSize, w.dw, w.ew, w.status);
-    else if (maxm <= 32)
+    else
         launch_pdl(k_sig_leaf<32>, grid, kSigLeafThreads, (size_t)4 * 32 * kSigLeafThreads * 8, s, sg, taskOf,
                    tOff, tSize, w.dw, w.ew, w.status);
-    else
-        launch_pdl(k_sig_leaf<64>, grid, kSigLeafThreads, (size_t)4 * 64 * kSigLeafThreads * 8, s, sg, taskOf,
-                   tOff, tSize, w.dw, w.ew, w.status);
     ++*launches;
-}
-
-void init_sigma_attributes() {
-    cudaFuncSetAttribute(k_sig_leaf<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4 * 64 * kSigLeafThreads * 8);
 }
 
 // stage 0: after k_merge_nn; 1: after k_surv_scan; 2: after the refreshed weights
