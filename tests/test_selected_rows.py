@@ -201,3 +201,15 @@ def test_gpu_rows_extreme_scales(solver, scale):
     wc, Rc = O.eigvals_rows(d, e, sel)
     assert np.array_equal(w, wc) and np.array_equal(R, Rc)
     assert np.allclose((R * R).sum(1), 1.0, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_gpu_rows_leaf_cutoff_32():
+    import paper_2605_26599_b200 as br
+    d, e = G.generate("sym-uniform", 2500)
+    e[[40, 41, 100]] = 0.0  # blocks of 1 and 59 rows beside the big one
+    sel = [0, 40, 41, 60, 2499]
+    with br.Solver(0, br.BrOptions(leaf_cutoff=32)) as s:
+        w, R = s.eigvals_rows(d, e, sel)
+    wc, Rc = O.eigvals_rows(d, e, sel, leaf_cutoff=32)
+    assert np.array_equal(w, wc) and np.array_equal(R, Rc)
