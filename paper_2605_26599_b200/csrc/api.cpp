@@ -53,7 +53,11 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int ngroups, const int2* tab,
                          const SolveParams& prm, int* launches, Prof* prof);
 void init_fused_attributes();
-constexpr int kFuseMaxElems = 1024;
+#ifndef BRGPU_FUSE_MAX_ELEMS
+#define BRGPU_FUSE_MAX_ELEMS 1024
+#endif
+constexpr int kFuseMaxElems = BRGPU_FUSE_MAX_ELEMS;
+constexpr int kGridMinN = 32768;  // below this order, underfilled 1024-shape levels stay fused  // largest merge of a fused SMEM level (512 or 1024)
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
 #ifndef BRGPU_SPLIT_MIN_SIZE
 #define BRGPU_SPLIT_MIN_SIZE 8192
@@ -128,6 +132,7 @@ struct Plan {
     int height = 0;
     int maxM = 0;
     int maxLeaf = 0;
+    int sms = 148;       // SM count of the device (fused-tier fill rule)
     bool sigma = false;  // requested-rows plan: grid tier everywhere, no root-only merges
     std::vector<int> tByOff;  // leaf tasks in offset order (requested-rows plans)
     // device copies
@@ -289,7 +294,14 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         }
         L.minSize = minSize;
         L.maxSize = maxSize;
-        L.fused = fuse && maxSize <= kFuseMaxElems;
+        // A 1024-shape level runs 2 CTAs per SM; with fewer merges than SMs most
+        // of the GPU idles (Toeplitz 2^16, level 6: 64 merges of K ~ 512), and the
+        // grid tier, which spreads every merge over the whole GPU, is faster
+        // once n is large enough to amortise its ~15 launches per level
+        // (A/B: Toeplitz 2^16 20.7 -> 20.1 ms; glued Wilkinson 2^18, 256 merges,
+        // and n = 4096 stay fused).
+        const bool underfilled = maxSize > kFuseSmallElems && L.M < p->sms && p->n >= kGridMinN;
+        L.fused = fuse && maxSize <= kFuseMaxElems && !underfilled;
         L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
         L.G = 0;
@@ -373,9 +385,11 @@ void plan_fused_runs(Plan* p) {
 // least 2^D * 2(cutoff+1) elements (D = floor(log2 nranks)) are split by
 // subtree; smaller blocks go to ranks in contiguous chunks of the total size.
 std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
-                                const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0) {
+                                const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0,
+                                int sms = 148) {
     auto p = std::make_unique<Plan>();
     p->n = n;
+    p->sms = sms;
     p->cutoff = cutoff;
     p->bstart = bstart;
     p->segs = segs;
@@ -835,7 +849,7 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
         u->w.counters = h->w.counters;
         CUDA_TRY(h, cudaMemcpyAsync(u->w.dw, h->w.dw, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(h, cudaMemcpyAsync(u->w.ew, h->w.ew, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-        plans.push_back(make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, P, k));
+        plans.push_back(make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, P, k, h->sms));
         if (int r = upload_plan(u, plans.back().get())) return fail(h, r, u->err);
         if (int r = ensure_buf_sizes(u, plans.back().get())) return fail(h, r, u->err);
         CUDA_TRY(h, cudaMemsetAsync(u->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
@@ -945,7 +959,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs ||
         p->sigma != sig) {
         if (h->plan) free_plan(h->plan.get());
-        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0, h->nranks, h->rank);
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0, h->nranks, h->rank, h->sms);
         p = h->plan.get();
         if (sig) {  // every merge propagates the requested rows: no root-only mode
             p->sigma = true;
