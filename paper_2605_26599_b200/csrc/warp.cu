@@ -177,36 +177,60 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
 }
 
 // ---------------------------------------------------------------------------
-// refreshed weights, one warp per pole (product over roots, split by lane)
+// refreshed weights, kZhatPerWarp poles per warp (product over roots, split by lane)
 // ---------------------------------------------------------------------------
+#ifndef BRGPU_ZHAT_PER_WARP
+#define BRGPU_ZHAT_PER_WARP 2
+#endif
+constexpr int kZhatPerWarp = BRGPU_ZHAT_PER_WARP;
+
+struct WarpZhatPole {
+    int g, ks, K, i;
+    bool act, fast;
+    double di, prod;
+};
+
+// Poles of one warp share every root tile read from shared memory (d_org,
+// tau, d_j: 24 B per term), which halves the SMEM traffic per FP64 term at 2
+// poles per warp.  Each pole keeps its lane-strided product order and the
+// butterfly, so results are bitwise those of one pole per warp.
 __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, int n) {
     pdl_entry();
     __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {  // uniform per CTA
-        const int g = base + wid;
-        bool act = g < T;
-        int ks = 0, K = 0, i = 0;
-        double di = 0.0;
-        if (act) {
-            const int m = w.aMerge[g];
-            int ke;
-            merge_active(w, L, m, ks, ke);
-            // a lone pole keeps its z (the checker refreshes only K > 1)
-            act = split_mode(L.mSize[m], ke - ks) && !(L.mFlags[m] & kMergeRoot) && owns(w, g) && ke - ks > 1;
-            K = ke - ks;
-            i = g - ks;
-            di = w.dA[g];
+    constexpr int PPC = (kWarpThreads / 32) * kZhatPerWarp;  // poles per CTA step
+    for (int base = blockIdx.x * PPC; base < T; base += gridDim.x * PPC) {  // uniform per CTA
+        WarpZhatPole pl[kZhatPerWarp];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < kZhatPerWarp; ++q) {
+            WarpZhatPole& P = pl[q];
+            P.g = base + wid * kZhatPerWarp + q;
+            P.ks = 0; P.K = 0; P.i = 0; P.act = false; P.fast = false; P.di = 0.0; P.prod = 1.0;
+            if (P.g < T) {
+                const int m = w.aMerge[P.g];
+                int ke;
+                merge_active(w, L, m, P.ks, ke);
+                // a lone pole keeps its z (the checker refreshes only K > 1)
+                P.act = split_mode(L.mSize[m], ke - P.ks) && !(L.mFlags[m] & kMergeRoot) && owns(w, P.g) &&
+                        ke - P.ks > 1;
+                P.K = ke - P.ks;
+                P.i = P.g - P.ks;
+                P.di = w.dA[P.g];
+                P.fast = P.act && !w.exact && zhat_guard(PolesPtr{w.dA + P.ks}, P.K, P.i);
+            }
+            any = any || P.act;
         }
-        if (!__syncthreads_or(act)) continue;
-        const int gl = min(base + 8, T) - 1;
+        if (!__syncthreads_or(any)) continue;
+        const int gl = min(base + PPC, T) - 1;
         int P0, P1, tmp;
         merge_active(w, L, w.aMerge[base], P0, tmp);
         merge_active(w, L, w.aMerge[gl], tmp, P1);
-        double prod = 1.0;
-        const bool fast = act && !w.exact && zhat_guard(PolesPtr{w.dA + ks}, K, i);
+        bool shared = true;  // every pole of the warp is fast and in the same merge
+#pragma unroll
+        for (int q = 0; q < kZhatPerWarp; ++q) shared = shared && pl[q].fast && pl[q].ks == pl[0].ks;
         for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
             const int thi = min(tlo + kWarpTile, P1);
             __syncthreads();
@@ -218,90 +242,159 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
                 s_dj[r - tlo] = w.dA[r];
             }
             __syncthreads();
-            if (fast) {
-                // roots before the pole, the pole's own factor, roots after:
-                // one split point per lane, so no per-term self select
-                const int lo = max(ks, tlo), hi = min(ks + K, thi);
-                const int mid = min(hi, ks + i);
+            if (shared) {
+                // the poles' own indices (ascending: consecutive g of one merge)
+                // split each lane's strided range; between them every factor is
+                // del / (d_i - d_j), so the inner loop has no per-term select
+                const int ks = pl[0].ks;
+                const int lo = max(ks, tlo), hi = min(ks + pl[0].K, thi);
                 int jg = strided_start(lo, ks, lane);
-#pragma unroll 4
-                for (; jg < mid; jg += 32) {
-                    const int t = jg - tlo;
-                    prod = prod * (((di - s_dorg[t]) - s_tau[t]) * rcp_nr(di - s_dj[t]));
+#pragma unroll
+                for (int sp = 0; sp <= kZhatPerWarp; ++sp) {
+                    const int stop = sp < kZhatPerWarp ? min(hi, ks + pl[sp].i) : hi;
+#pragma unroll 2
+                    for (; jg < stop; jg += 32) {
+                        const int t = jg - tlo;
+                        const double dorg = s_dorg[t], tau = s_tau[t], dj = s_dj[t];
+#pragma unroll
+                        for (int q = 0; q < kZhatPerWarp; ++q)
+                            pl[q].prod = pl[q].prod * (((pl[q].di - dorg) - tau) * rcp_nr(pl[q].di - dj));
+                    }
+                    if (sp < kZhatPerWarp && jg == ks + pl[sp].i && jg < hi) {
+                        const int t = jg - tlo;
+                        const double dorg = s_dorg[t], tau = s_tau[t], dj = s_dj[t];
+#pragma unroll
+                        for (int q = 0; q < kZhatPerWarp; ++q) {
+                            const double del = (pl[q].di - dorg) - tau;
+                            pl[q].prod = pl[q].prod * (q == sp ? del : del * rcp_nr(pl[q].di - dj));
+                        }
+                        jg += 32;
+                    }
                 }
-                if (jg == ks + i && jg < hi) {
-                    const int t = jg - tlo;
-                    prod = prod * ((di - s_dorg[t]) - s_tau[t]);
-                    jg += 32;
-                }
-#pragma unroll 4
-                for (; jg < hi; jg += 32) {
-                    const int t = jg - tlo;
-                    prod = prod * (((di - s_dorg[t]) - s_tau[t]) * rcp_nr(di - s_dj[t]));
+            } else {
+#pragma unroll
+                for (int q = 0; q < kZhatPerWarp; ++q) {
+                    WarpZhatPole& P = pl[q];
+                    if (!P.fast) continue;
+                    // roots before the pole, the pole's own factor, roots after:
+                    // one split point per lane, so no per-term self select
+                    const int ks = P.ks;
+                    const double di = P.di;
+                    const int lo = max(ks, tlo), hi = min(ks + P.K, thi);
+                    const int mid = min(hi, ks + P.i);
+                    int jg = strided_start(lo, ks, lane);
+                    double prod = P.prod;
+                    for (; jg < mid; jg += 32) {
+                        const int t = jg - tlo;
+                        prod = prod * (((di - s_dorg[t]) - s_tau[t]) * rcp_nr(di - s_dj[t]));
+                    }
+                    if (jg == ks + P.i && jg < hi) {
+                        const int t = jg - tlo;
+                        prod = prod * ((di - s_dorg[t]) - s_tau[t]);
+                        jg += 32;
+                    }
+                    for (; jg < hi; jg += 32) {
+                        const int t = jg - tlo;
+                        prod = prod * (((di - s_dorg[t]) - s_tau[t]) * rcp_nr(di - s_dj[t]));
+                    }
+                    P.prod = prod;
                 }
             }
         }
-        if (act) {
-            if (!fast) {  // exact redo
-                prod = 1.0;
-                for (int jg = ks + lane; jg < ks + K; jg += 32) {
-                    const double del = (di - w.dA[ks + w.org[jg]]) - w.tau[jg];
-                    if (jg - ks == i) prod = prod * del;
-                    else prod = prod * (del * __drcp_rn(di - w.dA[jg]));
+#pragma unroll
+        for (int q = 0; q < kZhatPerWarp; ++q) {
+            WarpZhatPole& P = pl[q];
+            if (!P.act) continue;
+            if (!P.fast) {  // exact redo
+                P.prod = 1.0;
+                for (int jg = P.ks + lane; jg < P.ks + P.K; jg += 32) {
+                    const double del = (P.di - w.dA[P.ks + w.org[jg]]) - w.tau[jg];
+                    if (jg - P.ks == P.i) P.prod = P.prod * del;
+                    else P.prod = P.prod * (del * __drcp_rn(P.di - w.dA[jg]));
                 }
             }
-            const double W = bfly_mul(prod);
+            const double W = bfly_mul(P.prod);
             if (lane == 0) {
                 const double mag = sqrt(fmax(0.0, -W));
-                w.zA[g] = w.zA[g] >= 0.0 ? mag : -mag;
+                w.zA[P.g] = w.zA[P.g] >= 0.0 ? mag : -mag;
             }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// boundary rows + placement, one warp per root
+// boundary rows + placement, kRowsPerWarp roots per warp
 // ---------------------------------------------------------------------------
+#ifndef BRGPU_ROWS_PER_WARP
+#define BRGPU_ROWS_PER_WARP 2
+#endif
+constexpr int kRowsPerWarp = BRGPU_ROWS_PER_WARP;  // roots per warp in k_rows_warp
+
+// One root of k_rows_warp.
+struct WarpRowRoot {
+    int g, ks, K, p;
+    bool rows, fast;
+    double dorg, tau;
+};
+
+// Up to kRowsPerWarp roots per warp: a pole tile read from shared memory
+// (d, zhat, r0, r1: 32 B per term) feeds every root of the warp, so the SMEM
+// traffic per FP64 term halves (the 1-root loop moved 8 SMEM wavefronts per
+// 5.5 FP64-issue cycles and was SMEM-bound).  Each root keeps its own lane-
+// strided accumulation order and butterfly, so results are bitwise those of
+// one root per warp.
 __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
     pdl_entry();
     __shared__ double s_d[kWarpTile], s_zh[kWarpTile], s_r0[kWarpTile], s_r1[kWarpTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int base = blockIdx.x * 8; base < T; base += gridDim.x * 8) {
-        const int g = base + wid;
-        bool act = g < T, rows = false;
-        int ks = 0, K = 0, p = 0;
-        double dorg = 0.0, tau = 0.0;
-        if (act) {
-            const int m = w.aMerge[g];
-            int ke;
-            merge_active(w, L, m, ks, ke);
-            act = split_mode(L.mSize[m], ke - ks);
-            if (act) {
-                K = ke - ks;
-                const int j = g - ks;
-                const int off = L.mOff[m], size = L.mSize[m];
-                dorg = w.dA[ks + w.org[g]];
-                tau = w.tau[g];
-                const double lam = dorg + tau;
-                const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + ks, K, lam);
-                p = off + pos;
-                if (lane == 0) {
-                    w.lam[p] = lam;
-                    w.tau[g] = lam;  // dead after the reads above: k_deflated_out searches root
-                    w.org[g] = p;    // values, the root-range split exchange finds the position
+    constexpr int RPC = (kWarpThreads / 32) * kRowsPerWarp;  // roots per CTA step
+    for (int base = blockIdx.x * RPC; base < T; base += gridDim.x * RPC) {
+        WarpRowRoot rt[kRowsPerWarp];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            WarpRowRoot& R = rt[q];
+            R.g = base + wid * kRowsPerWarp + q;
+            R.ks = 0; R.K = 0; R.p = 0; R.rows = false; R.fast = false; R.dorg = 0.0; R.tau = 0.0;
+            if (R.g < T) {
+                const int m = w.aMerge[R.g];
+                int ke;
+                merge_active(w, L, m, R.ks, ke);
+                if (split_mode(L.mSize[m], ke - R.ks)) {
+                    R.K = ke - R.ks;
+                    const int j = R.g - R.ks;
+                    const int off = L.mOff[m], size = L.mSize[m];
+                    R.dorg = w.dA[R.ks + w.org[R.g]];
+                    R.tau = w.tau[R.g];
+                    const double lam = R.dorg + R.tau;
+                    const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + R.ks, R.K, lam);
+                    R.p = off + pos;
+                    if (lane == 0) {
+                        w.lam[R.p] = lam;
+                        w.tau[R.g] = lam;  // dead after the reads above: k_deflated_out searches root
+                        w.org[R.g] = R.p;  // values, the root-range split exchange finds the position
+                    }
+                    R.rows = !(L.mFlags[m] & kMergeRoot) && owns(w, R.g);
+                    R.fast = R.rows && !w.exact &&
+                             eval_guard(GlobalPairs{w.dA + R.ks, w.z2A + R.ks}, R.K, j, R.dorg, R.tau);
                 }
-                rows = !(L.mFlags[m] & kMergeRoot) && owns(w, g);
             }
+            any = any || R.rows;
         }
-        if (!__syncthreads_or(rows)) continue;
-        const int gl = min(base + 8, T) - 1;
+        if (!__syncthreads_or(any)) continue;
+        const int gl = min(base + RPC, T) - 1;
         int P0, P1, tmp;
         merge_active(w, L, w.aMerge[base], P0, tmp);
         merge_active(w, L, w.aMerge[gl], tmp, P1);
-        double nn = 0.0, s0 = 0.0, s1 = 0.0;
-        const bool fast = rows && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, g - ks, dorg, tau);
+        double nn[kRowsPerWarp], s0[kRowsPerWarp], s1[kRowsPerWarp];
+        bool shared = true;  // every fast root of the warp streams the same pole range
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            nn[q] = 0.0; s0[q] = 0.0; s1[q] = 0.0;
+            shared = shared && rt[q].fast && rt[q].ks == rt[0].ks;
+        }
         for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
             const int thi = min(tlo + kWarpTile, P1);
             __syncthreads();
@@ -312,37 +405,60 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
                 s_r1[r - tlo] = w.r1A[r];
             }
             __syncthreads();
-            if (fast) {
-                const int lo = max(ks, tlo), hi = min(ks + K, thi);
-#pragma unroll 4
+            if (shared) {
+                const int ks = rt[0].ks;
+                const int lo = max(ks, tlo), hi = min(ks + rt[0].K, thi);
+#pragma unroll 2
                 for (int i = strided_start(lo, ks, lane); i < hi; i += 32) {
                     const int t = i - tlo;
-                    const double y = s_zh[t] * rcp_nr((s_d[t] - dorg) - tau);
-                    nn = __fma_rn(y, y, nn);
-                    s0 = __fma_rn(s_r0[t], y, s0);
-                    s1 = __fma_rn(s_r1[t], y, s1);
+                    const double d = s_d[t], zh = s_zh[t], a0 = s_r0[t], a1 = s_r1[t];
+#pragma unroll
+                    for (int q = 0; q < kRowsPerWarp; ++q) {
+                        const double y = zh * rcp_nr((d - rt[q].dorg) - rt[q].tau);
+                        nn[q] = __fma_rn(y, y, nn[q]);
+                        s0[q] = __fma_rn(a0, y, s0[q]);
+                        s1[q] = __fma_rn(a1, y, s1[q]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kRowsPerWarp; ++q) {
+                    if (!rt[q].fast) continue;
+                    const int ks = rt[q].ks;
+                    const double dorg = rt[q].dorg, tau = rt[q].tau;
+                    const int lo = max(ks, tlo), hi = min(ks + rt[q].K, thi);
+                    for (int i = strided_start(lo, ks, lane); i < hi; i += 32) {
+                        const int t = i - tlo;
+                        const double y = s_zh[t] * rcp_nr((s_d[t] - dorg) - tau);
+                        nn[q] = __fma_rn(y, y, nn[q]);
+                        s0[q] = __fma_rn(s_r0[t], y, s0[q]);
+                        s1[q] = __fma_rn(s_r1[t], y, s1[q]);
+                    }
                 }
             }
         }
-        if (rows) {
-            if (!fast) {  // exact redo; a zero delta is an error
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            const WarpRowRoot& R = rt[q];
+            if (!R.rows) continue;
+            if (!R.fast) {  // exact redo; a zero delta is an error
                 bool zero = false;
-                nn = 0.0; s0 = 0.0; s1 = 0.0;
-                for (int i = ks + lane; i < ks + K; i += 32) {
-                    const double del = (w.dA[i] - dorg) - tau;
+                nn[q] = 0.0; s0[q] = 0.0; s1[q] = 0.0;
+                for (int i = R.ks + lane; i < R.ks + R.K; i += 32) {
+                    const double del = (w.dA[i] - R.dorg) - R.tau;
                     zero |= (del == 0.0);
                     const double y = w.zA[i] * __drcp_rn(del);
-                    nn = __fma_rn(y, y, nn);
-                    s0 = __fma_rn(w.r0A[i], y, s0);
-                    s1 = __fma_rn(w.r1A[i], y, s1);
+                    nn[q] = __fma_rn(y, y, nn[q]);
+                    s0[q] = __fma_rn(w.r0A[i], y, s0[q]);
+                    s1[q] = __fma_rn(w.r1A[i], y, s1[q]);
                 }
                 if (__any_sync(0xffffffffu, zero) && lane == 0) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
             }
-            const double NN = bfly_add(nn), S0 = bfly_add(s0), S1 = bfly_add(s1);
+            const double NN = bfly_add(nn[q]), S0 = bfly_add(s0[q]), S1 = bfly_add(s1[q]);
             if (lane == 0) {
                 const double inv = 1.0 / sqrt(NN);
-                w.blo[p] = S0 * inv;
-                w.bhi[p] = S1 * inv;
+                w.blo[R.p] = S0 * inv;
+                w.bhi[R.p] = S1 * inv;
             }
         }
     }
