@@ -22,6 +22,14 @@ namespace brgpu {
 
 constexpr int kWarpThreads = 256;  // 8 warps
 constexpr int kWarpTile = 1024;    // (d, z^2) pairs per tile
+#ifndef BRGPU_SECW_THREADS
+#define BRGPU_SECW_THREADS 256
+#endif
+#ifndef BRGPU_SECW_TILE
+#define BRGPU_SECW_TILE 1024
+#endif
+constexpr int kSecWThreads = BRGPU_SECW_THREADS;  // k_secular_warp: roots in flight per CTA x 32
+constexpr int kSecWTile = BRGPU_SECW_TILE;        // k_secular_warp: (d, z^2) pairs per SMEM tile
 
 __device__ __forceinline__ void merge_active(const Work& w, const LevelDev& L, int m, int& ks, int& ke) {
     const int off = L.mOff[m];
@@ -38,14 +46,14 @@ __device__ __forceinline__ int strided_start(int lo, int ks, int lane) {
 // ---------------------------------------------------------------------------
 // secular roots, one warp per root
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelDev L, int n, int patched) {
+__global__ void __launch_bounds__(kSecWThreads, 512 / kSecWThreads) k_secular_warp(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
-    __shared__ double2 s_tile[2][kWarpTile];
+    __shared__ double2 s_tile[2][kSecWTile];
     __shared__ int s_next;
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int G = (int)gridDim.x;
-    const int R = max(kWarpThreads / 32, (T + G - 1) / G);
+    const int R = max(kSecWThreads / 32, (T + G - 1) / G);
     const int c0 = blockIdx.x * R;
     if (c0 >= T) return;
     const int c1 = min(c0 + R, T);
@@ -97,13 +105,13 @@ __global__ void __launch_bounds__(kWarpThreads, 2) k_secular_warp(Work w, LevelD
         // skips the fast pass and runs the exact one below
         const bool fast = need && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau);
         int buf = 0;
-        for (int i = P0 + (int)threadIdx.x; i < min(P0 + kWarpTile, P1); i += kWarpThreads)
+        for (int i = P0 + (int)threadIdx.x; i < min(P0 + kSecWTile, P1); i += kSecWThreads)
             s_tile[0][i - P0] = make_double2(w.dA[i], w.z2A[i]);
-        for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
-            const int thi = min(tlo + kWarpTile, P1);
+        for (int tlo = P0; tlo < P1; tlo += kSecWTile) {
+            const int thi = min(tlo + kSecWTile, P1);
             __syncthreads();
             if (thi < P1)
-                for (int i = thi + (int)threadIdx.x; i < min(thi + kWarpTile, P1); i += kWarpThreads)
+                for (int i = thi + (int)threadIdx.x; i < min(thi + kSecWTile, P1); i += kSecWThreads)
                     s_tile[buf ^ 1][i - thi] = make_double2(w.dA[i], w.z2A[i]);
             if (fast) {
                 const int lo = max(ks, tlo), hi = min(ks + K, thi);
@@ -477,7 +485,7 @@ constexpr int kWarpRowPerSm = BRGPU_WARP_ROW_PER_SM;
 static int warp_grid(const SolveParams& prm, int per_sm) { return prm.sms * per_sm; }
 
 void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    launch_pdl(k_secular_warp, warp_grid(prm, kWarpSecPerSm), kWarpThreads, 0, s, w, L, n, prm.patched);
+    launch_pdl(k_secular_warp, warp_grid(prm, kWarpSecPerSm), kSecWThreads, 0, s, w, L, n, prm.patched);
 }
 void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
     launch_pdl(k_zhat_warp, warp_grid(prm, kWarpRowPerSm), kWarpThreads, 0, s, w, L, n);
