@@ -43,6 +43,20 @@ __device__ __forceinline__ int strided_start(int lo, int ks, int lane) {
     return lo + r;
 }
 
+// (d, z^2) pairs of poles [a, b) into a shared-memory tile with cp.async: the
+// copies complete in the background (no register round trip, no stall on the
+// global load) and cp_async_wait_all + a barrier publish them.
+__device__ __forceinline__ void tile_fetch(double2* tile, const Work& w, int a, int b) {
+    for (int i = a + (int)threadIdx.x; i < b; i += kSecWThreads) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(tile + (i - a));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(w.dA + i) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u), "l"(w.z2A + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // secular roots, one warp per root
 // ---------------------------------------------------------------------------
@@ -62,6 +76,10 @@ __global__ void __launch_bounds__(kSecWThreads, 512 / kSecWThreads) k_secular_wa
     merge_active(w, L, w.aMerge[c0], P0, tmp);
     merge_active(w, L, w.aMerge[c1 - 1], tmp, P1);
     if (threadIdx.x == 0) s_next = 0;
+    // a window that fits one tile is loaded once for all evaluation rounds;
+    // a larger one streams through the two tiles every round
+    const bool resident = P1 - P0 <= kSecWTile;
+    if (resident) tile_fetch(s_tile[0], w, P0, P1);
     __syncthreads();
     const int lane = threadIdx.x & 31;
 
@@ -105,14 +123,12 @@ __global__ void __launch_bounds__(kSecWThreads, 512 / kSecWThreads) k_secular_wa
         // skips the fast pass and runs the exact one below
         const bool fast = need && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau);
         int buf = 0;
-        for (int i = P0 + (int)threadIdx.x; i < min(P0 + kSecWTile, P1); i += kSecWThreads)
-            s_tile[0][i - P0] = make_double2(w.dA[i], w.z2A[i]);
+        if (!resident) tile_fetch(s_tile[0], w, P0, min(P0 + kSecWTile, P1));
         for (int tlo = P0; tlo < P1; tlo += kSecWTile) {
             const int thi = min(tlo + kSecWTile, P1);
+            cp_async_wait_all();
             __syncthreads();
-            if (thi < P1)
-                for (int i = thi + (int)threadIdx.x; i < min(thi + kSecWTile, P1); i += kSecWThreads)
-                    s_tile[buf ^ 1][i - thi] = make_double2(w.dA[i], w.z2A[i]);
+            if (thi < P1) tile_fetch(s_tile[buf ^ 1], w, thi, min(thi + kSecWTile, P1));
             if (fast) {
                 const int lo = max(ks, tlo), hi = min(ks + K, thi);
                 const double2* __restrict__ tp = s_tile[buf] - tlo;
