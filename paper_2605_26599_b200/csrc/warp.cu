@@ -25,6 +25,9 @@ constexpr int kWarpTile = 1024;    // (d, z^2) pairs per tile
 #ifndef BRGPU_SECW_THREADS
 #define BRGPU_SECW_THREADS 256
 #endif
+#ifndef BRGPU_SECW_MINB
+#define BRGPU_SECW_MINB 3  // CTAs per SM: 80 registers, no spills (2: 107 registers, C3 +1%)
+#endif
 #ifndef BRGPU_SECW_TILE
 #define BRGPU_SECW_TILE 1024
 #endif
@@ -60,7 +63,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------------------
 // secular roots, one warp per root
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSecWThreads, 512 / kSecWThreads) k_secular_warp(Work w, LevelDev L, int n, int patched) {
+__global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
     __shared__ double2 s_tile[2][kSecWTile];
     __shared__ int s_next;
