@@ -53,6 +53,7 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int ngroups, const int2* tab,
                          const SolveParams& prm, int* launches, Prof* prof);
 void init_fused_attributes();
+void init_warp_attributes();
 #ifndef BRGPU_FUSE_MAX_ELEMS
 #define BRGPU_FUSE_MAX_ELEMS 1024
 #endif
@@ -1159,6 +1160,7 @@ int brgpu_create(brgpu_handle** out, int device) {
     }
     brgpu::init_kernel_attributes();
     brgpu::init_fused_attributes();
+    brgpu::init_warp_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
     *out = hh;

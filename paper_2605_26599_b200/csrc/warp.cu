@@ -29,7 +29,7 @@ constexpr int kWarpTile = 1024;    // (d, z^2) pairs per tile
 #define BRGPU_SECW_MINB 3  // CTAs per SM: 80 registers, no spills (2: 107 registers, C3 +1%)
 #endif
 #ifndef BRGPU_SECW_TILE
-#define BRGPU_SECW_TILE 1024
+#define BRGPU_SECW_TILE 2048  // 2 x 32 KB dynamic SMEM per CTA, 3 CTAs per SM
 #endif
 constexpr int kSecWThreads = BRGPU_SECW_THREADS;  // k_secular_warp: roots in flight per CTA x 32
 constexpr int kSecWTile = BRGPU_SECW_TILE;        // k_secular_warp: (d, z^2) pairs per SMEM tile
@@ -65,7 +65,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
-    __shared__ double2 s_tile[2][kSecWTile];
+    extern __shared__ __align__(16) double2 s_tiles[];  // two tiles of kSecWTile pairs (dynamic)
     __shared__ int s_next;
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(
     // a window that fits one tile is loaded once for all evaluation rounds;
     // a larger one streams through the two tiles every round
     const bool resident = P1 - P0 <= kSecWTile;
-    if (resident) tile_fetch(s_tile[0], w, P0, P1);
+    if (resident) tile_fetch(s_tiles, w, P0, P1);
     __syncthreads();
     const int lane = threadIdx.x & 31;
 
@@ -126,15 +126,15 @@ __global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(
         // skips the fast pass and runs the exact one below
         const bool fast = need && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau);
         int buf = 0;
-        if (!resident) tile_fetch(s_tile[0], w, P0, min(P0 + kSecWTile, P1));
+        if (!resident) tile_fetch(s_tiles, w, P0, min(P0 + kSecWTile, P1));
         for (int tlo = P0; tlo < P1; tlo += kSecWTile) {
             const int thi = min(tlo + kSecWTile, P1);
             cp_async_wait_all();
             __syncthreads();
-            if (thi < P1) tile_fetch(s_tile[buf ^ 1], w, thi, min(thi + kSecWTile, P1));
+            if (thi < P1) tile_fetch(s_tiles + (buf ^ 1) * kSecWTile, w, thi, min(thi + kSecWTile, P1));
             if (fast) {
                 const int lo = max(ks, tlo), hi = min(ks + K, thi);
-                const double2* __restrict__ tp = s_tile[buf] - tlo;
+                const double2* __restrict__ tp = s_tiles + buf * kSecWTile - tlo;
                 // terms i <= j, then the prefix snapshot, then i > j: a lane's
                 // strided terms are split at one point, so the two loops differ
                 // across lanes by at most one trip (no per-term snapshot selects)
@@ -503,8 +503,14 @@ constexpr int kWarpSecPerSm = BRGPU_WARP_SEC_PER_SM;
 constexpr int kWarpRowPerSm = BRGPU_WARP_ROW_PER_SM;
 static int warp_grid(const SolveParams& prm, int per_sm) { return prm.sms * per_sm; }
 
+constexpr size_t kSecWSmem = 2 * kSecWTile * sizeof(double2);
+
+void init_warp_attributes() {
+    cudaFuncSetAttribute(k_secular_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSecWSmem);
+}
+
 void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    launch_pdl(k_secular_warp, warp_grid(prm, kWarpSecPerSm), kSecWThreads, 0, s, w, L, n, prm.patched);
+    launch_pdl(k_secular_warp, warp_grid(prm, kWarpSecPerSm), kSecWThreads, kSecWSmem, s, w, L, n, prm.patched);
 }
 void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
     launch_pdl(k_zhat_warp, warp_grid(prm, kWarpRowPerSm), kWarpThreads, 0, s, w, L, n);
