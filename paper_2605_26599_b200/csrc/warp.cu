@@ -356,6 +356,22 @@ __global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, 
 #define BRGPU_ROWS_PER_WARP 2
 #endif
 constexpr int kRowsPerWarp = BRGPU_ROWS_PER_WARP;  // roots per warp in k_rows_warp
+#ifndef BRGPU_ROWS_TILE
+#define BRGPU_ROWS_TILE 512
+#endif
+constexpr int kRowsTile = BRGPU_ROWS_TILE;  // poles per k_rows_warp tile (2 buffers x 4 arrays: 32 KB)
+
+__device__ __forceinline__ void rows_fetch(double (*tile)[kRowsTile], const Work& w, int a, int b) {
+    for (int i = a + (int)threadIdx.x; i < b; i += kWarpThreads) {
+        const double* src[4] = {w.dA + i, w.zA + i, w.r0A + i, w.r1A + i};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(&tile[c][i - a]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src[c]) : "memory");
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 // One root of k_rows_warp.
 struct WarpRowRoot {
@@ -372,7 +388,9 @@ struct WarpRowRoot {
 // one root per warp.
 __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
     pdl_entry();
-    __shared__ double s_d[kWarpTile], s_zh[kWarpTile], s_r0[kWarpTile], s_r1[kWarpTile];
+    // two buffers of (d, zhat, r0, r1) tiles: the next tile streams in by
+    // cp.async while the current one is consumed
+    __shared__ __align__(16) double s_rt[2][4][kRowsTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -422,16 +440,17 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
             nn[q] = 0.0; s0[q] = 0.0; s1[q] = 0.0;
             shared = shared && rt[q].fast && rt[q].ks == rt[0].ks;
         }
-        for (int tlo = P0; tlo < P1; tlo += kWarpTile) {
-            const int thi = min(tlo + kWarpTile, P1);
+        int buf = 0;
+        rows_fetch(s_rt[0], w, P0, min(P0 + kRowsTile, P1));
+        for (int tlo = P0; tlo < P1; tlo += kRowsTile) {
+            const int thi = min(tlo + kRowsTile, P1);
+            cp_async_wait_all();
             __syncthreads();
-            for (int r = tlo + (int)threadIdx.x; r < thi; r += kWarpThreads) {
-                s_d[r - tlo] = w.dA[r];
-                s_zh[r - tlo] = w.zA[r];
-                s_r0[r - tlo] = w.r0A[r];
-                s_r1[r - tlo] = w.r1A[r];
-            }
-            __syncthreads();
+            if (thi < P1) rows_fetch(s_rt[buf ^ 1], w, thi, min(thi + kRowsTile, P1));
+            const double* __restrict__ s_d = s_rt[buf][0];
+            const double* __restrict__ s_zh = s_rt[buf][1];
+            const double* __restrict__ s_r0 = s_rt[buf][2];
+            const double* __restrict__ s_r1 = s_rt[buf][3];
             if (shared) {
                 const int ks = rt[0].ks;
                 const int lo = max(ks, tlo), hi = min(ks + rt[0].K, thi);
@@ -463,7 +482,9 @@ __global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, 
                     }
                 }
             }
+            buf ^= 1;
         }
+        __syncthreads();  // the last tile is consumed before the next step's prefetch
 #pragma unroll
         for (int q = 0; q < kRowsPerWarp; ++q) {
             const WarpRowRoot& R = rt[q];
