@@ -282,15 +282,23 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(int ntask, const int* __r
     r1[m - 1] = 1.0;
     const int st = values_only ? steqr_leaf<false>(m, d, e, r0, r1) : steqr_leaf<true>(m, d, e, r0, r1);
     if (st) set_status(status, st);
-    // stable ascending sort (qrql.cpp:348-364): rank = #{d_j < d_i} + #{j<i: d_j == d_i}
-    for (int i = 0; i < m; ++i) {
-        const double di = d[i];
-        int rank = 0;
-        for (int j = 0; j < m; ++j) rank += (d[j] < di) || (j < i && d[j] == di);
-        lam[off + rank] = di;
-        if (!values_only) {
-            blo[off + rank] = r0[i];
-            bhi[off + rank] = r1[i];
+    // stable ascending sort (qrql.cpp:348-364): rank = #{d_j < d_i} + #{j<i: d_j == d_i},
+    // on a register copy of the eigenvalues (unrolled; entries j >= m never count)
+    double dv[MAXM];
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j) dv[j] = j < m ? d[j] : 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXM; ++i) {
+        if (i < m) {
+            const double di = dv[i];
+            int rank = 0;
+#pragma unroll
+            for (int j = 0; j < MAXM; ++j) rank += j < m && ((dv[j] < di) || (j < i && dv[j] == di));
+            lam[off + rank] = di;
+            if (!values_only) {
+                blo[off + rank] = r0[i];
+                bhi[off + rank] = r1[i];
+            }
         }
     }
 }
