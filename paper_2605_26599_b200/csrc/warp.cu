@@ -221,7 +221,10 @@ struct WarpZhatPole {
 // tau, d_j: 24 B per term), which halves the SMEM traffic per FP64 term at 2
 // poles per warp.  Each pole keeps its lane-strided product order and the
 // butterfly, so results are bitwise those of one pole per warp.
-__global__ void __launch_bounds__(kWarpThreads) k_zhat_warp(Work w, LevelDev L, int n) {
+#ifndef BRGPU_ZHAT_MINB
+#define BRGPU_ZHAT_MINB 5  // CTAs per SM (48 registers): C3 zhat 2.97 -> 2.91 ms
+#endif
+__global__ void __launch_bounds__(kWarpThreads, BRGPU_ZHAT_MINB) k_zhat_warp(Work w, LevelDev L, int n) {
     pdl_entry();
     __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
@@ -386,7 +389,10 @@ struct WarpRowRoot {
 // 5.5 FP64-issue cycles and was SMEM-bound).  Each root keeps its own lane-
 // strided accumulation order and butterfly, so results are bitwise those of
 // one root per warp.
-__global__ void __launch_bounds__(kWarpThreads) k_rows_warp(Work w, LevelDev L, int n) {
+#ifndef BRGPU_ROWS_MINB
+#define BRGPU_ROWS_MINB 4  // CTAs per SM (64 registers): C3 rows 3.14 -> 3.02 ms
+#endif
+__global__ void __launch_bounds__(kWarpThreads, BRGPU_ROWS_MINB) k_rows_warp(Work w, LevelDev L, int n) {
     pdl_entry();
     // two buffers of (d, zhat, r0, r1) tiles: the next tile streams in by
     // cp.async while the current one is consumed
