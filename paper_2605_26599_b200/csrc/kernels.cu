@@ -1113,7 +1113,7 @@ static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 void launch_secular_tiled(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                           const SolveParams& prm);
-void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
+int launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
 void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
 void launch_rows_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm);
 
@@ -1276,8 +1276,7 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
             launch_secular_tiled(s, w, L, n, prm);
             nl += 3;
         }
-        launch_secular_warp(s, w, L, n, prm);
-        nl += 1;
+        nl += launch_secular_warp(s, w, L, n, prm);
         if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
         PMARK(BRGPU_K_SECULAR);
     } else if (part == 1) {

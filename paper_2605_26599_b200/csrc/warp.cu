@@ -63,14 +63,72 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // ---------------------------------------------------------------------------
 // secular roots, one warp per root
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(Work w, LevelDev L, int n, int patched) {
+#ifndef BRGPU_SECW_SLOTS
+#define BRGPU_SECW_SLOTS 2
+#endif
+#ifndef BRGPU_SECW2_MINB
+#define BRGPU_SECW2_MINB 2
+#endif
+constexpr int kSecWSlots = BRGPU_SECW_SLOTS;  // roots per warp in k_secular_warp (large-K levels)
+#ifndef BRGPU_SECW2_MIN_ROOTS
+#define BRGPU_SECW2_MIN_ROOTS 16384
+#endif
+constexpr int kSecW2MinRoots = kSecWSlots == 1 ? 0x7fffffff : BRGPU_SECW2_MIN_ROOTS;
+
+// Partial sums of one root's evaluation (lane-strided terms, split at the
+// root's own index for the prefix snapshot).
+struct SecAcc {
+    double sum, sum_d, psi, psum;
+};
+
+__device__ __forceinline__ void sec_terms(const double2* __restrict__ tp, int& i, int stop, double dorg, double tau,
+                                          SecAcc& A) {
+#pragma unroll 4
+    for (; i < stop; i += 32) {
+        const double2 dz = tp[i];
+        const double r = rcp_nr((dz.x - dorg) - tau);
+        const double t = dz.y * r;
+        A.sum += t;
+        A.sum_d = __fma_rn(t, r, A.sum_d);
+    }
+}
+
+// Two roots of one merge: each (d, z^2) pair read from shared memory feeds
+// both (half the SMEM traffic and barriers per root; 2 x 8 roots in flight per
+// CTA).  Per root the terms and their order are those of sec_terms.
+__device__ __forceinline__ void sec_terms2(const double2* __restrict__ tp, int& i, int stop, double dorg0,
+                                           double tau0, double dorg1, double tau1, SecAcc& A, SecAcc& B) {
+#pragma unroll 2
+    for (; i < stop; i += 32) {
+        const double2 dz = tp[i];
+        const double r0 = rcp_nr((dz.x - dorg0) - tau0);
+        const double r1 = rcp_nr((dz.x - dorg1) - tau1);
+        const double t0 = dz.y * r0, t1 = dz.y * r1;
+        A.sum += t0;
+        A.sum_d = __fma_rn(t0, r0, A.sum_d);
+        B.sum += t1;
+        B.sum_d = __fma_rn(t1, r1, B.sum_d);
+    }
+}
+
+// Secular roots, kSecWSlots roots per warp (split arithmetic: lane-strided
+// terms + xor butterfly, bitwise the checker's BRO_SPLIT evaluation).  A CTA
+// owns a chunk of roots and a CTA queue; every evaluation round streams the
+// chunk's pole window through shared memory once for all its warps' roots.
+template <int NS>
+__global__ void __launch_bounds__(kSecWThreads, NS == 1 ? BRGPU_SECW_MINB : BRGPU_SECW2_MINB)
+k_secular_warp(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
     extern __shared__ __align__(16) double2 s_tiles[];  // two tiles of kSecWTile pairs (dynamic)
     __shared__ int s_next;
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
+    // the second root slot of a warp is used only on large-K levels (Toeplitz /
+    // glued Wilkinson tops: half the SMEM traffic and barriers per root); on a
+    // level with few roots one root per warp keeps more warps busy
+    const int nsl = T < kSecW2MinRoots ? 1 : NS;
     const int G = (int)gridDim.x;
-    const int R = max(kSecWThreads / 32, (T + G - 1) / G);
+    const int R = max(kSecWThreads / 32 * nsl, (T + G - 1) / G);
     const int c0 = blockIdx.x * R;
     if (c0 >= T) return;
     const int c1 = min(c0 + R, T);
@@ -86,45 +144,58 @@ __global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(
     __syncthreads();
     const int lane = threadIdx.x & 31;
 
-    RootSM st;
-    int g = -1, ks = 0;
+    RootSM st[NS];
+    int g[NS], ks[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) { g[q] = -1; ks[q] = 0; }
     bool exhausted = false;
     unsigned long long evals = 0, terms = 0;
     for (;;) {
-        while (g < 0 && !exhausted) {
-            int q = 0;
-            if (lane == 0) q = atomicAdd(&s_next, 1);
-            q = __shfl_sync(0xffffffffu, q, 0);
-            if (c0 + q >= c1) { exhausted = true; break; }
-            const int gg = c0 + q;
-            if (!owns(w, gg)) continue;  // another rank's root (root-range split)
-            const int m = w.aMerge[gg];
-            int ke;
-            merge_active(w, L, m, ks, ke);
-            if (!split_mode(L.mSize[m], ke - ks)) continue;  // lane-per-root tier owns it
-            g = gg;
-            const int K = ke - ks, j = g - ks;
-            const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
-            double zsq = 0.0;
-            if (j == K - 1 && K > 1) {
-                for (int i = ks + lane; i < ke; i += 32) zsq += w.z2A[i];
-                zsq = bfly_add(zsq);
-            }
-            rs_begin_zsq(st, K, j, rho, PolesPtr{w.dA + ks}, w.zA[ks], zsq, w.z2A[ks + K - 1]);
-            if (st.phase == kRsDone) {
-                if (lane == 0) { w.org[g] = st.org; w.tau[g] = st.tau; }
-                g = -1;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            while (g[q] < 0 && !exhausted && q < nsl) {
+                int qq = 0;
+                if (lane == 0) qq = atomicAdd(&s_next, 1);
+                qq = __shfl_sync(0xffffffffu, qq, 0);
+                if (c0 + qq >= c1) { exhausted = true; break; }
+                const int gg = c0 + qq;
+                if (!owns(w, gg)) continue;  // another rank's root (root-range split)
+                const int m = w.aMerge[gg];
+                int ke;
+                merge_active(w, L, m, ks[q], ke);
+                if (!split_mode(L.mSize[m], ke - ks[q])) continue;  // lane-per-root tier owns it
+                g[q] = gg;
+                const int K = ke - ks[q], j = gg - ks[q];
+                const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+                double zsq = 0.0;
+                if (j == K - 1 && K > 1) {
+                    for (int i = ks[q] + lane; i < ke; i += 32) zsq += w.z2A[i];
+                    zsq = bfly_add(zsq);
+                }
+                rs_begin_zsq(st[q], K, j, rho, PolesPtr{w.dA + ks[q]}, w.zA[ks[q]], zsq, w.z2A[ks[q] + K - 1]);
+                if (st[q].phase == kRsDone) {
+                    if (lane == 0) { w.org[gg] = st[q].org; w.tau[gg] = st[q].tau; }
+                    g[q] = -1;
+                }
             }
         }
-        const bool need = g >= 0;
-        if (!__syncthreads_or(need)) break;
-        double sum = 0.0, sum_d = 0.0, psi = 0.0, psum = 0.0;
-        const int K = need ? st.K : 0;
-        const int j = st.j;
-        const double dorg = st.dorg, tau = st.tau;
-        // neighbour range guard (eval_guard, numerics.cuh); on failure the warp
-        // skips the fast pass and runs the exact one below
-        const bool fast = need && !w.exact && eval_guard(GlobalPairs{w.dA + ks, w.z2A + ks}, K, j, dorg, tau);
+        bool need[NS], fast[NS];
+        SecAcc acc[NS];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            need[q] = g[q] >= 0;
+            any = any || need[q];
+            acc[q] = SecAcc{0.0, 0.0, 0.0, 0.0};
+            // neighbour range guard (eval_guard, numerics.cuh); on failure the
+            // root skips the fast pass and runs the exact one below
+            fast[q] = need[q] && !w.exact &&
+                      eval_guard(GlobalPairs{w.dA + ks[q], w.z2A + ks[q]}, st[q].K, st[q].j, st[q].dorg, st[q].tau);
+        }
+        if (!__syncthreads_or(any)) break;
+        // both roots fast and in one merge: one pass over the shared pole range,
+        // split at both roots' own indices (prefix snapshots)
+        const bool pair = NS == 2 && fast[0] && fast[NS - 1] && ks[0] == ks[NS - 1];
         int buf = 0;
         if (!resident) tile_fetch(s_tiles, w, P0, min(P0 + kSecWTile, P1));
         for (int tlo = P0; tlo < P1; tlo += kSecWTile) {
@@ -132,68 +203,78 @@ __global__ void __launch_bounds__(kSecWThreads, BRGPU_SECW_MINB) k_secular_warp(
             cp_async_wait_all();
             __syncthreads();
             if (thi < P1) tile_fetch(s_tiles + (buf ^ 1) * kSecWTile, w, thi, min(thi + kSecWTile, P1));
-            if (fast) {
-                const int lo = max(ks, tlo), hi = min(ks + K, thi);
-                const double2* __restrict__ tp = s_tiles + buf * kSecWTile - tlo;
-                // terms i <= j, then the prefix snapshot, then i > j: a lane's
-                // strided terms are split at one point, so the two loops differ
-                // across lanes by at most one trip (no per-term snapshot selects)
-                const int mid = min(hi, ks + j + 1);
-                int i = strided_start(lo, ks, lane);
-#pragma unroll 4
-                for (; i < mid; i += 32) {
-                    const double2 dz = tp[i];
-                    const double r = rcp_nr((dz.x - dorg) - tau);
-                    const double t = dz.y * r;
-                    sum += t;
-                    sum_d = __fma_rn(t, r, sum_d);
-                }
-                if (lo < mid) { psi = sum_d; psum = sum; }
-#pragma unroll 4
-                for (; i < hi; i += 32) {
-                    const double2 dz = tp[i];
-                    const double r = rcp_nr((dz.x - dorg) - tau);
-                    const double t = dz.y * r;
-                    sum += t;
-                    sum_d = __fma_rn(t, r, sum_d);
+            const double2* __restrict__ tp = s_tiles + buf * kSecWTile - tlo;
+            if (pair) {
+                SecAcc& A = acc[0];
+                SecAcc& B = acc[NS - 1];
+                const int k0 = ks[0];
+                const int lo = max(k0, tlo), hi = min(k0 + st[0].K, thi);
+                const int m0 = min(hi, k0 + st[0].j + 1), m1 = min(hi, k0 + st[NS - 1].j + 1);
+                const int midA = min(m0, m1), midB = max(m0, m1);
+                const double d0 = st[0].dorg, t0 = st[0].tau, d1 = st[NS - 1].dorg, t1 = st[NS - 1].tau;
+                int i = strided_start(lo, k0, lane);
+                sec_terms2(tp, i, midA, d0, t0, d1, t1, A, B);
+                if (lo < m0 && m0 == midA) { A.psi = A.sum_d; A.psum = A.sum; }
+                if (lo < m1 && m1 == midA) { B.psi = B.sum_d; B.psum = B.sum; }
+                sec_terms2(tp, i, midB, d0, t0, d1, t1, A, B);
+                if (lo < m0 && m0 != midA) { A.psi = A.sum_d; A.psum = A.sum; }
+                if (lo < m1 && m1 != midA) { B.psi = B.sum_d; B.psum = B.sum; }
+                sec_terms2(tp, i, hi, d0, t0, d1, t1, A, B);
+            } else {
+#pragma unroll
+                for (int q = 0; q < NS; ++q) {
+                    if (!fast[q]) continue;
+                    // terms i <= j, then the prefix snapshot, then i > j: a lane's
+                    // strided terms are split at one point (no per-term selects)
+                    const int lo = max(ks[q], tlo), hi = min(ks[q] + st[q].K, thi);
+                    const int mid = min(hi, ks[q] + st[q].j + 1);
+                    int i = strided_start(lo, ks[q], lane);
+                    sec_terms(tp, i, mid, st[q].dorg, st[q].tau, acc[q]);
+                    if (lo < mid) { acc[q].psi = acc[q].sum_d; acc[q].psum = acc[q].sum; }
+                    sec_terms(tp, i, hi, st[q].dorg, st[q].tau, acc[q]);
                 }
             }
             buf ^= 1;
         }
         __syncthreads();
-        if (need) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            if (!need[q]) continue;
+            RootSM& S = st[q];
+            const int K = S.K, j = S.j;
             bool pole = false;
-            if (!fast) {  // rare: exact strided pass from global memory
-                sum = 0.0; sum_d = 0.0; psi = 0.0; psum = 0.0;
-                for (int i = ks + lane; i < ks + K; i += 32) {
-                    const double del = (w.dA[i] - dorg) - tau;
+            if (!fast[q]) {  // rare: exact strided pass from global memory
+                SecAcc& A = acc[q];
+                A = SecAcc{0.0, 0.0, 0.0, 0.0};
+                for (int i = ks[q] + lane; i < ks[q] + K; i += 32) {
+                    const double del = (w.dA[i] - S.dorg) - S.tau;
                     pole |= (del == 0.0);
                     const double r = __drcp_rn(del);
                     const double t = w.z2A[i] * r;
-                    sum += t;
-                    sum_d = __fma_rn(t, r, sum_d);
-                    if (i - ks <= j) { psi = sum_d; psum = sum; }
+                    A.sum += t;
+                    A.sum_d = __fma_rn(t, r, A.sum_d);
+                    if (i - ks[q] <= j) { A.psi = A.sum_d; A.psum = A.sum; }
                 }
                 pole = __any_sync(0xffffffffu, pole);
             }
-            const double S = bfly_add(sum), SD = bfly_add(sum_d);
-            const double PS = bfly_add(psi), PU = bfly_add(psum);
+            const double Sm = bfly_add(acc[q].sum), SD = bfly_add(acc[q].sum_d);
+            const double PS = bfly_add(acc[q].psi), PU = bfly_add(acc[q].psum);
             Ev ev;
-            ev.f = 1.0 + st.rho * S;
-            ev.fp = st.rho * SD;
-            ev.abs_sum = st.rho * (S - 2.0 * PU);
-            ev.psi = st.rho * PS;
+            ev.f = 1.0 + S.rho * Sm;
+            ev.fp = S.rho * SD;
+            ev.abs_sum = S.rho * (Sm - 2.0 * PU);
+            ev.psi = S.rho * PS;
             ev.pole = pole;
             ++evals;
             terms += (unsigned long long)K;
-            rs_consume(st, ev, PolesPtr{w.dA + ks}, Z2Ptr{w.z2A + ks}, patched != 0);
-            if (st.phase == kRsDone || st.phase == kRsFail) {
+            rs_consume(S, ev, PolesPtr{w.dA + ks[q]}, Z2Ptr{w.z2A + ks[q]}, patched != 0);
+            if (S.phase == kRsDone || S.phase == kRsFail) {
                 if (lane == 0) {
-                    if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
-                    w.org[g] = st.org;
-                    w.tau[g] = st.tau;
+                    if (S.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                    w.org[g[q]] = S.org;
+                    w.tau[g[q]] = S.tau;
                 }
-                g = -1;
+                g[q] = -1;
             }
         }
     }
@@ -533,11 +614,13 @@ static int warp_grid(const SolveParams& prm, int per_sm) { return prm.sms * per_
 constexpr size_t kSecWSmem = 2 * kSecWTile * sizeof(double2);
 
 void init_warp_attributes() {
-    cudaFuncSetAttribute(k_secular_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSecWSmem);
+    cudaFuncSetAttribute(k_secular_warp<kSecWSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSecWSmem);
 }
 
-void launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
-    launch_pdl(k_secular_warp, warp_grid(prm, kWarpSecPerSm), kSecWThreads, kSecWSmem, s, w, L, n, prm.patched);
+int launch_secular_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
+    launch_pdl(k_secular_warp<kSecWSlots>, warp_grid(prm, kWarpSecPerSm), kSecWThreads, kSecWSmem, s, w, L, n,
+               prm.patched);
+    return 1;
 }
 void launch_zhat_warp(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm) {
     launch_pdl(k_zhat_warp, warp_grid(prm, kWarpRowPerSm), kWarpThreads, 0, s, w, L, n);
