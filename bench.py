@@ -295,6 +295,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
         e2e_call()
         e2e.append(time.perf_counter() - t0)
     e2e_s = statistics.mean(e2e)
+    if os.environ.get("BENCH_DEBUG"):
+        print("e2e samples ms:", " ".join(f"{x * 1e3:.3f}" for x in e2e), file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
