@@ -58,7 +58,8 @@ void init_warp_attributes();
 #define BRGPU_FUSE_MAX_ELEMS 1024
 #endif
 constexpr int kFuseMaxElems = BRGPU_FUSE_MAX_ELEMS;
-constexpr int kGridMinN = 32768;  // below this order, underfilled 1024-shape levels stay fused  // largest merge of a fused SMEM level (512 or 1024)
+constexpr int kGridMinN = 32768;  // below this order, underfilled 1024-shape levels stay fused
+constexpr int kGridManyPerSm = 4;  // 1024-shape levels with >= 4 merges per SM run on the grid tier  // largest merge of a fused SMEM level (512 or 1024)
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
 #ifndef BRGPU_SPLIT_MIN_SIZE
 #define BRGPU_SPLIT_MIN_SIZE 8192
@@ -302,7 +303,12 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         // (A/B: Toeplitz 2^16 20.7 -> 20.1 ms; glued Wilkinson 2^18, 256 merges,
         // and n = 4096 stay fused).
         const bool underfilled = maxSize > kFuseSmallElems && L.M < p->sms && p->n >= kGridMinN;
-        L.fused = fuse && maxSize <= kFuseMaxElems && !underfilled;
+        // ... and with many merges (>= 4 per SM: the 1024-shape launch runs in
+        // several waves of 2 CTAs per SM) the grid tier's full-GPU kernels win
+        // too (A/B: random 2^20 4.59 -> 4.57 ms, 4096 x 1024 batch 12.30 -> 12.12 ms;
+        // glued Wilkinson 2^18 with 256 merges stays fused).
+        const bool many = maxSize > kFuseSmallElems && L.M >= kGridManyPerSm * p->sms && p->n >= kGridMinN;
+        L.fused = fuse && maxSize <= kFuseMaxElems && !underfilled && !many;
         L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
         L.G = 0;
