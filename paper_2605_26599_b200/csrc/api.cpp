@@ -59,7 +59,11 @@ void init_warp_attributes();
 #endif
 constexpr int kFuseMaxElems = BRGPU_FUSE_MAX_ELEMS;
 constexpr int kGridMinN = 32768;  // below this order, underfilled 1024-shape levels stay fused
-constexpr int kGridManyPerSm = 4;  // 1024-shape levels with >= 4 merges per SM run on the grid tier  // largest merge of a fused SMEM level (512 or 1024)
+constexpr int kGridManyPerSm = 4;  // 1024-shape levels with >= 4 merges per SM run on the grid tier
+#ifndef BRGPU_GRID_MANY_MIN_SIZE
+#define BRGPU_GRID_MANY_MIN_SIZE 128
+#endif
+constexpr int kGridManyMinSize = BRGPU_GRID_MANY_MIN_SIZE;  // ... when their merges exceed this size  // largest merge of a fused SMEM level (512 or 1024)
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
 #ifndef BRGPU_SPLIT_MIN_SIZE
 #define BRGPU_SPLIT_MIN_SIZE 8192
@@ -303,11 +307,14 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         // (A/B: Toeplitz 2^16 20.7 -> 20.1 ms; glued Wilkinson 2^18, 256 merges,
         // and n = 4096 stay fused).
         const bool underfilled = maxSize > kFuseSmallElems && L.M < p->sms && p->n >= kGridMinN;
-        // ... and with many merges (>= 4 per SM: the 1024-shape launch runs in
-        // several waves of 2 CTAs per SM) the grid tier's full-GPU kernels win
-        // too (A/B: random 2^20 4.59 -> 4.57 ms, 4096 x 1024 batch 12.30 -> 12.12 ms;
-        // glued Wilkinson 2^18 with 256 merges stays fused).
-        const bool many = maxSize > kFuseSmallElems && L.M >= kGridManyPerSm * p->sms && p->n >= kGridMinN;
+        // ... and a level of many merges (>= 4 per SM) larger than 128 runs on
+        // the grid tier too: its lane-per-root secular kernel packs the roots
+        // of all merges onto full warps, where a fused CTA holds only K ~ 100-140
+        // roots of one or two merges for its 256 lanes (A/B, levels 4-6 on the
+        // grid tier: random 2^20 4.59 -> 4.52 ms, 4096 x 1024 batch 12.30 ->
+        // 11.66 ms; glued Wilkinson 2^18 8.04 -> 8.15 ms, its few-root level 4
+        // prefers the fused tier; merges <= 128 stay fused everywhere).
+        const bool many = maxSize > kGridManyMinSize && L.M >= kGridManyPerSm * p->sms && p->n >= kGridMinN;
         L.fused = fuse && maxSize <= kFuseMaxElems && !underfilled && !many;
         L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
