@@ -774,12 +774,18 @@ constexpr int kSecWinQ = BRGPU_SEC_WIN;
 #ifndef BRGPU_SEC_MINB
 #define BRGPU_SEC_MINB 6
 #endif
+#ifndef BRGPU_SEC_MINB_SMALL
+#define BRGPU_SEC_MINB_SMALL 4
+#endif
+constexpr int kSecMinbSmall = BRGPU_SEC_MINB_SMALL;  // k_secular CTAs per SM below kSecBigLevel elements
+constexpr int kSecBigLevel = 1 << 21;
 // Secular roots (secular.cpp:80-241, tau-relative stop when patched).
 // A CTA owns a chunk of roots; each lane runs one root's iteration as a
 // resumable state machine (RootSM) and pulls the next root from a CTA queue
 // as soon as its root converges.  Evaluations are branch-free pole loops over
 // shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
-__global__ void __launch_bounds__(kSecBlock, BRGPU_SEC_MINB) k_secular(Work w, LevelDev L, int n, int patched) {
+template <int MINB>
+__global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ double2 s_snap[kSecBlock];
@@ -1272,8 +1278,19 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         nl += 4;
         if (lane_tier) {
             launch_pdl(k_level_modes, cdiv(L.M, 256), 256, 0, s, w, L);
-            launch_pdl(k_secular, prm.sec_grid, kSecBlock, 0, s, w, L, n, prm.patched);
-            launch_secular_tiled(s, w, L, n, prm);
+            // CTAs per SM (= the launch bounds' minimum and the grid): 4 on levels up to
+            // 2M elements (random 2^20 4.52 -> 4.46 ms), 6 on larger batched levels
+            // (4096 x 1024: 12.12 -> 11.67 ms at 6)
+            // (k_secular_tiled takes the same chunks: same grid)
+            SolveParams ps = prm;
+            if (n >= kSecBigLevel) {
+                ps.sec_grid = prm.sms * BRGPU_SEC_MINB;
+                launch_pdl(k_secular<BRGPU_SEC_MINB>, ps.sec_grid, kSecBlock, 0, s, w, L, n, prm.patched);
+            } else {
+                ps.sec_grid = prm.sms * kSecMinbSmall;
+                launch_pdl(k_secular<kSecMinbSmall>, ps.sec_grid, kSecBlock, 0, s, w, L, n, prm.patched);
+            }
+            launch_secular_tiled(s, w, L, n, ps);
             nl += 3;
         }
         nl += launch_secular_warp(s, w, L, n, prm);
