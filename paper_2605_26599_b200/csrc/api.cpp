@@ -314,7 +314,10 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         // grid tier: random 2^20 4.59 -> 4.52 ms, 4096 x 1024 batch 12.30 ->
         // 11.66 ms; glued Wilkinson 2^18 8.04 -> 8.15 ms, its few-root level 4
         // prefers the fused tier; merges <= 128 stay fused everywhere).
-        const bool many = maxSize > kGridManyMinSize && L.M >= kGridManyPerSm * p->sms && p->n >= kGridMinN;
+        // 512-shape levels (4 CTAs per SM) need twice as many merges (glued
+        // Wilkinson 2^18, level 4 with 1024 merges: 8.11 -> 7.99 ms fused)
+        const int perSm = maxSize > kFuseSmallElems ? kGridManyPerSm : 2 * kGridManyPerSm;
+        const bool many = maxSize > kGridManyMinSize && L.M >= perSm * p->sms && p->n >= kGridMinN;
         L.fused = fuse && maxSize <= kFuseMaxElems && !underfilled && !many;
         L.cap = maxSize <= kFuseSmallElems ? kFuseSmallElems : kFuseMaxElems;
         L.g0 = (int)p->gFirst.size();
