@@ -1251,6 +1251,9 @@ void launch_sigma_stage(cudaStream_t s, const Work& w, const LevelDev& L, const 
 void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
                        int part, int* launches, Prof* prof) {
     const bool lane_tier = !L.allSplit;  // all merges > kSplitMinSize: warp tier only
+    // merges of at most kSplitMinK elements can never reach the split rule
+    // (size > kSplitMinSize or K > kSplitMinK): no warp-tier launches
+    const bool warp_tier = L.maxSize > kSplitMinK;
     const bool x = prm.xsplit != 0;
     const int xg = cdiv(prm.xc, 256), xu = cdiv(prm.xc * w.own_P, 256);
     int nl = 0;
@@ -1293,15 +1296,14 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
             launch_secular_tiled(s, w, L, n, ps);
             nl += 3;
         }
-        nl += launch_secular_warp(s, w, L, n, prm);
+        if (warp_tier) nl += launch_secular_warp(s, w, L, n, prm);
         if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
         PMARK(BRGPU_K_SECULAR);
     } else if (part == 1) {
         if (x) { launch_pdl(k_xunpack, xu, 256, 0, s, w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
         if (prm.zhat) {
             if (lane_tier) { launch_pdl(k_zhat, cdiv(n, kSecBlock), kSecBlock, 0, s, w, L, n); ++nl; }
-            launch_zhat_warp(s, w, L, n, prm);
-            ++nl;
+            if (warp_tier) { launch_zhat_warp(s, w, L, n, prm); ++nl; }
             if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 1, prm.xc, prm.xA, prm.xB); ++nl; }
             PMARK(BRGPU_K_ZHAT);
         }
@@ -1310,8 +1312,7 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         // requested rows need the roots (tau, org) that the rows kernels overwrite
         if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 2, &nl);
         if (lane_tier) { launch_pdl(k_rows, cdiv(n, kSecBlock), kSecBlock, 0, s, w, L, n); ++nl; }
-        launch_rows_warp(s, w, L, n, prm);
-        ++nl;
+        if (warp_tier) { launch_rows_warp(s, w, L, n, prm); ++nl; }
         if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 2, prm.xc, prm.xA, prm.xB); ++nl; }
         PMARK(BRGPU_K_ROWS);
     } else {
