@@ -713,12 +713,12 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, in
 // Start of a grid-tier level: zero the per-merge scale words, the look-back
 // tile states + tickets and the tier-mode word.
 __global__ void k_level_zero(unsigned long long* __restrict__ mTol, int M, unsigned long long* __restrict__ st,
-                             int words, int* __restrict__ modes) {
+                             int words, int* __restrict__ modes, int modes0) {
     pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < M) mTol[i] = 0ULL;
     if (i < words) st[i] = 0ULL;
-    if (i == 0) *modes = 0;
+    if (i == 0) *modes = modes0;
 }
 
 // Which secular tiers a level needs (merges with K > 0): bit0 lane-per-root,
@@ -1263,8 +1263,10 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         // per-merge scales, tile states + tickets of the two single-pass scans
         // (mtiles + ntiles + 2 words) and the mode word: zeroed by a kernel so the
         // level's launches form one programmatic-dependency chain
+        // a level without warp-tier merges needs no k_level_modes: its mode word is
+        // the lane bit (the lane kernels exit on an empty level by its root count)
         launch_pdl(k_level_zero, cdiv(max(L.M, mtiles + ntiles + 2), 256), 256, 0, s, L.mTol, L.M, w.scanState,
-                   mtiles + ntiles + 2, w.levelModes);
+                   mtiles + ntiles + 2, w.levelModes, warp_tier ? 0 : 1);
         unsigned long long* st1 = w.scanState;
         unsigned long long* st2 = w.scanState + mtiles;
         int* tk = reinterpret_cast<int*>(w.scanState + mtiles + ntiles);
@@ -1280,7 +1282,7 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 1, &nl);
         nl += 4;
         if (lane_tier) {
-            launch_pdl(k_level_modes, cdiv(L.M, 256), 256, 0, s, w, L);
+            if (warp_tier) { launch_pdl(k_level_modes, cdiv(L.M, 256), 256, 0, s, w, L); ++nl; }
             // CTAs per SM (= the launch bounds' minimum and the grid): 4 on levels up to
             // 2M elements (random 2^20 4.52 -> 4.46 ms), 6 on larger batched levels
             // (4096 x 1024: 12.12 -> 11.67 ms at 6)
@@ -1294,7 +1296,7 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
                 launch_pdl(k_secular<kSecMinbSmall>, ps.sec_grid, kSecBlock, 0, s, w, L, n, prm.patched);
             }
             launch_secular_tiled(s, w, L, n, ps);
-            nl += 3;
+            nl += 2;
         }
         if (warp_tier) nl += launch_secular_warp(s, w, L, n, prm);
         if (x) { launch_pdl(k_xpack, xg, 256, 0, s, w, n, 0, prm.xc, prm.xA, prm.xB); ++nl; }
