@@ -598,6 +598,10 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int
 // Q = sum z^2, S0/S1 = sum z x -- one add per member on the dependency chain --
 // and records each member's prefix (Q, S0, S1) at its position in the free
 // lam/blo/bhi slots; k_surv_scan finishes the members in parallel.
+#ifndef BRGPU_WALK_BATCH
+#define BRGPU_WALK_BATCH 8
+#endif
+constexpr int kWalkBatch = BRGPU_WALK_BATCH;  // NN entries loaded per step of a long segment walk
 __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     pdl_entry();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -621,20 +625,20 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     // length 1 (the common case) exits after its first probe.
     if (q + 1 < qe && fabs(w.D[w.nnPos[q + 1]] - dp) <= tol) {
         bool done = false;
-        for (int qb = q + 1; !done && qb < qe; qb += 8) {
-            int kb[8];
-            double db[8], zb[8], x0b[8], x1b[8];
+        for (int qb = q + 1; !done && qb < qe; qb += kWalkBatch) {
+            int kb[kWalkBatch];
+            double db[kWalkBatch], zb[kWalkBatch], x0b[kWalkBatch], x1b[kWalkBatch];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) kb[u] = w.nnPos[min(qb + u, qe - 1)];
+            for (int u = 0; u < kWalkBatch; ++u) kb[u] = w.nnPos[min(qb + u, qe - 1)];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kWalkBatch; ++u) {
                 db[u] = w.D[kb[u]];
                 zb[u] = w.Z[kb[u]];
                 x0b[u] = w.R0[kb[u]];
                 x1b[u] = w.R1[kb[u]];
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kWalkBatch; ++u) {
                 const int q2 = qb + u;
                 if (done || q2 >= qe) { done = true; continue; }
                 const double d2 = db[u];
