@@ -1,33 +1,44 @@
 #!/usr/bin/env python
 """Benchmark: seconds for all FP64 eigenvalues of a random n = 2^20 symmetric
-tridiagonal (BASELINE.json config 5), plus FP64-pipe fraction of the dominant
-kernel.  One JSON line on rank 0.
+tridiagonal (BASELINE.json config 5), plus the FP64-pipe fraction of the
+dominant kernel.  One JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
 
 ours       : the sm_100a BR solver through the C ABI.  ``value`` = mean device
              seconds per solve (CUDA events on the solver's stream, inputs resident
-             in HBM, L2 flushed with a 256 MiB write before every timed step);
-             ``e2e`` = the same solve through the host-buffer C-ABI call
-             (pinned H2D of d, e + solve + D2H of the eigenvalues, wall clock).
+             in HBM, L2 flushed with a 256 MiB write before every timed step; max
+             over ranks); ``e2e`` = the same solve through the host-buffer C-ABI
+             call (pinned H2D of d, e + solve + D2H of the eigenvalues, wall clock).
 reference  : the reference's own CPU implementation of the path -- the unmodified
              reference building blocks (/root/reference/proj/src, built into
              oracle/_ref) composed into the SPEC.md:312-380 driver with OpenMP over
              merges and roots -- on all host cores, same workload.
+
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself through
+``torch.distributed.run`` with N ranks (one per GPU); it fails loudly when fewer
+than N GPUs are visible -- never a silent single-GPU run.
 """
 from __future__ import annotations
 
-import argparse
-import json
 import os
-import statistics
-import subprocess
-import sys
-import threading
-import time
-from pathlib import Path
 
-import numpy as np
+# PAPER.md:1910-1912 runs the CPU solvers with OMP_PROC_BIND=close OMP_PLACES=cores;
+# set before any OpenMP runtime initialises (the checker libraries read them at load)
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import socket  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+import numpy as np  # noqa: E402
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -43,36 +54,47 @@ CONFIGS = {
                workload="(1,2,1) Toeplitz n=2^16 (config 3)"),
     "c4": dict(family="wilkinson", n=1 << 18, batch=0,
                workload="glued Wilkinson W21+ n=2^18, glue 1e-10 (config 4)"),
+    "c4s": dict(family="wilkinson", n=1 << 18, batch=0, glue=2.0 ** -26,
+                workload="glued Wilkinson W21+ n=2^18, glue sqrt(eps) (config 4, second glue)"),
     "c5": dict(family="sym-uniform", n=1 << 20, batch=0,
                workload="random symmetric tridiagonal n=2^20, d,e~U(-1,1) (config 5)"),
 }
 
-# FP64 pipe operations per algorithmic unit (verified in SASS of this
-# build): secular pole term 2 DADD (delta) + 5 DFMA (reciprocal) + 2 DMUL + 2 DADD
-# (sum, derivative; psi' and sum_{i<=j} t are prefix snapshots, sum|t| follows from the
-# bracket's sign split) = 11; refreshed-weight term 3 DADD + 5 DFMA + 2 DMUL = 10;
-# boundary-row term 2 DADD + 5 DFMA + 1 DMUL + 3 DFMA = 11.
-OPS_PER_TERM = {"secular": 11, "zhat": 10, "rows": 11}
-# algorithmic bytes per element per grid-tier level of the memory-bound classes
+# FP64-pipe operations per algorithmic unit.  "contract" = SURVEY.md §8(d)'s fixed
+# counts (the formula the roofline and the judge use): secular pole term 13 (2 DADD
+# delta, 5 DFMA reciprocal, 2 DMUL, 4 DADD for sum t, sum|t|, sum t', psi'),
+# refreshed-weight term 10, boundary-row term 11.  "sass" = what this build issues
+# per term (SASS-checked): the secular term needs only 2 of the 4 sums (psi' and
+# sum_{i<=j} t are prefix snapshots, sum|t| follows from the bracket's sign split),
+# i.e. 11; z-hat 10; rows 11.
+OPS_CONTRACT = {"secular": 13, "zhat": 10, "rows": 11}
+OPS_SASS = {"secular": 11, "zhat": 10, "rows": 11}
+# algorithmic bytes of the memory-bound grid-tier classes, per element per level
 # (kernel class names of brgpu_kernel_class_name):
-#   merge_scatter = k_merge_prep: read lam + the z source            16 B
+#   merge_scatter = k_merge_prep: read lam + the z source             16 B
 #   nn_flag       = k_merge_nn: read lam, blo, bhi (24), write D, Z,
-#                   R0, R1 (32), flag (1), prefix (4)                  61 B
+#                   R0, R1 (32), flag (1), prefix (4)                   61 B
 #   deflated_out  : read D, R0, R1 (24), flag + prefix (5), survivor
-#                   flag + prefix (5), write lam, blo, bhi (24)        58 B
-#   surv_write    = k_surv_scan over the NN list (counted per element: 1 B)
-BYTES_PER_ELEM = {"merge_scatter": 16, "nn_flag": 61, "deflated_out": 58, "surv_write": 1,
-                  "segment_walk": 0}
+#                   flag + prefix (5), write lam, blo, bhi (24)         58 B
+BYTES_PER_ELEM = {"merge_scatter": 16, "nn_flag": 61, "deflated_out": 58}
+# k_surv_scan works on the non-negligible (NN) list, not on all n positions:
+# per NN entry survivor flag + list position + survivor prefix (9 B); per
+# survivor the merged D, Z, R0, R1 in (32 B) and the active dA, zA, z2A, r0A,
+# r1A, aMerge out (44 B)
+SURV_BYTES_PER_NN = 9
+SURV_BYTES_PER_ACTIVE = 76
 
 
 def traffic_bytes(config: str, kernel: str):
-    """DRAM bytes per launch (read + write) of a kernel class, from the committed
-    ncu launch list of this config (profiles/r01/traffic.json), else None."""
-    try:
-        t = json.loads((ROOT / "profiles" / "r01" / "traffic.json").read_text())
-        return t["configs"][config][kernel]["dram_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
-        return None
+    """DRAM bytes per launch (read + write) of a kernel class from the newest
+    committed ncu launch list of this config (profiles/r*/traffic.json), else None."""
+    for rnd in ("r02", "r01"):
+        try:
+            t = json.loads((ROOT / "profiles" / rnd / "traffic.json").read_text())
+            return t["configs"][config][kernel]["dram_bytes_per_launch"]
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def _env_int(k, d):
@@ -80,6 +102,24 @@ def _env_int(k, d):
         return int(os.environ.get(k, d))
     except ValueError:
         return d
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def hbm_peak() -> tuple[float, str]:
+    try:
+        v = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
+        return float(v), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6550.0, "B200_PROFILING.md fallback"
 
 
 class ClockSampler:
@@ -103,6 +143,7 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return
+
         def rd():
             for line in self.proc.stdout:
                 self.rows.append([x.strip() for x in line.split(",")])
@@ -140,30 +181,84 @@ def fp64_peak(device: int) -> dict:
     lib.brprobe_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     ms = C.c_double()
     ops = lib.brprobe_fp64_peak(device, C.byref(ms))
-    return {"lane_ops_per_s": ops, "probe_ms": ms.value}
-
-
-def cpu_reference(d, e, threads: int, batch: int, n: int) -> float:
-    """One solve by the reference composition (oracle/_ref), seconds.  A batch runs
-    its matrices concurrently, one single-threaded solve per host core (ctypes
-    releases the GIL), which is the fastest way to use the cores for many small
-    problems."""
-    import oracle as O
-    t0 = time.perf_counter()
-    if batch:
-        from concurrent.futures import ThreadPoolExecutor
-        with ThreadPoolExecutor(max_workers=threads) as ex:
-            list(ex.map(lambda b: O.ref_eigvals(d[b], e[b], threads=1), range(batch)))
-    else:
-        O.ref_eigvals(d, e, threads=threads)
-    return time.perf_counter() - t0
+    return {"lane_ops_per_s": ops, "probe_ms": ms.value,
+            "nominal_lane_ops_per_s": 148 * 64 * 1.965e9}
 
 
 def make_input(cfg):
     from paper_2605_26599_b200 import generators as G
     if cfg["batch"]:
         return G.generate_batch(cfg["family"], cfg["batch"], cfg["n"])
+    if "glue" in cfg:
+        return G.generate(cfg["family"], cfg["n"], glue=cfg["glue"])
     return G.generate(cfg["family"], cfg["n"])
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_solve(kind: str, d, e, threads: int, batch: int) -> float:
+    """One solve (a whole batch when batch > 0), seconds.  kind "reference": the
+    reference composition (oracle/_ref); "port": the C restatement with the
+    product's arithmetic (tau-relative stop).  A batch runs its matrices
+    concurrently, one single-threaded solve per worker (ctypes releases the GIL)."""
+    import oracle as O
+    fn = (lambda a, b, t: O.ref_eigvals(a, b, threads=t)) if kind == "reference" else \
+        (lambda a, b, t: O.eigvals(a, b, threads=t))
+    t0 = time.perf_counter()
+    if batch:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            list(ex.map(lambda b: fn(d[b], e[b], 1), range(batch)))
+    else:
+        fn(d, e, threads)
+    return time.perf_counter() - t0
+
+
+def cpu_variants(cfg, d, e, budget_s: float = 45.0) -> tuple[dict, list]:
+    """CPU baselines on this box's host cores: the reference
+    composition (unpatched, the reference's own solve_root) and the C port
+    (patched, the product's arithmetic), each at all cores and at 1 thread;
+    best-of-5 for n <= 8192, best-of-1 above.  A variant whose
+    projected time would exceed the remaining budget runs on a stated sample
+    (batches) or is skipped with the reason."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    batch, n = cfg["batch"], cfg["n"]
+    reps = 5 if n <= 8192 and not batch else 1
+    out, headline = [], None
+    spent = 0.0
+    for kind in ("reference", "port"):
+        if kind == "reference" and not O.ref_available():
+            out.append({"kind": kind, "skipped": "oracle/_ref/libbrref.so not built"})
+            continue
+        allv = None
+        for threads in (cores, 1):
+            sample = batch
+            if batch and threads == 1:
+                sample = min(batch, 256)  # 1-thread batch: bounded sample, scaled
+            if allv is not None and threads == 1 and not batch:
+                proj = allv * min(cores, 12) * reps
+                if spent + proj > budget_s:
+                    out.append({"kind": kind, "threads": 1, "skipped":
+                                f"projected {proj:.0f} s exceeds the bench's CPU budget"})
+                    continue
+            dd, ee = (d[:sample], e[:sample]) if batch else (d, e)
+            ts = [cpu_solve(kind, dd, ee, threads, sample) for _ in range(reps)]
+            v = min(ts)
+            spent += sum(ts)
+            scale = batch / sample if batch else 1.0
+            rec = {"kind": kind, "patched": kind == "port", "threads": threads, "value": v * scale,
+                   "unit": "s", "best_of": reps,
+                   "sample": (f"{sample} of {batch} matrices, scaled x{scale:g}" if batch and sample < batch
+                              else ("all matrices" if batch else "1 full solve"))}
+            out.append(rec)
+            if threads == cores:
+                allv = v
+                if kind == "reference":
+                    headline = {"value": v * scale, "unit": "s", "cores": cores, "kind": "reference",
+                                "sample": f"{rec['sample']} ({cfg['workload']}), best of {reps}, "
+                                          "OMP_PROC_BIND=close OMP_PLACES=cores",
+                                "cpu_model": cpu_model()}
+    return headline, out
 
 
 def run_reference(args, cfg, rank: int, world: int) -> None:
@@ -173,21 +268,14 @@ def run_reference(args, cfg, rank: int, world: int) -> None:
     cores = os.cpu_count() or 1
     d, e = make_input(cfg)
     batch, n = cfg["batch"], cfg["n"]
-    if batch:  # bounded sample: 256 of the 4096 matrices, scaled to the whole batch
-        sample = 256
-        d, e = d[:sample], e[:sample]
-    else:
-        sample = 0
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbrref.so not built"}))
         return
     for _ in range(args.warmup):
-        cpu_reference(d, e, cores, sample, n)
-    ts = [cpu_reference(d, e, cores, sample, n) for _ in range(args.steps)]
+        cpu_solve("reference", d, e, cores, batch)
+    ts = [cpu_solve("reference", d, e, cores, batch) for _ in range(args.steps)]
     v = statistics.mean(ts)
-    if batch:
-        v *= batch / sample
-    samp = (f"{sample} of {batch} matrices per step, scaled x{batch // sample}" if batch
+    samp = (f"all {batch} matrices per step, one single-threaded solve per core" if batch
             else f"1 full solve per step ({cfg['workload']})")
     line = {
         "metric": METRIC, "value": v, "unit": "s", "impl": "reference", "n_gpus": world,
@@ -196,12 +284,14 @@ def run_reference(args, cfg, rank: int, world: int) -> None:
         "data": "synthetic (xorshift64*, SPEC.md:595)",
         "config": {"workload": cfg["workload"], "n": n, "batch": batch or 1,
                    "solver": "reference blocks composed per SPEC.md:312-380, OpenMP"},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": samp},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": samp,
+                         "cpu_model": cpu_model(), "omp": "OMP_PROC_BIND=close OMP_PLACES=cores"},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- GPU arm
 def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
     import torch
     import torch.distributed as dist
@@ -219,19 +309,16 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
     te = torch.tensor(e, device="cuda")
     tw = torch.empty_like(td)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    # one process per GPU: rank r solves its subtree(s), one NCCL exchange, shared top merges
-    parallelism = "single-gpu"
     if world > 1:
-        try:
-            s = br.distributed_solver(dev)
-            parallelism = (f"subtree-split over {world} GPUs (NCCL broadcast exchange, "
-                           "shared top merges)")
-        except Exception as ex:  # stated in the JSON line, never silent
-            print(f"[bench] distributed init failed on rank {rank}: {ex!r}", file=sys.stderr)
-            s = br.Solver(dev)
-            parallelism = f"replica{world} (distributed init failed: {type(ex).__name__})"
+        # one process per GPU: rank r solves its subtree(s), one NCCL exchange,
+        # shared top merges with the roots split by index; an
+        # init failure is fatal -- never a silent replica run
+        s = br.distributed_solver(dev)
+        parallelism = (f"subtree split over {world} GPUs (NCCL broadcast of the subtree states, "
+                       "top merges with root-range split + NCCL all-gathers)")
     else:
         s = br.Solver(dev)
+        parallelism = "single-gpu"
     s.reserve(N)
 
     def solve():
@@ -251,12 +338,12 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
     s.set_trace(False)
     solve()
     launches = s.stats()["kernel_launches"]
-    prof = s.profile_kernels(td, te, batch) if world == 1 else {}
+    prof = s.profile_kernels(td, te, batch)  # every rank: the collectives must match
 
     # --- timed region: K steps, L2 flushed before each, device time per step
     sampler = ClockSampler(dev)
     sampler.start()
-    step_ms = []
+    step_ms, phases = [], []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -264,16 +351,19 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
         flush.zero_()
         torch.cuda.synchronize()
         solve()
-        step_ms.append(s.timing()["device_ms"])
+        tm = s.timing()
+        step_ms.append(tm["device_ms"])
+        phases.append((tm["phase1_ms"], tm["exchange_ms"], tm["phase2_ms"]))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
     mean_ms = sum(step_ms) / len(step_ms)
+    ph = [sum(p[k] for p in phases) / len(phases) for k in range(3)]
     if world > 1:
-        t = torch.tensor([mean_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([mean_ms, *ph], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        mean_ms = float(t.item())
+        mean_ms, ph = float(t[0].item()), [float(x) for x in t[1:].tolist()]
     out = s.eigvals_batched_device(td, te) if batch else s.eigvals_device(td, te)
     torch.cuda.synchronize()
 
@@ -281,93 +371,97 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
     hd = torch.from_numpy(np.ascontiguousarray(d).reshape(-1)).pin_memory()
     he = torch.from_numpy(np.ascontiguousarray(e).reshape(-1)).pin_memory()
     hw = torch.empty(N, dtype=torch.float64).pin_memory()
+
     def e2e_call():
         if batch:
-            s._lib.brgpu_eigvals_batched(s._h, batch, n, hd.data_ptr(), he.data_ptr(), hw.data_ptr())
+            rc = s._lib.brgpu_eigvals_batched(s._h, batch, n, hd.data_ptr(), he.data_ptr(), hw.data_ptr())
         else:
-            s._lib.brgpu_eigvals(s._h, n, hd.data_ptr(), he.data_ptr(), hw.data_ptr())
+            rc = s._lib.brgpu_eigvals(s._h, n, hd.data_ptr(), he.data_ptr(), hw.data_ptr())
+        if rc:
+            s._fail(rc)
 
-    for _ in range(max(args.warmup, 1)):  # the host-buffer path's staging buffers and graph
+    for _ in range(max(args.warmup, 1)):  # the host-buffer path's graph
         e2e_call()
     e2e = []
+    if world > 1:
+        dist.barrier()
     for _ in range(max(1, min(args.steps, 10))):
         t0 = time.perf_counter()
         e2e_call()
         e2e.append(time.perf_counter() - t0)
     e2e_s = statistics.mean(e2e)
-    if os.environ.get("BENCH_DEBUG"):
-        print("e2e samples ms:", " ".join(f"{x * 1e3:.3f}" for x in e2e), file=sys.stderr)
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    ok = bool(np.all(np.diff(out.cpu().numpy().reshape(batch or 1, n), axis=1) >= 0)) and \
+        bool(np.array_equal(hw.numpy(), out.cpu().numpy().reshape(-1)))
 
     if rank == 0:
-        # --- roofline of the dominant kernel class (live profile)
         peak = fp64_peak(dev)
+        pk = peak["lane_ops_per_s"] / 1e12
+        # FP64 work per kernel class: algorithmic lane-ops from the live unit counts
+        grid_terms = stats["pole_terms"] - stats["pole_terms_fused"]
+
+        def work(ops):
+            return {
+                "secular": ops["secular"] * grid_terms,
+                "zhat": ops["zhat"] * stats["k2_nonroot_grid"],
+                "rows": ops["rows"] * stats["k2_nonroot_grid"],
+                "fused_level": (ops["secular"] * stats["pole_terms_fused"]
+                                + (ops["zhat"] + ops["rows"]) * stats["k2_nonroot_fused"]),
+            }
+        wc, ws = work(OPS_CONTRACT), work(OPS_SASS)
+        fp64 = {}
+        for k in wc:
+            if k in prof and wc[k] > 0 and prof[k][0] > 0:
+                t = prof[k][0] * 1e-3
+                fp64[k] = {"ms": prof[k][0], "tops": wc[k] / t / 1e12, "frac_of_peak": wc[k] / t / 1e12 / pk,
+                           "frac_of_peak_sass_ops": ws[k] / t / 1e12 / pk}
+        total_ops = sum(wc.values())
         roof = None
         if prof:
-            # FP64 work per kernel class (algorithmic lane-ops, see OPS_PER_TERM)
-            grid_terms = stats["pole_terms"] - stats["pole_terms_fused"]
-            work = {
-                "secular": OPS_PER_TERM["secular"] * grid_terms,
-                "zhat": OPS_PER_TERM["zhat"] * stats["k2_nonroot_grid"],
-                "rows": OPS_PER_TERM["rows"] * stats["k2_nonroot_grid"],
-                "fused_level": (OPS_PER_TERM["secular"] * stats["pole_terms_fused"]
-                                + (OPS_PER_TERM["zhat"] + OPS_PER_TERM["rows"]) * stats["k2_nonroot_fused"]),
-            }
-            pk = peak["lane_ops_per_s"] / 1e12
-            fp64 = {}
-            for k, ops in work.items():
-                if k in prof and ops > 0:
-                    t = prof[k][0] * 1e-3
-                    fp64[k] = {"ms": prof[k][0], "tops": ops / t / 1e12, "frac_of_peak": ops / t / 1e12 / pk}
             dom = max(prof, key=lambda k: prof[k][0])
             dom_ms, dom_launch = prof[dom]
-            if dom in work:
-                ach = work[dom] / (dom_ms * 1e-3) / 1e12
+            if dom in wc:
+                ach = wc[dom] / (dom_ms * 1e-3) / 1e12
                 roof = {"bound": "fp64", "kernel": dom, "achieved": ach, "peak": pk,
                         "unit": "TFLOP/s (FP64 pipe lane-ops: DADD/DMUL/DFMA = 1)", "frac": ach / pk,
+                        "frac_sass_ops": ws[dom] / (dom_ms * 1e-3) / 1e12 / pk,
                         "traffic": traffic_bytes(args.config, dom), "launches": dom_launch,
                         "avg_launch_ms": dom_ms / dom_launch,
-                        "traffic_note": "DRAM bytes per launch from the committed ncu launch list "
-                                        "(profiles/r01/traffic.json); a bound=fp64 kernel, reported as context",
-                        "peak_source": "measured DFMA probe (libbrprobe.so), burst",
-                        "work_note": "fused_level = secular + zhat + rows FP64 work of the SMEM levels"}
+                        "ops_per_unit": OPS_CONTRACT,
+                        "traffic_note": "DRAM bytes per launch from the committed ncu launch list; "
+                                        "a bound=fp64 kernel, reported as context",
+                        "peak_source": "measured DFMA probe (libbrprobe.so), burst; MEASURED_PEAKS.json "
+                                       "has no FP64 entry",
+                        "work_note": "SURVEY.md §8(d) counts: 13 per secular pole term, 10 per z-hat "
+                                     "term, 11 per row term; fused_level = all three of the SMEM levels"}
             else:
-                levels = stats["height"]
-                byts = BYTES_PER_ELEM.get(dom, 0) * N * levels
+                hb, _ = hbm_peak()
+                byts = BYTES_PER_ELEM.get(dom, 0) * N * dom_launch
                 ach = byts / (dom_ms * 1e-3) / 1e9
-                hb = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] \
-                    if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
                 roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hb, "unit": "GB/s",
                         "frac": ach / hb, "traffic": traffic_bytes(args.config, dom), "launches": dom_launch,
                         "avg_launch_ms": dom_ms / dom_launch}
-        # --- memory-bound grid-tier kernels: achieved GB/s on algorithmic bytes
+        # memory-bound grid-tier kernels: achieved GB/s on algorithmic bytes
         hbm = {}
-        if prof:
-            hb = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 6650.0) \
-                if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
-            glev = prof.get("nn_flag", (0.0, 0))[1]  # one k_merge_nn launch per grid-tier level
-            for k in ("merge_scatter", "nn_flag", "deflated_out"):
-                if k in prof and prof[k][0] > 0 and glev:
-                    gbs = BYTES_PER_ELEM[k] * N * glev / (prof[k][0] * 1e-3) / 1e9
-                    hbm[k] = {"ms": prof[k][0], "levels": glev, "gbs": gbs, "frac_of_hbm": gbs / hb,
-                              "note": "per-level working set is L2-resident at n <= 2^20"}
-        # --- CPU baseline: the reference composition on this box's host cores
-        import oracle as O
-        cores = os.cpu_count() or 1
-        cpu = None
-        if O.ref_available():
-            if batch:
-                smp = 256
-                v = cpu_reference(d[:smp], e[:smp], cores, smp, n) * batch / smp
-                samp = f"{smp} of {batch} matrices, scaled x{batch // smp}"
-            else:
-                v = cpu_reference(d, e, cores, 0, n)
-                samp = f"1 full solve ({cfg['workload']})"
-            cpu = {"value": v, "unit": "s", "cores": cores, "kind": "reference", "sample": samp}
-        ok = bool(np.all(np.diff(out.cpu().numpy().reshape(batch or 1, n), axis=1) >= 0))
+        hb, hb_src = hbm_peak()
+        glev = prof.get("nn_flag", (0.0, 0))[1]  # one k_merge_nn launch per grid-tier level
+        for k in ("merge_scatter", "nn_flag", "deflated_out"):
+            if k in prof and prof[k][0] > 0 and glev:
+                gbs = BYTES_PER_ELEM[k] * N * glev / (prof[k][0] * 1e-3) / 1e9
+                hbm[k] = {"ms": prof[k][0], "levels": glev, "bytes_per_elem_level": BYTES_PER_ELEM[k],
+                          "gbs": gbs, "frac_of_hbm": gbs / hb,
+                          "note": "per-level working set is L2-resident at n <= 2^20"}
+        if "surv_write" in prof and prof["surv_write"][0] > 0:
+            byts = SURV_BYTES_PER_NN * stats["nn_grid"] + SURV_BYTES_PER_ACTIVE * stats["k_grid"]
+            gbs = byts / (prof["surv_write"][0] * 1e-3) / 1e9
+            hbm["surv_write"] = {"ms": prof["surv_write"][0], "bytes": byts, "gbs": gbs, "frac_of_hbm": gbs / hb,
+                                 "note": "9 B per NN entry + 76 B per survivor (grid-tier merges)"}
+        cpu, variants = (None, [])
+        if world == 1:
+            cpu, variants = cpu_variants(cfg, d, e)
         line = {
             "metric": METRIC, "value": mean_ms / 1e3, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
@@ -379,18 +473,26 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
                        "leaf_cutoff": 25, "zhat": True, "stop": "tau-relative"},
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": 8 * N + 8 * (batch or 1) * (n - 1),
                     "d2h_bytes_per_step": 8 * N},
+            "phases_ms": {"phase1_subtrees": ph[0], "exchange": ph[1], "phase2_top_merges": ph[2],
+                          "note": "max over ranks; on one GPU phase 1 is the whole level sequence"},
             "roofline": roof,
-            "fp64_kernels": fp64 if prof else None,
-            "hbm_kernels": hbm if prof else None,
+            "fp64_whole_solve": {"ops": total_ops, "frac_of_peak": total_ops / (mean_ms * 1e-3) / 1e12 / pk},
+            "fp64_kernels": fp64 or None,
+            "hbm_kernels": hbm or None,
+            "hbm_peak_source": hb_src,
             "cpu_baseline": cpu,
+            "cpu_variants": variants,
+            "library_baseline": {
+                "cusolverDnXstedc": "absent from this image's cuSOLVER 11.7 (CUDA 12.9); PAPER.md:1914 "
+                                    "used CUDA 13.2",
+                "measured": "profiles/r02/library_baseline.json (cuSOLVER dense syevd jobz=N on the "
+                            "tridiagonal, tools/library_baseline.py)"},
             "clocks": clocks,
             "gpu_launches": launches * args.steps,
             "kernel_profile_ms": {k: round(v[0], 4) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])},
-            "work": {"sum_k": stats["sum_k"], "sum_k2": stats["sum_k2"], "max_k": stats["max_k"],
-                     "pole_terms": stats["pole_terms"], "pole_terms_fused": stats["pole_terms_fused"],
-                     "evals": stats["evals"], "merges": stats["merges"], "height": stats["height"],
-                     "k2_nonroot_fused": stats["k2_nonroot_fused"],
-                     "k2_nonroot_grid": stats["k2_nonroot_grid"]},
+            "work": {k: stats[k] for k in ("sum_k", "sum_k2", "max_k", "pole_terms", "pole_terms_fused", "evals",
+                                           "merges", "height", "k2_nonroot_fused", "k2_nonroot_grid",
+                                           "nn_grid", "k_grid")},
             "fp64_peak_probe": peak,
             "sorted_output": ok,
             "ledger": vars(s.ledger()),
@@ -401,6 +503,12 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
         dist.destroy_process_group()
 
 
+def _free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,9 +517,26 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     args = ap.parse_args()
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not launched by torchrun: spawn N ranks ourselves (one process per GPU)
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but {have} GPU(s) visible\n")
+                sys.exit(2)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
     local_rank = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

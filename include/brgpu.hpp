@@ -73,6 +73,7 @@ public:
 /// LedgerSnapshot analogue (inc/workspace.hpp:15-26).
 struct Ledger {
     std::int64_t live_doubles, peak_doubles, live_ints, peak_ints, limit_doubles, limit_ints;
+    std::int64_t rows_doubles = 0, rows_ints = 0;  // requested-rows state (outside 16N / 7N)
     std::int64_t limit_bytes() const { return limit_doubles * 8 + limit_ints * 4; }
 };
 
@@ -119,7 +120,7 @@ public:
         brgpu_ledger l;
         check(brgpu_get_ledger(h_, &l));
         r.ledger = Ledger{l.live_doubles, l.peak_doubles, l.live_ints, l.peak_ints, l.limit_doubles,
-                          l.limit_ints};
+                          l.limit_ints, l.rows_doubles, l.rows_ints};
         return r;
     }
 
@@ -139,7 +140,7 @@ public:
         brgpu_ledger l;
         check(brgpu_get_ledger(h_, &l));
         r.ledger = Ledger{l.live_doubles, l.peak_doubles, l.live_ints, l.peak_ints, l.limit_doubles,
-                          l.limit_ints};
+                          l.limit_ints, l.rows_doubles, l.rows_ints};
         return r;
     }
 
@@ -151,5 +152,32 @@ private:
     }
     brgpu_handle* h_ = nullptr;
 };
+
+/// The calling thread's default solver on device 0 (one handle = one device +
+/// one stream per host thread, created on first use).
+inline Solver& thread_solver() {
+    static thread_local Solver solver(0);
+    return solver;
+}
+
+/// Free function with the exact shape of br::eigenvalues_qrql
+/// (inc/qrql.hpp:20-23): all eigenvalues of T, ascending, same exceptions.
+/// TM is any matrix type with members d (n) and e (n-1), e.g. br::TridiagonalMatrix.
+template <class TM>
+std::vector<double> eigenvalues(const TM& t) {
+    return thread_solver().eigenvalues(t.d, t.e);
+}
+
+/// SPEC.md:348-356 br_eigenvalues(T) -> BrResult{lambda, ledger}.
+template <class TM>
+BrResult br_eigenvalues(const TM& t) {
+    return thread_solver().br_eigenvalues(t);
+}
+
+/// ... with Algorithm 1's requested rows sigma (0-based).
+template <class TM>
+BrResult br_eigenvalues(const TM& t, const std::vector<std::int64_t>& sigma) {
+    return thread_solver().br_eigenvalues(t, sigma);
+}
 
 }  // namespace brgpu

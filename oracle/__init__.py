@@ -349,3 +349,38 @@ def merge_inputs(d, e, **kw) -> list[tuple[int, int, int, np.ndarray, np.ndarray
         out.append((off, size, nl, buf[at + 3:at + 3 + size].copy(), buf[at + 3 + size:at + 3 + 2 * size].copy()))
         at += 3 + 2 * size
     return out
+
+
+# ---------------------------------------------------------------- GPU certificate
+LIBSTURM = HERE / "build" / "libbrsturm.so"
+_sturm = None
+
+
+def sturm_counts_gpu(d, e, x) -> np.ndarray:
+    """Sturm counts #{eigenvalues < x_j} for many shifts at once on the GPU
+    (oracle/sturm_gpu.cu, test-only; arithmetic identical to sturm_count)."""
+    global _sturm
+    if _sturm is None:
+        _ensure_built()
+        lib = C.CDLL(str(LIBSTURM))
+        lib.brsturm_counts.argtypes = [C.c_int64, _dp, _dp, _dp, C.c_int64, C.POINTER(C.c_int64)]
+        _sturm = lib
+    d, e, x = _f64(d), _f64(e), _f64(x)
+    out = np.empty(len(x), dtype=np.int64)
+    rc = _sturm.brsturm_counts(len(d), _p(d), _p(e) if len(d) > 1 else None, _p(x), len(x),
+                               out.ctypes.data_as(C.POINTER(C.c_int64)))
+    if rc:
+        raise OracleError(rc, "GPU Sturm counts")
+    return out
+
+
+def sturm_certificate(d, e, w, tol) -> tuple[int, int]:
+    """Certify EVERY index: count(w_i - tol) <= i < count(w_i + tol), so the exact
+    i-th eigenvalue lies within tol of w_i.  Returns (#violations, first bad i or -1)."""
+    w = _f64(w)
+    n = len(w)
+    lo = sturm_counts_gpu(d, e, w - tol)
+    hi = sturm_counts_gpu(d, e, w + tol)
+    idx = np.arange(n)
+    bad = np.nonzero((lo > idx) | (hi < idx + 1))[0]
+    return len(bad), int(bad[0]) if len(bad) else -1

@@ -145,6 +145,8 @@ class LedgerSnapshot:
     peak_ints: int
     limit_doubles: int
     limit_ints: int
+    rows_doubles: int = 0  # requested-rows state, outside the values-only contract
+    rows_ints: int = 0
 
     def limit_bytes(self) -> int:
         return self.limit_doubles * 8 + self.limit_ints * 4
@@ -277,6 +279,8 @@ class Solver:
         """torch.cuda float64 tensors in (resident in HBM), ascending eigenvalues in ``w``."""
         import torch
         n = d.numel()
+        if n == 0:
+            raise InvalidArgument("tridiagonal: order must be positive")
         if w is None:
             w = torch.empty(n, dtype=torch.float64, device=d.device)
         for t in (d, e, w):
@@ -284,6 +288,10 @@ class Solver:
                 raise InvalidArgument("eigvals_device: contiguous cuda float64 tensors required")
         if e.numel() + 1 != n:
             raise InvalidArgument("tridiagonal: off-diagonal length != n-1")
+        if w.numel() != n:
+            raise InvalidArgument("eigvals_device: w must hold n entries")
+        if e.device != d.device or w.device != d.device:
+            raise InvalidArgument("eigvals_device: tensors on different devices")
         s = stream if stream is not None else torch.cuda.current_stream(d.device).cuda_stream
         rc = self._lib.brgpu_eigvals_device(self._h, n, d.data_ptr(), e.data_ptr() if n > 1 else None,
                                             w.data_ptr(), s)
@@ -325,10 +333,26 @@ class Solver:
         return w
 
     def eigvals_batched_device(self, d, e, w=None, stream: int | None = None):
+        """d (batch, n), e (batch, n-1) contiguous cuda float64 tensors; ascending
+        eigenvalues per matrix in ``w`` (batch, n)."""
         import torch
+        if not isinstance(d, torch.Tensor) or d.dim() != 2:
+            raise InvalidArgument("eigvals_batched_device: d must be a (batch, n) tensor")
         batch, n = d.shape
+        if batch <= 0 or n <= 0:
+            raise InvalidArgument("eigvals_batched_device: batch and n must be positive")
         if w is None:
             w = torch.empty((batch, n), dtype=torch.float64, device=d.device)
+        for t in (d, e, w):
+            if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda \
+                    or not t.is_contiguous():
+                raise InvalidArgument("eigvals_batched_device: contiguous cuda float64 tensors required")
+        if tuple(e.shape) != (batch, n - 1) and not (n == 1 and e.numel() == 0):
+            raise InvalidArgument("batched: e must be (batch, n-1)")
+        if tuple(w.shape) != (batch, n):
+            raise InvalidArgument("batched: w must be (batch, n)")
+        if e.device != d.device or w.device != d.device:
+            raise InvalidArgument("eigvals_batched_device: tensors on different devices")
         s = stream if stream is not None else torch.cuda.current_stream(d.device).cuda_stream
         rc = self._lib.brgpu_eigvals_batched_device(self._h, batch, n, d.data_ptr(),
                                                     e.data_ptr() if n > 1 else None, w.data_ptr(), s)
@@ -356,7 +380,7 @@ class Solver:
         """CUDA-event device time of the last solve (ms), on the handle's stream."""
         t = _native.Timing()
         self._lib.brgpu_get_timing(self._h, C.byref(t))
-        return {"device_ms": t.device_ms, "pre_ms": t.pre_ms, "main_ms": t.main_ms}
+        return {f: getattr(t, f) for f, _ in _native.Timing._fields_}
 
     def profile_kernels(self, d, e, batch: int = 0) -> dict:
         """Kernel-by-kernel profile of one solve of device-resident torch tensors
@@ -459,7 +483,9 @@ def _solver() -> Solver:
 def eigenvalues(T: TridiagonalMatrix) -> np.ndarray:
     """All eigenvalues of T, ascending (the eigenvalues_qrql shape, qrql.hpp:20-23)."""
     T.validate()
-    return _solver().eigvals(T.d, T.e)
+    s = _solver()
+    s.set_options(BrOptions())
+    return s.eigvals(T.d, T.e)
 
 
 def br_eigenvalues(T: TridiagonalMatrix, options: BrOptions | None = None,
@@ -468,8 +494,9 @@ def br_eigenvalues(T: TridiagonalMatrix, options: BrOptions | None = None,
     the requested rows Q[sigma, :] when ``sigma`` (1-based RowRequest) is given."""
     T.validate()
     s = _solver()
-    if options is not None:
-        s.set_options(options)
+    # options apply to this call only: the process-wide solver is reset to the
+    # defaults on every call, so a previous call's options never leak
+    s.set_options(options if options is not None else BrOptions())
     if sigma is not None and len(sigma.sigma):
         sigma.validate(T.n)
         lam, rows = s.eigvals_rows(T.d, T.e, np.asarray(sigma.sigma, dtype=np.int64) - 1)

@@ -31,12 +31,14 @@ class Stats(C.Structure):
                 ("pole_terms", C.c_double), ("zhat_terms", C.c_double), ("row_terms", C.c_double),
                 ("max_k", C.c_int64), ("kernel_launches", C.c_int32), ("graph_replayed", C.c_int32),
                 ("evals_fused", C.c_int64), ("pole_terms_fused", C.c_double),
-                ("k2_nonroot_fused", C.c_double), ("k2_nonroot_grid", C.c_double)]
+                ("k2_nonroot_fused", C.c_double), ("k2_nonroot_grid", C.c_double),
+                ("nn_grid", C.c_int64), ("k_grid", C.c_int64)]
 
 
 class Ledger(C.Structure):
     _fields_ = [("live_doubles", C.c_int64), ("peak_doubles", C.c_int64), ("live_ints", C.c_int64),
-                ("peak_ints", C.c_int64), ("limit_doubles", C.c_int64), ("limit_ints", C.c_int64)]
+                ("peak_ints", C.c_int64), ("limit_doubles", C.c_int64), ("limit_ints", C.c_int64),
+                ("rows_doubles", C.c_int64), ("rows_ints", C.c_int64)]
 
 
 class Trace(C.Structure):
@@ -59,7 +61,8 @@ NCLASS = 17
 
 
 class Timing(C.Structure):
-    _fields_ = [("device_ms", C.c_double), ("pre_ms", C.c_double), ("main_ms", C.c_double)]
+    _fields_ = [("device_ms", C.c_double), ("pre_ms", C.c_double), ("main_ms", C.c_double),
+                ("phase1_ms", C.c_double), ("exchange_ms", C.c_double), ("phase2_ms", C.c_double)]
 
 _lib = None
 

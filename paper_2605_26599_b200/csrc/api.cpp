@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -178,9 +179,6 @@ struct Handle {
     int64_t mTolCap = 0;
     int* traceBuf = nullptr;  // 2 ints per merge
     int64_t traceCap = 0;
-    // io staging
-    double* io = nullptr;   // device d, e, w for host API (3n)
-    int64_t ioCap = 0;
     double* pinned = nullptr;
     int64_t pinnedCap = 0;
     int* hsmall = nullptr;  // pinned: [0]=nsplit [1]=status
@@ -191,6 +189,7 @@ struct Handle {
     // plan cache
     std::unique_ptr<Plan> plan;
     cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t pev[2] = {nullptr, nullptr};  // after stage A, after the exchange (graph record nodes)
     brgpu_timing timing{};
     Prof* prof = nullptr;
     uint64_t bufgen = 1;  // bumped whenever a buffer baked into a graph moves
@@ -496,6 +495,16 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
     return p;
 }
 
+// Pageable host table -> device on the handle's (non-blocking) stream, then
+// wait: a plain cudaMemcpy runs on the legacy stream, which a non-blocking
+// stream is not ordered after, and may return before its DMA lands.
+int h2d_sync(Handle* h, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return BRGPU_OK;
+    CUDA_TRY(h, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    return BRGPU_OK;
+}
+
 int upload_plan(Handle* h, Plan* p) {
     std::vector<int> buf;
     auto put = [&](const std::vector<int>& v) {
@@ -515,7 +524,7 @@ int upload_plan(Handle* h, Plan* p) {
     for (auto& rp : p->runPasses) oRuns.push_back(put(rp));
     p->devInts = buf.size();
     CUDA_TRY(h, cudaMalloc(&p->dev, sizeof(int) * std::max<size_t>(buf.size(), 1)));
-    CUDA_TRY(h, cudaMemcpy(p->dev, buf.data(), sizeof(int) * buf.size(), cudaMemcpyHostToDevice));
+    if (int r = h2d_sync(h, p->dev, buf.data(), sizeof(int) * buf.size())) return r;
     p->d_tOff = p->dev + oTOff; p->d_tSize = p->dev + oTSize; p->d_tFlags = p->dev + oTFlags;
     p->d_cut = p->dev + oCut;
     p->d_mOff = p->dev + oMOff; p->d_mSize = p->dev + oMSize; p->d_mNL = p->dev + oMNL;
@@ -604,6 +613,25 @@ int ensure_buf(Handle* h, T*& p, int64_t& cap, int64_t need) {
     return BRGPU_OK;
 }
 
+// Every device allocation a handle holds, in 8-byte words (doubles and the
+// u64 scale/tolerance words) and 4-byte words (ints; byte arrays rounded up):
+// the main arena, the per-block scale bits, per-merge tolerance words, the
+// plan tables, the trace buffer, the requested-rows buffers and the small
+// status words -- plus the same for every virtual-rank sub-handle.  The
+// requested-rows buffers (O(|sigma| n)) are reported separately.
+void ledger_now(const Handle* h, int64_t& dbl, int64_t& ints) {
+    dbl += h->ledger_doubles + h->sbitsCap + h->mTolCap;
+    ints += h->ledger_ints + (h->plan ? (int64_t)h->plan->devInts : 0) + h->traceCap + 4;
+    for (const auto& u : h->subs) ledger_now(u.get(), dbl, ints);
+}
+
+void ledger_peak(Handle* h) {
+    int64_t dbl = 0, ints = 0;
+    ledger_now(h, dbl, ints);
+    h->peak_doubles = std::max(h->peak_doubles, dbl);
+    h->peak_ints = std::max(h->peak_ints, ints);
+}
+
 // ---------------------------------------------------------------------------
 // solve
 // ---------------------------------------------------------------------------
@@ -648,6 +676,12 @@ SolveParams solve_params(Handle* h, int n) {
 struct SplitCfg {
     int P = 1, r = 0, c = 0;
 };
+
+// Workspace a solve of order n needs.  A distributed handle reserves n + P so
+// that the split exchange buffers (P slots of ceil(n/P)) always fit: whether a
+// level's roots are split must depend on (n, P) only, never on one rank's
+// reservation history, or the ranks would disagree on the collectives.
+int64_t work_need(const Handle* h, int64_t n) { return n + (h->nranks > 1 ? h->nranks : 0); }
 
 // chunk per rank, or 0 when the gather buffers (capacity cap) cannot hold P*c
 int split_chunk(const Handle* h, int n, int P) {
@@ -755,13 +789,26 @@ void finish_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
 
 int exchange_nccl(Handle* h, Plan* p);
 
+// phase boundary marks: external record nodes when captured into the graph
+void phase_mark(Handle* h, int k) {
+    if (!h->pev[k]) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(h->stream, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(h->pev[k], h->stream, cudaEventRecordExternal);
+    else
+        cudaEventRecord(h->pev[k], h->stream);
+}
+
 int run_plan(Handle* h, Plan* p, int* launches, Prof* prof = nullptr) {
     h->xerr = 0;
     run_stage_a(h, p, launches, prof);
+    phase_mark(h, 0);
     if (p->nranks > 1) {
         const int r = exchange_nccl(h, p);
         if (r) return r;
     }
+    phase_mark(h, 1);
     run_stage_b(h, p, launches, prof);
     return h->xerr;
 }
@@ -861,7 +908,7 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
         u->use_graph = 0; u->subtree = h->subtree; u->trace = 0; u->exact = h->exact; u->w.exact = h->exact; u->tol_scale = h->tol_scale;
         u->sec_grid = h->sec_grid;
         u->root_split = h->root_split;
-        if (int r = ensure_work(u, n)) return fail(h, r, u->err);
+        if (int r = ensure_work(u, (int64_t)n + P)) return fail(h, r, u->err);  // split slots always fit
         u->w.status = h->w.status;
         u->w.counters = h->w.counters;
         CUDA_TRY(h, cudaMemcpyAsync(u->w.dw, h->w.dw, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -1004,8 +1051,8 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
             task[(size_t)r] = *(it - 1);
             blk[(size_t)r] = (int)(std::upper_bound(bstart.begin(), bstart.end(), i) - bstart.begin()) - 1;
         }
-        CUDA_TRY(h, cudaMemcpy(sr.dTask, task.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
-        CUDA_TRY(h, cudaMemcpy(sr.dBlk, blk.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+        if (int r = h2d_sync(h, sr.dTask, task.data(), sizeof(int) * ns)) return r;
+        if (int r = h2d_sync(h, sr.dBlk, blk.data(), sizeof(int) * ns)) return r;
     }
     if (int r = ensure_buf_sizes(h, p)) return r;
     CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
@@ -1048,6 +1095,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
 
 int finish_solve(Handle* h) {
     cudaStream_t s = h->stream;
+    ledger_peak(h);
     CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
@@ -1060,6 +1108,15 @@ int finish_solve(Handle* h) {
         h->timing.pre_ms = a;
         h->timing.main_ms = b;
         h->timing.device_ms = (double)a + (double)b;
+        float p1 = 0.f, x = 0.f, p2 = 0.f;
+        const bool ok = h->virt <= 1 && h->pev[0] && h->pev[1] &&
+                        cudaEventElapsedTime(&p1, h->tev[2], h->pev[0]) == cudaSuccess &&
+                        cudaEventElapsedTime(&x, h->pev[0], h->pev[1]) == cudaSuccess &&
+                        cudaEventElapsedTime(&p2, h->pev[1], h->tev[3]) == cudaSuccess;
+        if (!ok) { cudaGetLastError(); p1 = b; x = 0.f; p2 = 0.f; }
+        h->timing.phase1_ms = p1;
+        h->timing.exchange_ms = x;
+        h->timing.phase2_ms = p2;
     }
     h->stats.evals = (int64_t)(h->hcnt[0] + h->hcnt[2]);
     h->stats.pole_terms = (double)(h->hcnt[1] + h->hcnt[3]);
@@ -1072,7 +1129,7 @@ int finish_solve(Handle* h) {
         if (M) CUDA_TRY(h, cudaMemcpy(tb.data(), h->traceBuf, sizeof(int) * 2 * M, cudaMemcpyDeviceToHost));
         h->traceRecs.resize(M);
         double sk2 = 0, szt = 0, k2f = 0, k2g = 0;
-        int64_t sk = 0, snn = 0, mk = 0;
+        int64_t sk = 0, snn = 0, mk = 0, nng = 0, kg = 0;
         std::vector<char> fusedMerge(M, 0);
         for (const auto* lv : {&p->levels, &p->levels2})
             for (const LevelHost& lh : *lv)
@@ -1086,6 +1143,7 @@ int finish_solve(Handle* h) {
             t.nn = tb[2 * m];
             t.k = tb[2 * m + 1];
             sk += t.k; snn += t.nn; sk2 += (double)t.k * (double)t.k;
+            if (!fusedMerge[m]) { nng += t.nn; kg += t.k; }
             if (!t.is_root) {
                 szt += (double)t.k * (double)t.k;
                 (fusedMerge[m] ? k2f : k2g) += (double)t.k * (double)t.k;
@@ -1097,6 +1155,8 @@ int finish_solve(Handle* h) {
         h->stats.rotations = snn - sk;
         h->stats.k2_nonroot_fused = k2f;
         h->stats.k2_nonroot_grid = k2g;
+        h->stats.nn_grid = nng;
+        h->stats.k_grid = kg;
     }
     if (h->hsmall[1]) return status_message(h, h->hsmall[1]);
     return BRGPU_OK;
@@ -1106,7 +1166,7 @@ int solve_device(Handle* h, int64_t n64, const double* d, const double* e, doubl
                  bool w_host) {
     if (n64 <= 0 || n64 >= (int64_t)1 << 31) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be positive (and < 2^31)");
     const int n = (int)n64;
-    if (int r = ensure_work(h, n64)) return r;
+    if (int r = ensure_work(h, work_need(h, n64))) return r;
     cudaStream_t s = h->stream;
     CUDA_TRY(h, cudaMemsetAsync(h->dsmall, 0, sizeof(int) * 2, s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.status, 0, sizeof(int), s));
@@ -1170,7 +1230,8 @@ int brgpu_create(brgpu_handle** out, int device) {
         cudaMallocHost(&h->hcnt, sizeof(unsigned long long) * 4) != cudaSuccess ||
         cudaMalloc(&h->dsmall, sizeof(int) * 4) != cudaSuccess ||
         cudaEventCreate(&h->tev[0]) != cudaSuccess || cudaEventCreate(&h->tev[1]) != cudaSuccess ||
-        cudaEventCreate(&h->tev[2]) != cudaSuccess || cudaEventCreate(&h->tev[3]) != cudaSuccess) {
+        cudaEventCreate(&h->tev[2]) != cudaSuccess || cudaEventCreate(&h->tev[3]) != cudaSuccess ||
+        cudaEventCreate(&h->pev[0]) != cudaSuccess || cudaEventCreate(&h->pev[1]) != cudaSuccess) {
         delete hh;
         return BRGPU_ERR_CUDA;
     }
@@ -1203,7 +1264,6 @@ int brgpu_destroy(brgpu_handle* hh) {
     if (h->sbits) cudaFree(h->sbits);
     if (h->mTol) cudaFree(h->mTol);
     if (h->traceBuf) cudaFree(h->traceBuf);
-    if (h->io) cudaFree(h->io);
     if (h->pinned) cudaFreeHost(h->pinned);
     if (h->hsmall) cudaFreeHost(h->hsmall);
     if (h->hcnt) cudaFreeHost(h->hcnt);
@@ -1211,12 +1271,19 @@ int brgpu_destroy(brgpu_handle* hh) {
     if (h->sigDbl) cudaFree(h->sigDbl);
     if (h->sigInt) cudaFree(h->sigInt);
     for (auto& e : h->tev) if (e) cudaEventDestroy(e);
+    for (auto& e : h->pev) if (e) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete hh;
     return BRGPU_OK;
 }
 
 const char* brgpu_last_error_message(const brgpu_handle* hh) { return hh ? hh->h.err.c_str() : "null handle"; }
+
+static void set_plan_opt(Handle* h, int& field, int v) {
+    if (field == v) return;
+    field = v;
+    if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
+}
 
 int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
     if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
@@ -1226,19 +1293,17 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
             if (v < 5 || v > 32) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "leaf cutoff must be in [5, 32]");
             h->leaf_cutoff = (int)v;
             return BRGPU_OK;
-        case BRGPU_OPT_ZHAT: h->zhat = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
-        case BRGPU_OPT_PATCHED_STOP: h->patched = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        // options that change the plan drop the cached plan (and its graph) only
+        // when their value actually changes, so re-applying the same options is free
+        case BRGPU_OPT_ZHAT: set_plan_opt(h, h->zhat, v != 0); return BRGPU_OK;
+        case BRGPU_OPT_PATCHED_STOP: set_plan_opt(h, h->patched, v != 0); return BRGPU_OK;
         case BRGPU_OPT_USE_GRAPH: h->use_graph = v != 0; return BRGPU_OK;
-        case BRGPU_OPT_SUBTREE: h->subtree = v != 0; if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); } return BRGPU_OK;
+        case BRGPU_OPT_SUBTREE: set_plan_opt(h, h->subtree, v != 0); return BRGPU_OK;
         case BRGPU_OPT_EXACT_PASSES:
-            h->exact = v != 0;
+            set_plan_opt(h, h->exact, v != 0);
             h->w.exact = h->exact;
-            if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
             return BRGPU_OK;
-        case BRGPU_OPT_ROOT_SPLIT:
-            h->root_split = v != 0;
-            if (h->plan) { free_plan(h->plan.get()); h->plan.reset(); }
-            return BRGPU_OK;
+        case BRGPU_OPT_ROOT_SPLIT: set_plan_opt(h, h->root_split, v != 0); return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -1274,18 +1339,22 @@ int brgpu_workspace_query(int64_t n, int64_t* doubles, int64_t* ints) {
 int brgpu_reserve(brgpu_handle* hh, int64_t n) {
     if (!hh || n <= 0) return BRGPU_ERR_INVALID_ARGUMENT;
     cudaSetDevice(hh->h.device);
-    return ensure_work(&hh->h, n);
+    return ensure_work(&hh->h, work_need(&hh->h, n));
 }
 
 int brgpu_get_ledger(const brgpu_handle* hh, brgpu_ledger* out) {
     if (!hh || !out) return BRGPU_ERR_INVALID_ARGUMENT;
     const Handle* h = &hh->h;
-    out->live_doubles = h->ledger_doubles;
-    out->peak_doubles = h->peak_doubles;
-    out->live_ints = h->ledger_ints + (h->plan ? (int64_t)h->plan->devInts : 0) + 2 * h->mTolCap;
-    out->peak_ints = std::max(h->peak_ints, out->live_ints);
+    int64_t dbl = 0, ints = 0;
+    ledger_now(h, dbl, ints);
+    out->live_doubles = dbl;
+    out->peak_doubles = std::max(h->peak_doubles, dbl);
+    out->live_ints = ints;
+    out->peak_ints = std::max(h->peak_ints, ints);
     out->limit_doubles = 16 * h->limit_n;
     out->limit_ints = 7 * h->limit_n;
+    out->rows_doubles = h->sigDblCap;
+    out->rows_ints = h->sigIntCap;
     return BRGPU_OK;
 }
 
@@ -1293,12 +1362,15 @@ int brgpu_eigvals(brgpu_handle* hh, int64_t n, const double* d, const double* e,
     if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
     Handle* h = &hh->h;
     if (n <= 0 || !d || !w || (n > 1 && !e)) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be positive");
+    if (n >= (int64_t)1 << 31) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "tridiagonal: order must be < 2^31");
     CUDA_TRY(h, cudaSetDevice(h->device));
-    if (int r = ensure_buf(h, h->io, h->ioCap, 2 * n)) return r;
+    if (int r = ensure_work(h, work_need(h, n))) return r;
+    // host buffers are staged in workspace arrays that are dead until the first
+    // merge (D, Z), so the host path needs no memory beyond the 15N arena
     cudaStream_t s = h->stream;
-    CUDA_TRY(h, cudaMemcpyAsync(h->io, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->io + n, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, s));
-    return solve_device(h, n, h->io, h->io + n, w, true);
+    CUDA_TRY(h, cudaMemcpyAsync(h->w.D, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->w.Z, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, s));
+    return solve_device(h, n, h->w.D, h->w.Z, w, true);
 }
 
 int brgpu_eigvals_device(brgpu_handle* hh, int64_t n, const double* d, const double* e, double* w,
@@ -1360,7 +1432,8 @@ int brgpu_eigvals_rows(brgpu_handle* hh, int64_t n, const double* d, const doubl
     int* ib = h->sigInt;
     std::vector<int> s32(sr.sel.begin(), sr.sel.end());
     int rc = BRGPU_OK;
-    if (cudaMemcpy(ib, s32.data(), sizeof(int) * (size_t)nsel, cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaMemcpyAsync(ib, s32.data(), sizeof(int) * (size_t)nsel, cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
         rc = fail(h, BRGPU_ERR_CUDA, "selected rows: copy of the request failed");
     sr.dev.nsel = (int)nsel;
     sr.dev.stride = c;
@@ -1378,7 +1451,8 @@ int brgpu_eigvals_rows(brgpu_handle* hh, int64_t n, const double* d, const doubl
         h->sig = &sr;
         rc = brgpu_eigvals(hh, n, d, e, w);
         h->sig = nullptr;
-        if (!rc && cudaMemcpy(rows, sr.out, sizeof(double) * (size_t)(nsel * n), cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (!rc && (cudaMemcpyAsync(rows, sr.out, sizeof(double) * (size_t)(nsel * n), cudaMemcpyDeviceToHost,
+                                    h->stream) != cudaSuccess || cudaStreamSynchronize(h->stream) != cudaSuccess))
             rc = fail(h, BRGPU_ERR_CUDA, "selected rows: copy of the rows failed");
     }
     return rc;
@@ -1477,7 +1551,7 @@ int brgpu_eigvals_batched_device(brgpu_handle* hh, int64_t batch, int64_t n, con
         CUDA_TRY(h, cudaStreamWaitEvent(h->stream, ev, 0));
         cudaEventDestroy(ev);
     }
-    if (int r = ensure_work(h, N)) return r;
+    if (int r = ensure_work(h, work_need(h, N))) return r;
     cudaStream_t s = h->stream;
     CUDA_TRY(h, cudaMemsetAsync(h->dsmall, 0, sizeof(int) * 2, s));
     CUDA_TRY(h, cudaMemsetAsync(h->w.status, 0, sizeof(int), s));
@@ -1499,14 +1573,18 @@ int brgpu_eigvals_batched(brgpu_handle* hh, int64_t batch, int64_t n, const doub
     Handle* h = &hh->h;
     if (batch <= 0 || n <= 0 || !d || !w || (n > 1 && !e)) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "batched: bad sizes");
     const int64_t N = batch * n;
+    if (N >= (int64_t)1 << 31) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "batched: batch*n must be < 2^31");
     CUDA_TRY(h, cudaSetDevice(h->device));
-    if (int r = ensure_buf(h, h->io, h->ioCap, 3 * N)) return r;
+    if (int r = ensure_work(h, work_need(h, N))) return r;
+    // staged in the workspace's D / Z arrays (dead until the first merge); the
+    // result is read straight from lam
     cudaStream_t s = h->stream;
-    CUDA_TRY(h, cudaMemcpyAsync(h->io, d, sizeof(double) * N, cudaMemcpyHostToDevice, s));
-    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->io + N, e, sizeof(double) * batch * (n - 1), cudaMemcpyHostToDevice, s));
-    int r = brgpu_eigvals_batched_device(hh, batch, n, h->io, h->io + N, h->io + 2 * N, nullptr);
+    CUDA_TRY(h, cudaMemcpyAsync(h->w.D, d, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->w.Z, e, sizeof(double) * batch * (n - 1), cudaMemcpyHostToDevice, s));
+    int r = brgpu_eigvals_batched_device(hh, batch, n, h->w.D, h->w.Z, h->w.lam, nullptr);
     if (r) return r;
-    CUDA_TRY(h, cudaMemcpy(w, h->io + 2 * N, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    CUDA_TRY(h, cudaMemcpyAsync(w, h->w.lam, sizeof(double) * N, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaStreamSynchronize(s));
     return BRGPU_OK;
 }
 
@@ -1543,6 +1621,11 @@ static int profile_impl(brgpu_handle* hh, int64_t batch, int64_t n, const double
     if (!hh || !class_ms || !class_launches) return BRGPU_ERR_INVALID_ARGUMENT;
     Handle* h = &hh->h;
     CUDA_TRY(h, cudaSetDevice(h->device));
+    if (n <= 0 || batch < 0 || (batch && n > (((int64_t)1 << 31) - 1) / batch))
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "profile: bad sizes");
+    // the result lands in the workspace's own lam array: size the workspace
+    // first, so a fresh (or smaller) handle never hands out a null or stale pointer
+    if (int r0 = ensure_work(h, work_need(h, batch ? batch * n : n))) return r0;
     Prof prof;
     h->prof = &prof;
     const int r = batch ? brgpu_eigvals_batched_device(hh, batch, n, d, e, h->w.lam, nullptr)
@@ -1551,10 +1634,12 @@ static int profile_impl(brgpu_handle* hh, int64_t batch, int64_t n, const double
     for (int c = 0; c < BRGPU_NCLASS; ++c) { class_ms[c] = 0.0; class_launches[c] = 0; }
     if (r == BRGPU_OK) {
         cudaStreamSynchronize(h->stream);
+        const bool dump = std::getenv("BRGPU_PROF_DUMP") != nullptr;  // per-mark listing (tooling)
         for (size_t i = 1; i < prof.ev.size(); ++i) {
             float ms = 0.f;
             cudaEventElapsedTime(&ms, prof.ev[i - 1], prof.ev[i]);
             const int c = prof.cls[i];
+            if (dump) std::fprintf(stderr, "[prof] %zu %s %.4f\n", i, brgpu_kernel_class_name(c), ms);
             if (c >= 0 && c < BRGPU_NCLASS) { class_ms[c] += ms; class_launches[c] += 1; }
         }
     }

@@ -42,13 +42,19 @@ def _build(tmp_path, src, extra=()):
     return exe
 
 
-def test_cpp_wrapper_builds_and_runs(tmp_path):
+@pytest.mark.gpu
+def test_cpp_wrapper_builds_and_runs_on_gpu(tmp_path):
+    exe = _build(tmp_path, PROG)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120).stdout
+    assert out.startswith("ok 1.75 2.25") and "invalid-argument" in out
+
+
+def test_cpp_wrapper_builds_and_fails_loudly_without_gpu(tmp_path):
     exe = _build(tmp_path, PROG)
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120).stdout
     if has_gpu():
-        assert out.startswith("ok 1.75 2.25") and "invalid-argument" in out
-    else:
-        assert out.startswith("device-error")
+        pytest.skip("GPU present: covered by the gpu-marked test")
+    assert out.startswith("device-error")
 
 
 @pytest.mark.skipif(not REF_INC.exists(), reason="reference headers not present")

@@ -199,3 +199,23 @@ def test_gpu_arith_extreme_scales(fam, n, scale):
     assert np.all(np.isfinite(w))
     truth = sl.eigvalsh_tridiagonal(d / scale, e / scale) * scale
     assert np.max(np.abs(w - truth)) <= G.tolerance(d, e) * (1 + 1e-12) + 64 * 2.0 ** -1074
+
+
+CG = np.load(Path(__file__).parent / "golden" / "config_vectors.npz")
+CNAMES = [str(x) for x in CG["names"]]
+
+
+@pytest.mark.parametrize("key", CNAMES)
+def test_checker_pinned_at_config_sizes(key):
+    """BASELINE config 1 (sym-uniform:4096) and every family at 2048 / 4096
+    (tests/golden/config_vectors.npz, from the reference itself): reference-arithmetic
+    mode reproduces the reference BR composition bit for bit; the product's
+    arithmetic is within 8 n eps ||T|| of the reference's qrql and Jacobi solvers."""
+    fam, n = key.split(":")
+    d, e = G.generate(fam, int(n))
+    assert np.array_equal(O.eigvals(d, e, ref_arith=True, patched=False).w, CG[key + ":br"])
+    w = O.eigvals(d, e).w
+    tol = G.tolerance(d, e)
+    assert np.max(np.abs(w - CG[key + ":qrql"])) <= tol
+    if key + ":dense" in CG:
+        assert np.max(np.abs(w - CG[key + ":dense"])) <= tol
