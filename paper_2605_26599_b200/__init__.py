@@ -135,6 +135,7 @@ class BrOptions:
     virtual_ranks: int = 1  # >1: run the multi-GPU decomposition on this device (test mode)
     exact_passes: bool = False  # test hook: every pole pass through the exact-reciprocal path
     root_split: bool = True  # multi-rank: split the shared top merges' roots across ranks
+    sparse: bool = False  # opt-in: grid levels with <= C non-negligible poles per merge run the sparse pipeline
 
 
 @dataclass
@@ -224,6 +225,7 @@ class Solver:
         self._opt(_native.OPT_SUBTREE, int(o.subtree))
         self._opt(_native.OPT_EXACT_PASSES, int(o.exact_passes))
         self._opt(_native.OPT_ROOT_SPLIT, int(o.root_split))
+        self._opt(_native.OPT_SPARSE, int(o.sparse))
         if self.nranks == 1:
             self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o

@@ -22,6 +22,7 @@ OPT_SUBTREE = 5
 OPT_VIRTUAL_RANKS = 6
 OPT_EXACT_PASSES = 7
 OPT_ROOT_SPLIT = 8
+OPT_SPARSE = 9
 
 
 class Stats(C.Structure):
@@ -57,7 +58,7 @@ EXPORTS = [
     "brgpu_phase_cycles", "brgpu_eigvals_dense_device", "brgpu_eigvals_rows",
 ]
 
-NCLASS = 17
+NCLASS = 20
 
 
 class Timing(C.Structure):

@@ -44,8 +44,17 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
 int level_exchange_arrays(const SolveParams& prm, int part);
 void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n, int* out,
                         int* launches, Prof* prof);
+void launch_level_sparse(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
+                         int* blockCnt, int* traceOut, int* launches, Prof* prof);
+void launch_state_home(cudaStream_t s, const Work& w, const LevelDev& E, int n, int sms, int* launches);
+void init_sparse_attributes();
+int sparse_cap();
+int sparse_groups_max(int n, int M, int span);
+int sparse_min_merge();
+int sparse_flag_grid(int n, int sms);
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
-                   const unsigned long long* sbits, double* lam, int* launches, Prof* prof);
+                   const unsigned long long* sbits, double* lam, const double* alt, const LevelDev& E,
+                   int* launches, Prof* prof);
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
                        int nruns, int* launches, Prof* prof);
 void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
@@ -66,6 +75,7 @@ constexpr int kGridManyPerSm = 4;  // 1024-shape levels with >= 4 merges per SM 
 #endif
 constexpr int kGridManyMinSize = BRGPU_GRID_MANY_MIN_SIZE;  // ... when their merges exceed this size  // largest merge of a fused SMEM level (512 or 1024)
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
+constexpr int kSpMinSpan = 16;        // smallest k_sp_solve group key span (group table size)
 #ifndef BRGPU_SPLIT_MIN_SIZE
 #define BRGPU_SPLIT_MIN_SIZE 8192
 #endif
@@ -111,6 +121,11 @@ struct LevelHost {
     int cap;     // group capacity (elements): 512 (small shape) or 1024
     int minSize; // smallest merge of the level
     int maxSize; // largest merge of the level
+    int sp = 0;        // sparse-capable grid level (sparse.cu; device-side decision)
+    int spStatic = 0;  // every merge <= the sparse cap: sparse always, no dense kernels
+    int spCap = 0;     // sparse iff every merge has NN <= spCap
+    int spSpan = 0;    // k_sp_solve group key span
+    int ctl = 0;       // index of the level's control words (4 ints)
 };
 
 struct Plan {
@@ -149,6 +164,17 @@ struct Plan {
     int *d_mOff = nullptr, *d_mSize = nullptr, *d_mNL = nullptr, *d_mFlags = nullptr;
     int *d_tileFirst = nullptr, *d_bstart = nullptr, *d_gFirst = nullptr, *d_gCount = nullptr;
     std::vector<int*> d_runs;
+    // sparse levels: control words (4 per level + a zero block), per-merge
+    // tables (spCs, spCsR, spNN, spK: 4 per merge), group starts, per-CTA counts
+    int* d_ctl = nullptr;
+    int nctl = 0;
+    int* d_spTab = nullptr;
+    int* d_spGroup = nullptr;
+    int* d_blockCnt = nullptr;
+    int* d_spTiles = nullptr;  // k_sp_place tile records: merge + split per 1024 positions
+    int* h_ctl = nullptr;  // pinned copy of the control words after a solve (deflation profile)
+    int dbgStop = 0;       // debug (BRGPU_DEBUG_STOP_LEVEL): run only the first k levels of phase 1
+    bool anySp = false;
     cudaGraphExec_t graph = nullptr;
     bool graph_trace = false;
     uint64_t graph_gen = 0;
@@ -165,6 +191,7 @@ struct Handle {
     int patched = 1;
     int use_graph = 1;
     int subtree = 1;
+    int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
     int exact = 0;
     int trace = 0;
     double tol_scale = 1.0;
@@ -402,7 +429,7 @@ void plan_fused_runs(Plan* p) {
 // subtree; smaller blocks go to ranks in contiguous chunks of the total size.
 std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
                                 const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0,
-                                int sms = 148) {
+                                int sms = 148, bool sparse = false) {
     auto p = std::make_unique<Plan>();
     p->n = n;
     p->sms = sms;
@@ -467,6 +494,21 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
     add_levels(p.get(), mine, fuse, p->levels);
     add_levels(p.get(), top, fuse, p->levels2);
     plan_fused_runs(p.get());
+    // control words per level; phase-1 grid levels may run the sparse pipeline
+    // (sparse.cu); the shared top merges of a multi-rank plan stay dense (their
+    // roots are split across ranks by the dense kernels)
+    {
+        int ci = 0;
+        for (LevelHost& lh : p->levels) {
+            lh.ctl = 4 * ci++;
+            // k_sp_place bounds its merge segments per tile by the smallest merge
+            lh.sp = sparse && !lh.fused && lh.minSize >= sparse_min_merge() ? 1 : 0;
+            lh.spCap = sparse_cap();
+            lh.spSpan = 2 * sparse_cap() - lh.spCap;
+            lh.spStatic = lh.sp && lh.maxSize <= lh.spCap ? 1 : 0;
+        }
+        for (LevelHost& lh : p->levels2) lh.ctl = 4 * ci++;
+    }
     // final merge passes: runs = blocks, merged pairwise inside each segment;
     // a segment with an odd run count gets an empty partner so that pairs
     // (2k, 2k+1) of a pass table never straddle segments.
@@ -522,6 +564,19 @@ int upload_plan(Handle* h, Plan* p) {
     const size_t oML = put(p->mlTab);  // int2 pairs: 8-byte aligned (offsets are multiples of 4 ints)
     std::vector<size_t> oRuns;
     for (auto& rp : p->runPasses) oRuns.push_back(put(rp));
+    p->nctl = 4 * (int)(p->levels.size() + p->levels2.size() + 1);
+    const size_t oCtl = put(std::vector<int>((size_t)p->nctl, 0));
+    int ngMax = 1;
+    bool anySp = false;
+    for (const auto* lv : {&p->levels, &p->levels2})
+        for (const LevelHost& lh : *lv)
+            if (lh.sp) { anySp = true; ngMax = std::max(ngMax, sparse_groups_max(p->n, lh.M, kSpMinSpan)); }
+    p->anySp = anySp;
+    const size_t oSpTab = put(std::vector<int>(anySp ? 4 * p->mOff.size() : 0, 0));
+    const size_t oSpGroup = put(std::vector<int>(anySp ? (size_t)ngMax + 1 : 0, 0));
+    const size_t oBlk = put(std::vector<int>(anySp ? (size_t)sparse_flag_grid(p->n, p->sms) : 0, 0));
+    const size_t oTiles = put(std::vector<int>(anySp ? 2 * (size_t)(p->n / 1024 + 2) : 0, 0));
+    if (anySp) CUDA_TRY(h, cudaMallocHost(&p->h_ctl, sizeof(int) * (size_t)p->nctl));
     p->devInts = buf.size();
     CUDA_TRY(h, cudaMalloc(&p->dev, sizeof(int) * std::max<size_t>(buf.size(), 1)));
     if (int r = h2d_sync(h, p->dev, buf.data(), sizeof(int) * buf.size())) return r;
@@ -532,6 +587,11 @@ int upload_plan(Handle* h, Plan* p) {
     p->d_gFirst = p->dev + oGF; p->d_gCount = p->dev + oGC;
     p->d_mlTab = reinterpret_cast<int2*>(p->dev + oML);
     for (size_t o : oRuns) p->d_runs.push_back(p->dev + o);
+    p->d_ctl = p->dev + oCtl;
+    p->d_spTab = p->dev + oSpTab;
+    p->d_spGroup = p->dev + oSpGroup;
+    p->d_blockCnt = p->dev + oBlk;
+    p->d_spTiles = p->dev + oTiles;
     return BRGPU_OK;
 }
 
@@ -539,6 +599,8 @@ void free_plan(Plan* p) {
     if (!p) return;
     if (p->graph) cudaGraphExecDestroy(p->graph);
     if (p->dev) cudaFree(p->dev);
+    if (p->h_ctl) cudaFreeHost(p->h_ctl);
+    p->h_ctl = nullptr;
     p->graph = nullptr;
     p->dev = nullptr;
 }
@@ -644,8 +706,8 @@ int status_message(Handle* h, int st) {
     }
 }
 
-LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh) {
-    LevelDev L;
+LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh, const LevelHost* prev = nullptr) {
+    LevelDev L{};
     L.mOff = p->d_mOff + lh.m0;
     L.mSize = p->d_mSize + lh.m0;
     L.mNL = p->d_mNL + lh.m0;
@@ -655,7 +717,37 @@ LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh) {
     L.M = lh.M;
     L.allSplit = lh.minSize > kSplitMinSizeHost ? 1 : 0;
     L.maxSize = lh.maxSize;
+    // plans without sparse levels keep the state in slot 0: no control words
+    L.ctl = p->anySp ? p->d_ctl + lh.ctl : nullptr;
+    L.pctl = p->anySp && prev ? p->d_ctl + prev->ctl : nullptr;
+    L.pcap = (prev && prev->sp) ? prev->spCap : 0;
+    L.spCap = lh.sp ? lh.spCap : 0;
+    L.spStatic = lh.spStatic;
+    L.spSpan = lh.spSpan;
+    if (lh.sp) {
+        const size_t M = p->mOff.size();
+        L.spCs = p->d_spTab + lh.m0;
+        L.spCsR = p->d_spTab + M + lh.m0;
+        L.spNN = p->d_spTab + 2 * M + lh.m0;
+        L.spK = p->d_spTab + 3 * M + lh.m0;
+        L.spGroup = p->d_spGroup;
+        L.spTileM = p->d_spTiles;
+        L.spTileSplit = p->d_spTiles + (p->n / 1024 + 2);
+    }
     return L;
+}
+
+// Words describing the state slot after the last level of `levels` (the
+// previous-level fields only), for k_rescale / k_state_home.
+LevelDev end_words(Plan* p, const std::vector<LevelHost>& levels) {
+    LevelDev E{};
+    if (!levels.empty()) {
+        const LevelHost& lh = p->dbgStop > 0 && &levels == &p->levels && (size_t)p->dbgStop <= levels.size()
+                                  ? levels[(size_t)p->dbgStop - 1] : levels.back();
+        E.pctl = p->anySp ? p->d_ctl + lh.ctl : nullptr;
+        E.pcap = lh.sp ? lh.spCap : 0;
+    }
+    return E;
 }
 
 SolveParams solve_params(Handle* h, int n) {
@@ -707,15 +799,21 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
     SolveParams prm = solve_params(h, n);
     const bool phase1 = &levels == &p->levels;
     size_t mr = 0;
+    {
+        const char* ev = std::getenv("BRGPU_DEBUG_STOP_LEVEL");
+        p->dbgStop = ev ? std::atoi(ev) : 0;
+    }
     for (size_t li = 0; li < levels.size(); ++li) {
+        if (phase1 && p->dbgStop > 0 && li >= (size_t)p->dbgStop) break;
         const LevelHost& lh = levels[li];
+        const LevelHost* prev = li ? &levels[li - 1] : nullptr;
         if (phase1 && mr < p->multi.size() && p->multi[mr].lev0 == (int)li) {
             const Plan::MultiRun& run = p->multi[mr++];
             FusedRun fr{};
             fr.nlev = run.nlev;
             for (int l = 0; l < run.nlev; ++l) {
                 const LevelHost& ll = levels[li + (size_t)l];
-                fr.L[l] = level_dev(h, p, ll);
+                fr.L[l] = level_dev(h, p, ll, l ? &levels[li + (size_t)l - 1] : prev);
                 fr.trace[l] = h->trace ? h->traceBuf + 2 * ll.m0 : nullptr;
             }
             set_split(h, nullptr, prm);
@@ -724,21 +822,27 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
             li += (size_t)run.nlev - 1;
             continue;
         }
-        const LevelDev L = level_dev(h, p, lh);
+        const LevelDev L = level_dev(h, p, lh, prev);
         if (lh.fused) {
             set_split(h, nullptr, prm);
             launch_level_fused(s, h->w, L, lh.G, lh.cap, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
                                h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
-        } else {
-            set_split(h, sc, prm);
-            for (int part = 0; part < 4; ++part) {
-                launch_level_part(s, h->w, L, n, prm, part, launches, prof);
-                if (const int k = level_exchange_arrays(prm, part))
-                    if (const int e = exchange_allgather(h, *sc, k)) h->xerr = h->xerr ? h->xerr : e;
-            }
-            set_split(h, nullptr, prm);
-            if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
+            continue;
         }
+        if (lh.sp) {
+            set_split(h, nullptr, prm);
+            launch_level_sparse(s, h->w, L, n, prm, p->d_blockCnt, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr,
+                                launches, prof);
+            if (lh.spStatic) continue;
+        }
+        set_split(h, sc, prm);
+        for (int part = 0; part < 4; ++part) {
+            launch_level_part(s, h->w, L, n, prm, part, launches, prof);
+            if (const int k = level_exchange_arrays(prm, part))
+                if (const int e = exchange_allgather(h, *sc, k)) h->xerr = h->xerr ? h->xerr : e;
+        }
+        set_split(h, nullptr, prm);
+        if (h->trace) launch_level_trace(s, h->w, L, n, h->traceBuf + 2 * lh.m0, launches, prof);
     }
 }
 
@@ -748,6 +852,7 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     if (prof) prof_mark(prof, (void*)s, -1);
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
+    if (p->anySp) cudaMemsetAsync(p->d_ctl, 0, sizeof(int) * (size_t)p->nctl, s);  // level words (barrier counters)
     launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
                    p->d_cut, launches, prof);
     launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
@@ -755,6 +860,8 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     if (h->sig)
         launch_sigma_leaves(s, h->sig->dev, p->maxLeaf, h->sig->dTask, p->d_tOff, p->d_tSize, h->w, launches);
     run_levels(h, p, p->levels, launches, prof);
+    // a phase exchange moves (lam, blo, bhi): bring the state home to slot 0
+    if (p->nranks > 1) launch_state_home(s, h->w, end_words(p, p->levels), n, h->sms, launches);
 }
 
 // Stage B: shared top merges (roots split across ranks when enabled),
@@ -773,7 +880,8 @@ void finish_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
     cudaStream_t s = h->stream;
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
-    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
+    const LevelDev E = end_words(p, p->levels2.empty() ? p->levels : p->levels2);
+    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, h->w.D, E, launches, prof);
     if (h->sig)
         launch_sigma_final(s, h->sig->dev, h->w.lam, p->d_bstart, nblk, h->sig->dBlk, h->sig->maxBlock,
                            h->sig->out, n, launches);
@@ -908,12 +1016,13 @@ int solve_virtual(Handle* h, int n, const std::vector<int>& bstart, const std::v
         u->use_graph = 0; u->subtree = h->subtree; u->trace = 0; u->exact = h->exact; u->w.exact = h->exact; u->tol_scale = h->tol_scale;
         u->sec_grid = h->sec_grid;
         u->root_split = h->root_split;
+        u->sparse = h->sparse;
         if (int r = ensure_work(u, (int64_t)n + P)) return fail(h, r, u->err);  // split slots always fit
         u->w.status = h->w.status;
         u->w.counters = h->w.counters;
         CUDA_TRY(h, cudaMemcpyAsync(u->w.dw, h->w.dw, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
         CUDA_TRY(h, cudaMemcpyAsync(u->w.ew, h->w.ew, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-        plans.push_back(make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, P, k, h->sms));
+        plans.push_back(make_plan(n, h->leaf_cutoff, bstart, segs, h->subtree != 0, P, k, h->sms, h->sparse != 0));
         if (int r = upload_plan(u, plans.back().get())) return fail(h, r, u->err);
         if (int r = ensure_buf_sizes(u, plans.back().get())) return fail(h, r, u->err);
         CUDA_TRY(h, cudaMemsetAsync(u->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
@@ -1023,7 +1132,8 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs ||
         p->sigma != sig) {
         if (h->plan) free_plan(h->plan.get());
-        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0, h->nranks, h->rank, h->sms);
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0, h->nranks, h->rank, h->sms,
+                            !sig && h->sparse != 0);
         p = h->plan.get();
         if (sig) {  // every merge propagates the requested rows: no root-only mode
             p->sigma = true;
@@ -1084,6 +1194,8 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
         h->stats.graph_replayed = 0;
     }
     CUDA_TRY(h, cudaEventRecord(h->tev[3], s));
+    if (p->anySp && p->h_ctl)  // the deflation profile of this solve (adapt_sparse, after the sync)
+        CUDA_TRY(h, cudaMemcpyAsync(p->h_ctl, p->d_ctl, sizeof(int) * (size_t)p->nctl, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaGetLastError());
     h->stats.kernel_launches = launches + 2;  // + input copy and scan
     h->stats.n = n;
@@ -1093,12 +1205,52 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     return BRGPU_OK;
 }
 
+// Sparse-level configuration from the deflation profile of the last solve
+// (k_sp_flag's per-level words: largest NN of a merge, total NN): the cap C
+// becomes the next power of two >= max NN (>= the level's merge size when that
+// is <= 1024, so such levels stay dense-free), and the group span fills the SMs
+// with whole waves of k_sp_solve groups.  Results never depend on it: a level
+// whose merges exceed its cap runs the dense pipeline.  A changed configuration
+// drops the captured graph (re-captured by the next solve).
+void adapt_sparse(Handle* h, Plan* p) {
+    if (!p || !p->anySp || !p->h_ctl) return;
+    const int capMax = sparse_cap(), room0 = 2 * sparse_cap();
+    bool changed = false;
+    for (LevelHost& lh : p->levels) {
+        if (!lh.sp) continue;
+        const int maxNN = p->h_ctl[lh.ctl + 1], tot = p->h_ctl[lh.ctl + 3];
+        int cap = capMax, span = room0 - capMax;
+        if (maxNN <= capMax && tot >= 0) {
+            cap = 64;
+            while (cap < maxNN) cap <<= 1;
+            if (lh.maxSize <= capMax) while (cap < lh.maxSize) cap <<= 1;
+            cap = std::min(cap, capMax);
+            const int room = room0 - cap;
+            const long long keys = (long long)tot + 4LL * lh.M;
+            long long groups = std::max<long long>(1, (keys + room - 1) / room);
+            groups = (groups + h->sms - 1) / h->sms * h->sms;
+            span = (int)std::max<long long>(kSpMinSpan, std::min<long long>(room, keys / groups));
+        }
+        if (cap != lh.spCap || span != lh.spSpan) {
+            lh.spCap = cap;
+            lh.spSpan = span;
+            lh.spStatic = lh.maxSize <= cap ? 1 : 0;
+            changed = true;
+        }
+    }
+    if (changed && p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+}
+
 int finish_solve(Handle* h) {
     cudaStream_t s = h->stream;
     ledger_peak(h);
     CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
+    if (h->virt <= 1) adapt_sparse(h, h->plan.get());
     {
         // both pairs are recorded on every path; a failure here must not leave a
         // pending error for the next CUDA_TRY (of this or any other handle)
@@ -1237,6 +1389,7 @@ int brgpu_create(brgpu_handle** out, int device) {
     }
     brgpu::init_kernel_attributes();
     brgpu::init_fused_attributes();
+    brgpu::init_sparse_attributes();
     brgpu::init_warp_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
@@ -1304,6 +1457,7 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
             h->w.exact = h->exact;
             return BRGPU_OK;
         case BRGPU_OPT_ROOT_SPLIT: set_plan_opt(h, h->root_split, v != 0); return BRGPU_OK;
+        case BRGPU_OPT_SPARSE: set_plan_opt(h, h->sparse, v != 0); return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -1325,6 +1479,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_VIRTUAL_RANKS: *v = h->virt; return BRGPU_OK;
         case BRGPU_OPT_ROOT_SPLIT: *v = h->root_split; return BRGPU_OK;
         case BRGPU_OPT_EXACT_PASSES: *v = h->exact; return BRGPU_OK;
+        case BRGPU_OPT_SPARSE: *v = h->sparse; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }
 }
@@ -1612,7 +1767,7 @@ const char* brgpu_kernel_class_name(int c) {
     static const char* names[BRGPU_NCLASS] = {
         "prepare(scale+cuts)", "leaf", "merge_tol", "merge_scatter", "nn_flag", "scan_tiles",
         "nn_write", "segment_walk", "surv_count", "surv_write", "secular", "zhat", "rows",
-        "deflated_out", "trace", "finish", "fused_level"};
+        "deflated_out", "trace", "finish", "fused_level", "sparse_flag", "sparse_solve", "sparse_place"};
     return (c >= 0 && c < BRGPU_NCLASS) ? names[c] : "?";
 }
 

@@ -19,6 +19,8 @@
 #include "internal.hpp"
 #include "launch.cuh"
 #include "numerics.cuh"
+#include "grid_common.cuh"
+#include "level_state.cuh"
 
 namespace brgpu {
 
@@ -68,68 +70,6 @@ struct FuseSmem {
     int cnt;
     unsigned long long evals, terms;
 };
-
-template <int kFuseThreads>
-__device__ __forceinline__ int cta_excl_scan(int v, int& total, int* warp_tot) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    constexpr int NW = kFuseThreads / 32;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        int t = lane < NW ? warp_tot[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, t, o);
-            if (lane >= o) t += y;
-        }
-        if (lane < NW) warp_tot[lane] = t;
-    }
-    __syncthreads();
-    const int base = wid ? warp_tot[wid - 1] : 0;
-    total = warp_tot[NW - 1];
-    __syncthreads();
-    return base + x - v;
-}
-
-// exclusive prefix of flags[0..E) into pre[0..E]; each thread scans a contiguous chunk
-template <int kFuseThreads>
-__device__ __forceinline__ int cta_scan_flags(const unsigned char* flags, int E, int* pre, int* warp_tot) {
-    const int per = (E + kFuseThreads - 1) / kFuseThreads;
-    const int i0 = threadIdx.x * per;
-    int local = 0;
-    for (int k = 0; k < per; ++k) {
-        const int i = i0 + k;
-        if (i < E) local += flags[i];
-    }
-    int tot;
-    int run = cta_excl_scan<kFuseThreads>(local, tot, warp_tot);
-    for (int k = 0; k < per; ++k) {
-        const int i = i0 + k;
-        if (i < E) {
-            pre[i] = run;
-            run += flags[i];
-        }
-    }
-    if (threadIdx.x == 0) pre[E] = tot;
-    __syncthreads();
-    return tot;
-}
-
-// largest t in [0, cnt) with a[t] <= x
-__device__ __forceinline__ int upper_index(const int* a, int cnt, int x) {
-    int lo = 0, hi = cnt;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] <= x) lo = mid; else hi = mid;
-    }
-    return lo;
-}
 
 // One group of merges of one level: merges m0 .. m0+cnt-1 (level-local
 // indices) tile a contiguous range; state in and out through w.lam/blo/bhi.
@@ -511,9 +451,12 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
 
 template <int kFuseMax, int kFuseThreads>
 __global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
-k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
+k_level_fused(Work w0, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
               SolveParams prm, int* __restrict__ traceOut) {
     pdl_entry();
+    const int slot = slot_from_prev(L);  // first (only) kernel of the level: publish the state slot
+    if (blockIdx.x == 0 && threadIdx.x == 0 && L.ctl) L.ctl[0] = slot;
+    const Work w = with_slot(w0, slot);
     extern __shared__ __align__(16) unsigned char fuse_raw[];
     using Smem = FuseSmem<kFuseMax, kFuseThreads>;
     Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
@@ -528,8 +471,13 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
 // and different CTAs' root-queue tails overlap across levels.
 template <int kFuseMax, int kFuseThreads>
 __global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
-k_levels_fused(Work w, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
+k_levels_fused(Work w0, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
     pdl_entry();
+    const int slot = slot_from_prev(run.L[0]);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (int l = 0; l < run.nlev; ++l)
+            if (run.L[l].ctl) run.L[l].ctl[0] = slot;
+    const Work w = with_slot(w0, slot);
     extern __shared__ __align__(16) unsigned char fuse_raw[];
     using Smem = FuseSmem<kFuseMax, kFuseThreads>;
     Smem& S = *reinterpret_cast<Smem*>(fuse_raw);

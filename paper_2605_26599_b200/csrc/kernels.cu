@@ -20,79 +20,10 @@
 #include "internal.hpp"
 #include "launch.cuh"
 #include "numerics.cuh"
+#include "grid_common.cuh"
+#include "level_state.cuh"
 
 namespace brgpu {
-
-// ---------------------------------------------------------------------------
-// helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int find_merge(const LevelDev& L, int p) {
-    const int t = p / kTile;
-    int m = L.tileFirst[t];
-    const int last = L.tileFirst[t + 1] < L.M ? L.tileFirst[t + 1] : L.M - 1;
-    while (m < last && L.mOff[m + 1] <= p) ++m;
-    if (m >= L.M || m < 0) return -1;
-    const int off = L.mOff[m];
-    if (p < off || p >= off + L.mSize[m]) return -1;
-    return m;
-}
-
-__device__ __forceinline__ double merge_tol(const LevelDev& L, int m, double tol_scale) {
-    const double mx = __longlong_as_double((long long)L.mTol[m]);
-    return 8.0 * kU * mx * tol_scale;
-}
-
-// Active range [ks, ke) of merge m in the level-global compacted arrays.
-__device__ __forceinline__ void active_range(const Work& w, const LevelDev& L, int m, int& ks, int& ke) {
-    const int off = L.mOff[m];
-    ks = w.survPre[w.nnPre[off]];
-    ke = w.survPre[w.nnPre[off + L.mSize[m]]];
-}
-
-template <int BLOCK>
-__device__ __forceinline__ int block_exclusive_scan(int v, int& total) {
-    __shared__ int warp_tot[BLOCK / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        int t = lane < BLOCK / 32 ? warp_tot[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, t, o);
-            if (lane >= o) t += y;
-        }
-        if (lane < BLOCK / 32) warp_tot[lane] = t;
-    }
-    __syncthreads();
-    const int base = wid ? warp_tot[wid - 1] : 0;
-    total = warp_tot[BLOCK / 32 - 1];
-    __syncthreads();
-    return base + x - v;
-}
-
-template <int BLOCK>
-__device__ __forceinline__ int block_sum(int v) {
-    __shared__ int red[BLOCK / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[wid] = v;
-    __syncthreads();
-    int t = 0;
-    if (threadIdx.x < 32) {
-        t = lane < BLOCK / 32 ? red[lane] : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    }
-    return t;  // valid in thread 0
-}
 
 constexpr int kScanBlock = 1024;
 
@@ -375,31 +306,6 @@ __device__ __forceinline__ int cta_lookback(unsigned long long* state, int tile,
     return *s_bcast;
 }
 
-// Number of left-child elements among the first d outputs of the stable merge
-// of sorted a[0..nl) (left) and b[0..nr) (right): left element i precedes
-// right element j iff a_i <= b_j (std::stable_sort of the concatenation by
-// '<', deflate.cpp:62-66).  Warp-cooperative 32-ary search (all lanes call it
-// with the same arguments): about log32 of the child size dependent L2 round
-// trips instead of log2.
-__device__ __forceinline__ int warp_merge_split(const double* __restrict__ a, int nl,
-                                                const double* __restrict__ b, int nr, int d) {
-    const int lane = threadIdx.x & 31;
-    int lo = max(0, d - nr), hi = min(d, nl);  // answer in [lo, hi]; pred(i) holds for i <= answer
-    while (hi > lo) {
-        const int span = hi - lo;
-        const int step = (span + 31) >> 5;
-        const int c = min(lo + (lane + 1) * step, hi);
-        const bool pred = (d - c >= nr) || !(b[d - c] < a[c - 1]);  // a[c-1] is within the first d
-        const unsigned bal = __ballot_sync(0xffffffffu, pred);
-        const int k = __popc(bal);  // candidates are monotone: the first k hold
-        if (step == 1) { lo = min(lo + k, hi); break; }  // capped duplicates of hi may add to k
-        const int nlo = k ? min(lo + k * step, hi) : lo;
-        hi = min(hi, lo + (k + 1) * step - 1);
-        lo = nlo;
-    }
-    return lo;
-}
-
 constexpr int kMergeTile = 256;
 constexpr int kPrepVec = 4;  // merge tiles per k_merge_prep CTA: the whole level is one wave
 
@@ -410,8 +316,10 @@ constexpr int kPrepVec = 4;  // merge tiles per k_merge_prep CTA: the whole leve
 //    memory first);
 //  * the merge-path diagonal split at each tile's first position (warp k for
 //    tile k, 32-ary search), kept in split[tile] for k_merge_nn.
-__global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w, LevelDev L, int n, int* __restrict__ split) {
+__global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w0, LevelDev L, int n, int* __restrict__ split) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     __shared__ unsigned long long s_max[kPrepVec][kMergeTile / 32];
     __shared__ int s_m[kPrepVec][kMergeTile / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -488,10 +396,12 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w, LevelDev L, i
 // loaded coalesced at once, placed by searches in shared memory and written
 // back coalesced in merged order.  The tile's flag count (order-free: the same
 // elements) is published before the placement so the look-back overlaps it.
-__global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int n, double tol_scale,
+__global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w0, LevelDev L, int n, double tol_scale,
                                                          const int* __restrict__ split,
                                                          unsigned long long* state, int* ticket) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     // inputs (lam, blo, bhi), then the merged tile (D, Z, R0 alias them; R1)
     __shared__ double s_v[kMergeTile], s_b0[kMergeTile], s_b1[kMergeTile], s_R1[kMergeTile];
     double* s_D = s_v;
@@ -602,8 +512,10 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int
 #define BRGPU_WALK_BATCH 8
 #endif
 constexpr int kWalkBatch = BRGPU_WALK_BATCH;  // NN entries loaded per step of a long segment walk
-__global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
+__global__ void k_segment_walk(Work w0, LevelDev L, int n, double tol_scale) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int NN = w.nnPre[n];
     if (q >= NN) return;
@@ -675,9 +587,11 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
 
 // survivor prefix over NN indices + compacted active problem (deflate.cpp:100-105),
 // one pass; tile 0 always runs so survPre[NN] is written even when NN == 0
-__global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, int n,
+__global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w0, LevelDev L, int n,
                                                           unsigned long long* state, int* ticket) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     __shared__ int s_tile, s_pref;
     const int NN = w.nnPre[n];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -715,20 +629,28 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, in
 }
 
 // Start of a grid-tier level: zero the per-merge scale words, the look-back
-// tile states + tickets and the tier-mode word.
-__global__ void k_level_zero(unsigned long long* __restrict__ mTol, int M, unsigned long long* __restrict__ st,
-                             int words, int* __restrict__ modes, int modes0) {
+// tile states + tickets and the tier-mode word.  On a dense-only level this is
+// the level's first kernel: it publishes the state slot (level_state.cuh).
+__global__ void k_level_zero(LevelDev L, unsigned long long* __restrict__ st, int words, int* __restrict__ modes,
+                             int modes0) {
     pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < M) mTol[i] = 0ULL;
+    if (L.spCap == 0) {
+        if (i == 0 && L.ctl) L.ctl[0] = slot_from_prev(L);
+    } else if (level_sparse(L)) {
+        return;
+    }
+    if (i < L.M) L.mTol[i] = 0ULL;
     if (i < words) st[i] = 0ULL;
     if (i == 0) *modes = modes0;
 }
 
 // Which secular tiers a level needs (merges with K > 0): bit0 lane-per-root,
 // bit1 warp-per-root.  Kernels of an absent tier exit on their first load.
-__global__ void k_level_modes(Work w, LevelDev L) {
+__global__ void k_level_modes(Work w0, LevelDev L) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     int bits = 0;
     if (m < L.M) {
@@ -789,8 +711,10 @@ constexpr int kSecBigLevel = 1 << 21;
 // as soon as its root converges.  Evaluations are branch-free pole loops over
 // shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
 template <int MINB>
-__global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w, LevelDev L, int n, int patched) {
+__global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w0, LevelDev L, int n, int patched) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ double2 s_snap[kSecBlock];
     __shared__ int s_next;
@@ -893,8 +817,10 @@ __global__ void k_selftest_rcp(long long count, unsigned long long seed, unsigne
 // The roots' (d_origin, tau, d_j) triples stream through shared memory in
 // tiles of kWin covering the CTA's window (one tile when it fits), in root
 // order, so the product order is the checker's.
-__global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
+__global__ void __launch_bounds__(kSecBlock) k_zhat(Work w0, LevelDev L, int n) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     __shared__ double s_dorg[kWin], s_tau[kWin], s_dj[kWin];
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -961,8 +887,10 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
 // y = zhat/Delta_j / ||zhat/Delta_j|| streamed (never stored),
 // plus placement of lambda_j in the parent's ascending order.  Poles (d, zhat,
 // r0, r1) stream through shared memory in tiles, in pole order.
-__global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
+__global__ void __launch_bounds__(kSecBlock) k_rows(Work w0, LevelDev L, int n) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     __shared__ double s_d[kWin], s_zh[kWin], s_r0[kWin], s_r1[kWin];
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -1045,8 +973,10 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
 }
 
 // deflated columns: parent position t + #{roots < D}
-__global__ void k_deflated_out(Work w, LevelDev L, int n) {
+__global__ void k_deflated_out(Work w0, LevelDev L, int n) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int m = find_merge(L, k);
@@ -1076,8 +1006,10 @@ __global__ void k_deflated_out(Work w, LevelDev L, int n) {
 }
 
 // per-merge (nn, K) for the trace
-__global__ void k_level_trace(Work w, LevelDev L, int* __restrict__ out) {
+__global__ void k_level_trace(Work w0, LevelDev L, int* __restrict__ out) {
     pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= L.M) return;
     const int off = L.mOff[m], end = off + L.mSize[m];
@@ -1090,13 +1022,26 @@ __global__ void k_level_trace(Work w, LevelDev L, int* __restrict__ out) {
 // rescale + cross-block merge
 // ---------------------------------------------------------------------------
 __global__ void k_rescale(int n, const int* __restrict__ bstart, int nblk,
-                          const unsigned long long* __restrict__ sbits, double* __restrict__ lam) {
+                          const unsigned long long* __restrict__ sbits, double* __restrict__ lam,
+                          const double* __restrict__ alt, LevelDev E) {
     pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const double* src = slot_from_prev(E) ? alt : lam;  // the last level may have left the state in slot 1
     const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
     const double s = block_scale_of(sbits[b]);
-    lam[i] = lam[i] * s;
+    lam[i] = src[i] * s;
+}
+
+// State back to slot 0 (lam, blo, bhi) before a phase exchange (multi-rank plans).
+__global__ void k_state_home(Work w, LevelDev E, int n) {
+    pdl_entry();
+    if (!slot_from_prev(E)) return;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        w.lam[i] = w.D[i];
+        w.blo[i] = w.R0[i];
+        w.bhi[i] = w.R1[i];
+    }
 }
 
 // one pass of a bottom-up stable merge sort over runs [rs[r], rs[r+1])
@@ -1269,7 +1214,7 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         // level's launches form one programmatic-dependency chain
         // a level without warp-tier merges needs no k_level_modes: its mode word is
         // the lane bit (the lane kernels exit on an empty level by its root count)
-        launch_pdl(k_level_zero, cdiv(max(L.M, mtiles + ntiles + 2), 256), 256, 0, s, L.mTol, L.M, w.scanState,
+        launch_pdl(k_level_zero, cdiv(max(L.M, mtiles + ntiles + 2), 256), 256, 0, s, L, w.scanState,
                    mtiles + ntiles + 2, w.levelModes, warp_tier ? 0 : 1);
         unsigned long long* st1 = w.scanState;
         unsigned long long* st2 = w.scanState + mtiles;
@@ -1353,10 +1298,16 @@ void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n,
 }
 
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
-                   const unsigned long long* sbits, double* lam, int* launches, Prof* prof) {
-    launch_pdl(k_rescale, cdiv(n, 256), 256, 0, s, n, bstart, nblk, sbits, lam);
+                   const unsigned long long* sbits, double* lam, const double* alt, const LevelDev& E,
+                   int* launches, Prof* prof) {
+    launch_pdl(k_rescale, cdiv(n, 256), 256, 0, s, n, bstart, nblk, sbits, lam, alt, E);
     *launches += 1;
     PMARK(BRGPU_K_FINISH);
+}
+
+void launch_state_home(cudaStream_t s, const Work& w, const LevelDev& E, int n, int sms, int* launches) {
+    launch_pdl(k_state_home, sms * 4, 256, 0, s, w, E, n);
+    *launches += 1;
 }
 
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
