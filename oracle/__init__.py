@@ -201,6 +201,19 @@ def leaf(d, e, ref_arith=False):
     return lam, blo, bhi
 
 
+def leaf_full(d, e, ref_arith=False):
+    """(lam, Q) of a leaf by the leaf QL/QR sweeps, every row tracked (Q[i, k] =
+    row i of eigenvector k) -- test infrastructure for the Theorem 1 check."""
+    d = _f64(d)
+    e = _f64(e) if len(d) > 1 else np.zeros(1)
+    m = len(d)
+    lam, Q = np.empty(m), np.empty((m, m))
+    rc = bro().bro_leaf_full(m, _p(d), _p(e), _p(lam), _p(Q), int(ref_arith))
+    if rc:
+        raise OracleError(rc)
+    return lam, Q
+
+
 def solve_root(d, z, rho, j, patched=True, ref_arith=False):
     d, z = _f64(d), _f64(z)
     org, tau, ne = C.c_int(0), C.c_double(0.0), C.c_int(0)

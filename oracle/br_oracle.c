@@ -844,6 +844,26 @@ int bro_leaf(int m, const double* d, const double* e, double* lam, double* blo, 
     return BRO_OK;
 }
 
+/* Full eigenvector matrix of a leaf (Q[i*m + k] = row i of eigenvector k) by the
+ * same QL/QR sweeps, tracking one row per run: the conventional full-eigenvector
+ * D&C restatement of the Theorem 1 check (tests/test_theorem1_gpu.py) starts
+ * from exactly the leaf vectors whose boundary rows the BR path carries. */
+int bro_leaf_full(int m, const double* d, const double* e, double* lam, double* Q, int ref) {
+    double ee[64], x[64], l2[64];
+    if (m <= 0 || m > 64) return BRO_INVALID_ARGUMENT;
+    for (int i = 0; i < m; ++i) {
+        memcpy(l2, d, sizeof(double) * (size_t)m);
+        if (m > 1) memcpy(ee, e, sizeof(double) * (size_t)(m - 1));
+        for (int k = 0; k < m; ++k) x[k] = k == i ? 1.0 : 0.0;
+        int st = steqr(m, l2, ee, x, NULL, ref);
+        if (st) return st;
+        stable_sort_rows(m, l2, x, NULL);
+        memcpy(Q + (size_t)i * (size_t)m, x, sizeof(double) * (size_t)m);
+        if (i == 0) memcpy(lam, l2, sizeof(double) * (size_t)m);
+    }
+    return BRO_OK;
+}
+
 static int cmp_double(const void* a, const void* b) {
     double x = *(const double*)a, y = *(const double*)b;
     return (x < y) ? -1 : (y < x) ? 1 : 0;

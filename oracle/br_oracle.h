@@ -102,6 +102,7 @@ int bro_eigvals_rows(int64_t n, const double* d, const double* e, double* w, int
 int bro_qrql_values(int64_t n, const double* d, const double* e, double* w, int ref_arith);
 
 /* Leaf solve: eigenvalues ascending plus first/last eigenvector rows. */
+int bro_leaf_full(int m, const double* d, const double* e, double* lam, double* Q, int ref);
 int bro_leaf(int m, const double* d, const double* e, double* lam, double* blo,
              double* bhi, int ref_arith);
 

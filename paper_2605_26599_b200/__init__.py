@@ -413,6 +413,31 @@ class Solver:
         self._lib.brgpu_get_trace(self._h, buf, n.value, C.byref(n))
         return [(t.level, t.is_root, t.offset, t.size, t.nn, t.k) for t in buf[: n.value]]
 
+    def set_secular_trace(self, on: bool) -> None:
+        """Record every merge's secular problem (rho, D_active, z_active) on the
+        next solves (grid tier, bit-identical results) -- the Theorem 1 check."""
+        rc = self._lib.brgpu_set_secular_trace(self._h, int(on))
+        if rc:
+            self._fail(rc)
+
+    def secular_trace(self) -> list[tuple]:
+        """Per merge of the last solve, in trace() order: (level, is_root, offset,
+        size, K, rho, D_active, z_active)."""
+        recs = self.trace()
+        n = C.c_int64()
+        rc = self._lib.brgpu_get_secular_trace(self._h, None, 0, C.byref(n))
+        if rc:
+            self._fail(rc)
+        buf = np.empty(max(n.value, 1))
+        self._lib.brgpu_get_secular_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_double)), n.value, C.byref(n))
+        M = len(recs)
+        rho, at, out = buf[:M], M, []
+        for m, (lev, root, off, size, nn, k) in enumerate(recs):
+            dz = buf[at:at + 2 * k].reshape(-1, 2)
+            at += 2 * k
+            out.append((lev, root, off, size, k, float(rho[m]), dz[:, 0].copy(), dz[:, 1].copy()))
+        return out
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.brgpu_destroy(self._h)

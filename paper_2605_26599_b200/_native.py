@@ -53,7 +53,7 @@ EXPORTS = [
     "brgpu_get_ledger", "brgpu_eigvals", "brgpu_eigvals_device", "brgpu_eigvals_batched",
     "brgpu_eigvals_batched_device", "brgpu_get_stats", "brgpu_set_trace", "brgpu_get_trace",
     "brgpu_get_timing", "brgpu_profile_kernels", "brgpu_profile_kernels_batched",
-    "brgpu_kernel_class_name", "brgpu_selftest_rcp",
+    "brgpu_kernel_class_name", "brgpu_selftest_rcp", "brgpu_set_secular_trace", "brgpu_get_secular_trace",
     "brgpu_nccl_unique_id", "brgpu_create_distributed", "brgpu_plan_owned", "brgpu_version",
     "brgpu_phase_cycles", "brgpu_eigvals_dense_device", "brgpu_eigvals_rows",
 ]
@@ -97,6 +97,8 @@ def lib() -> C.CDLL:
     L.brgpu_get_stats.argtypes = [hp, C.POINTER(Stats)]
     L.brgpu_set_trace.argtypes = [hp, C.c_int]
     L.brgpu_get_trace.argtypes = [hp, C.POINTER(Trace), C.c_int64, C.POINTER(C.c_int64)]
+    L.brgpu_set_secular_trace.argtypes = [hp, C.c_int]
+    L.brgpu_get_secular_trace.argtypes = [hp, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
     L.brgpu_version.restype = C.c_char_p
     L.brgpu_get_timing.argtypes = [hp, C.POINTER(Timing)]
     L.brgpu_profile_kernels.argtypes = [hp, C.c_int64, _dp, _dp, C.POINTER(C.c_double),

@@ -48,6 +48,8 @@ void launch_level_sparse(cudaStream_t s, const Work& w, const LevelDev& L, int n
                          int* blockCnt, int* traceOut, int* launches, Prof* prof);
 void launch_state_home(cudaStream_t s, const Work& w, const LevelDev& E, int n, int sms, int* launches);
 void init_sparse_attributes();
+void launch_dump_active(cudaStream_t s, const Work& w, const LevelDev& L, int n, double* out, double* rho,
+                        int* launches);
 int sparse_cap();
 int sparse_groups_max(int n, int M, int span);
 int sparse_min_merge();
@@ -192,6 +194,9 @@ struct Handle {
     int use_graph = 1;
     int subtree = 1;
     int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
+    int strace = 0;  // secular-problem trace (brgpu_set_secular_trace): grid tier, dump per level
+    double* strBuf = nullptr;  // per level 2n doubles (d, z) + rho per merge
+    int64_t strCap = 0;
     int exact = 0;
     int trace = 0;
     double tol_scale = 1.0;
@@ -838,6 +843,12 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
         set_split(h, sc, prm);
         for (int part = 0; part < 4; ++part) {
             launch_level_part(s, h->w, L, n, prm, part, launches, prof);
+            if (part == 0 && h->strace && h->strBuf) {  // active problem before the refreshed weights
+                const size_t li2 = (phase1 ? 0 : p->levels.size()) + li;
+                launch_dump_active(s, h->w, L, n, h->strBuf + 2 * (size_t)n * li2,
+                                   h->strBuf + 2 * (size_t)n * (p->levels.size() + p->levels2.size()) + lh.m0,
+                                   launches);
+            }
             if (const int k = level_exchange_arrays(prm, part))
                 if (const int e = exchange_allgather(h, *sc, k)) h->xerr = h->xerr ? h->xerr : e;
         }
@@ -1099,6 +1110,11 @@ int ensure_buf_sizes(Handle* h, Plan* p) {
     if (int r = ensure_buf(h, h->mTol, h->mTolCap, std::max(p->maxM, 1))) return r;
     if (h->trace)
         if (int r = ensure_buf(h, h->traceBuf, h->traceCap, 2 * (int64_t)std::max<size_t>(p->mOff.size(), 1))) return r;
+    if (h->strace)
+        if (int r = ensure_buf(h, h->strBuf, h->strCap,
+                               2 * (int64_t)p->n * (int64_t)std::max<size_t>(p->levels.size() + p->levels2.size(), 1) +
+                                   (int64_t)std::max<size_t>(p->mOff.size(), 1)))
+            return r;
     return BRGPU_OK;
 }
 
@@ -1132,8 +1148,8 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs ||
         p->sigma != sig) {
         if (h->plan) free_plan(h->plan.get());
-        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0, h->nranks, h->rank, h->sms,
-                            !sig && h->sparse != 0);
+        h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0 && !h->strace, h->nranks,
+                            h->rank, h->sms, !sig && h->sparse != 0 && !h->strace);
         p = h->plan.get();
         if (sig) {  // every merge propagates the requested rows: no root-only mode
             p->sigma = true;
@@ -1408,6 +1424,7 @@ int brgpu_destroy(brgpu_handle* hh) {
         if (u->sbits) cudaFree(u->sbits);
         if (u->mTol) cudaFree(u->mTol);
         if (u->traceBuf) cudaFree(u->traceBuf);
+        if (u->strBuf) cudaFree(u->strBuf);
     }
     h->subs.clear();
     if (h->comm && nccl_api().ok) nccl_api().CommDestroy(h->comm);
@@ -1417,6 +1434,7 @@ int brgpu_destroy(brgpu_handle* hh) {
     if (h->sbits) cudaFree(h->sbits);
     if (h->mTol) cudaFree(h->mTol);
     if (h->traceBuf) cudaFree(h->traceBuf);
+    if (h->strBuf) cudaFree(h->strBuf);
     if (h->pinned) cudaFreeHost(h->pinned);
     if (h->hsmall) cudaFreeHost(h->hsmall);
     if (h->hcnt) cudaFreeHost(h->hcnt);
@@ -1508,7 +1526,7 @@ int brgpu_get_ledger(const brgpu_handle* hh, brgpu_ledger* out) {
     out->peak_ints = std::max(h->peak_ints, ints);
     out->limit_doubles = 16 * h->limit_n;
     out->limit_ints = 7 * h->limit_n;
-    out->rows_doubles = h->sigDblCap;
+    out->rows_doubles = h->sigDblCap + h->strCap;  // requested rows + the secular-trace diagnostic buffer
     out->rows_ints = h->sigIntCap;
     return BRGPU_OK;
 }
@@ -1875,6 +1893,48 @@ int brgpu_plan_owned(int64_t n, int32_t leaf_cutoff, int32_t nranks, const int32
 int brgpu_set_trace(brgpu_handle* hh, int enable) {
     if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
     hh->h.trace = enable != 0;
+    return BRGPU_OK;
+}
+
+int brgpu_set_secular_trace(brgpu_handle* hh, int enable) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    Handle* h = &hh->h;
+    if (enable && (h->nranks > 1 || h->virt > 1))
+        return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "secular trace: single-device handles only");
+    set_plan_opt(h, h->strace, enable != 0);
+    if (enable) h->trace = 1;  // the per-merge K's locate each merge's entries
+    return BRGPU_OK;
+}
+
+int brgpu_get_secular_trace(const brgpu_handle* hh, double* out, int64_t cap, int64_t* len) {
+    if (!hh) return BRGPU_ERR_INVALID_ARGUMENT;
+    const Handle* h = &hh->h;
+    const Plan* p = h->plan.get();
+    if (!h->strace || !p || !h->strBuf) return BRGPU_ERR_INVALID_ARGUMENT;
+    const int64_t n = p->n;
+    const size_t nlev = p->levels.size() + p->levels2.size();
+    const int64_t M = (int64_t)p->mOff.size();
+    std::vector<double> buf((size_t)(2 * n * (int64_t)nlev + M));
+    if (!buf.empty() && cudaMemcpy(buf.data(), h->strBuf, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return BRGPU_ERR_CUDA;
+    // rho per merge, then each merge's (d, z) pairs in trace order
+    std::vector<double> res(buf.begin() + 2 * n * (int64_t)nlev, buf.end());
+    size_t li2 = 0;
+    for (const auto* lv : {&p->levels, &p->levels2})
+        for (const LevelHost& lh : *lv) {
+            int64_t g = 0;  // level-global active index (merges in offset order)
+            for (int q = 0; q < lh.M; ++q) {
+                const int64_t K = h->traceRecs.size() > (size_t)(lh.m0 + q) ? h->traceRecs[(size_t)(lh.m0 + q)].k : 0;
+                for (int64_t j = 0; j < K; ++j) {
+                    res.push_back(buf[(size_t)(2 * n * (int64_t)li2 + 2 * (g + j))]);
+                    res.push_back(buf[(size_t)(2 * n * (int64_t)li2 + 2 * (g + j) + 1)]);
+                }
+                g += K;
+            }
+            ++li2;
+        }
+    if (len) *len = (int64_t)res.size();
+    if (out) std::copy(res.begin(), res.begin() + std::min<int64_t>(cap, (int64_t)res.size()), out);
     return BRGPU_OK;
 }
 

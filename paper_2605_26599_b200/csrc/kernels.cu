@@ -1005,6 +1005,27 @@ __global__ void k_deflated_out(Work w0, LevelDev L, int n) {
     }
 }
 
+// Secular-problem trace (brgpu_set_secular_trace): the level's active problem
+// (dA, zA before the refreshed weights replace zA) and rho per merge.
+__global__ void k_dump_active(Work w0, LevelDev L, int n, double* __restrict__ out, double* __restrict__ rho) {
+    pdl_entry();
+    Work w;
+    if (!dense_entry(w0, L, w)) return;
+    const int T = w.survPre[w.nnPre[n]];
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < T; g += gridDim.x * blockDim.x) {
+        out[2 * g] = w.dA[g];
+        out[2 * g + 1] = w.zA[g];
+    }
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < L.M; m += gridDim.x * blockDim.x)
+        rho[m] = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+}
+
+void launch_dump_active(cudaStream_t s, const Work& w, const LevelDev& L, int n, double* out, double* rho,
+                        int* launches) {
+    launch_pdl(k_dump_active, 64, 256, 0, s, w, L, n, out, rho);
+    *launches += 1;
+}
+
 // per-merge (nn, K) for the trace
 __global__ void k_level_trace(Work w0, LevelDev L, int* __restrict__ out) {
     pdl_entry();

@@ -83,3 +83,18 @@ def test_br_merges_equal_full_dc(fam, n):
         for g in groups(poles, 1e-7 * tn):
             # z carries the accumulated rounding of the boundary rows below this merge
             assert abs(np.sum(z[g] ** 2) - np.sum(zf[g] ** 2)) <= 1e-11, (off, size, g[:3])
+
+
+@pytest.mark.parametrize("fam,n", [("uniform", 256), ("toeplitz", 256), ("clustered", 128), ("sym-uniform", 4096)])
+def test_full_dc_restatement_matches_checker(fam, n):
+    """oracle/full_dc.py (the conventional D&C of the GPU Theorem 1 check,
+    tests/test_theorem1_gpu.py): same deflation decisions at every merge as the
+    checker, eigenvalues within a few ulps of ||T||."""
+    from oracle.full_dc import full_dc_trace
+    d, e = G.generate(fam, n)
+    lam, recs = full_dc_trace(d, e)
+    r = O.eigvals(d, e, trace=True, threads=1)
+    tr = sorted(r.trace, key=lambda t: (t[0], t[2]))
+    assert [t[5] for t in tr] == [x[3] for x in recs]
+    tn = float(np.max(np.abs(d) + np.r_[np.abs(e), 0] + np.r_[0, np.abs(e)]))
+    assert np.max(np.abs(lam - r.w)) <= 64 * 2.0 ** -52 * tn
