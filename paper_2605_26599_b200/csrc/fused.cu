@@ -66,7 +66,7 @@ struct FuseSmem {
     double neg[kFuseMaxMerges];  // -1 when e_m < 0
     unsigned long long tolb[kFuseMaxMerges];
     int scan[kFuseThreads / 32];
-    int next;
+    int next, nextLast;
     int cnt;
     unsigned long long evals, terms;
 };
@@ -111,6 +111,7 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
     }
     if (tid == 0) {
         S.next = 0;
+        S.nextLast = 0;
         S.evals = 0;
         S.terms = 0;
         S.cnt = cnt;
@@ -275,14 +276,27 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
         double2* snap = reinterpret_cast<double2*>(S.Z) + tid;
         RootSM st;
         int g = -1, ks = 0;
-        bool exhausted = false;
+        bool exhausted = false, lastDone = false;
         unsigned long long evals = 0, terms = 0;
         for (;;) {
+            // queue order: every merge's last root first (the one-pole model of the
+            // root above the largest pole averages ~2.5x the evaluations of an
+            // interior root: started last it would set the phase's tail), then the
+            // interior roots in order -- the order never changes a result
             while (g < 0 && !exhausted) {
-                const int q = atomicAdd(&S.next, 1);
-                if (q >= T) { exhausted = true; break; }
-                g = q;
-                const int t = upper_index(S.kS, cnt, g);
+                int t;
+                if (!lastDone) {
+                    t = atomicAdd(&S.nextLast, 1);
+                    if (t >= cnt) { lastDone = true; continue; }
+                    if (S.kS[t + 1] == S.kS[t]) continue;
+                    g = S.kS[t + 1] - 1;
+                } else {
+                    const int q = atomicAdd(&S.next, 1);
+                    if (q >= T) { exhausted = true; break; }
+                    t = upper_index(S.kS, cnt, q);
+                    if (q == S.kS[t + 1] - 1) continue;  // a last root: already taken
+                    g = q;
+                }
                 ks = S.kS[t];
                 const int K = S.kS[t + 1] - ks;
                 rs_begin(st, K, g - ks, S.rho[t], PolesPairs{pairs + ks}, zA[ks], Z2Pairs{pairs + ks});

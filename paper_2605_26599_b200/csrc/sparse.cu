@@ -427,7 +427,7 @@ struct SpSmem {
     double rho[MM];
     double tol[MM];
     int scan[NT / 32];
-    int next, nextW;
+    int next, nextW, nextLast;
 };
 
 // one root, one warp: split arithmetic (lane-strided terms + xor butterfly),
@@ -524,6 +524,7 @@ __device__ __forceinline__ void sp_group(const Work& w, const LevelDev& L, const
     if (tid == 0) {
         S.next = 0;
         S.nextW = 0;
+        S.nextLast = 0;
     }
     __syncthreads();
     const int E = S.mo[cnt];
@@ -650,12 +651,21 @@ __device__ __forceinline__ void sp_group(const Work& w, const LevelDev& L, const
         double2* snap = reinterpret_cast<double2*>(S.Z) + tid;
         RootSM st;
         int g = -1, ks = 0;
-        bool exhausted = false;
+        bool exhausted = false, lastDone = false;
         for (;;) {
-            while (g < 0 && !exhausted) {
-                const int q = atomicAdd(&S.next, 1);
-                if (q >= T) { exhausted = true; break; }
-                const int t = upper_index(S.kS, cnt, q);
+            while (g < 0 && !exhausted) {  // last roots first (fused.cu), then interior roots
+                int t, q;
+                if (!lastDone) {
+                    t = atomicAdd(&S.nextLast, 1);
+                    if (t >= cnt) { lastDone = true; continue; }
+                    if (S.kS[t + 1] == S.kS[t]) continue;
+                    q = S.kS[t + 1] - 1;
+                } else {
+                    q = atomicAdd(&S.next, 1);
+                    if (q >= T) { exhausted = true; break; }
+                    t = upper_index(S.kS, cnt, q);
+                    if (q == S.kS[t + 1] - 1) continue;
+                }
                 ks = S.kS[t];
                 const int K = S.kS[t + 1] - ks;
                 if (split_mode(S.ms[t], K)) continue;

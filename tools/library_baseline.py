@@ -10,7 +10,7 @@ PAPER.md:2031-2055) next to this repo's BR solver, on the same inputs.
 
 Families: the paper's four (uniform, normal, Toeplitz (2, 0.25), clustered;
 PAPER.md:1916) plus BASELINE's random sym-uniform, at N = 4096, 16384 and the
-paper's N = 49,152 (GPU library only where the dense matrix fits; dsterf only to
+largest N whose dense n x n fits the 32-bit cuSOLVER dense API (32768; the paper used 49,152); dsterf only to
 16384).  Writes one JSON document (stdout and --out).
 
     python tools/library_baseline.py --out profiles/r02/library_baseline.json
@@ -71,7 +71,7 @@ def br_values(solver, d, e, reps: int = 5) -> tuple[float, np.ndarray]:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="")
-    ap.add_argument("--sizes", default="4096,16384,49152")
+    ap.add_argument("--sizes", default="4096,16384,32768")
     a = ap.parse_args()
     import scipy.linalg as sl
     import torch
@@ -106,7 +106,8 @@ def main() -> None:
                     wl = sl.eigvalsh_tridiagonal(d, e, lapack_driver="sterf")
                     row["lapack_dsterf_s"] = time.perf_counter() - t0
                     row["max_abs_diff_vs_dsterf"] = float(np.max(np.abs(wb - wl)))
-                row["br_workspace_bytes"] = 8 * 15 * n
+                led = s.ledger()
+                row["br_workspace_bytes"] = 8 * led.peak_doubles + 4 * led.peak_ints
                 res["rows"].append(row)
                 print(json.dumps(row), flush=True)
     txt = json.dumps(res, indent=1)
