@@ -533,6 +533,26 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
             prevf = ev.f;
         }
         double tau_next = NAN;
+#ifndef BRO_NO_LAST_GUESS
+        /* GPU arithmetic, the last root's start (dlaed4's case i = n): its first
+         * iterate is the bracket midpoint, often far from the root; the first
+         * step solves the model of the two largest poles plus a constant fitted
+         * at that point, c + rho z_{k-2}^2/(delta - t) + rho z_{k-1}^2/(-t) = 0
+         * (delta = d_{k-2} - d_{k-1}), instead of the one-pole model. */
+        if (!ref && last && iter == 0 && k >= 2) {
+            const double delta = d[k - 2] - d[k - 1];
+            const double a = rho * (z[k - 2] * z[k - 2]), b = rho * (z[k - 1] * z[k - 1]);
+            const double ta = a / (delta - tau), tb = b / (-tau);
+            const double c = ev.f - ta - tb;
+            const double fprest = ev.fp - ta / (delta - tau) - tb / (-tau);
+            if (fabs(fprest) * tau <= fabs(c)) {  /* the rest is flat over [0, tau] */
+                gmode = 1;
+                gA = c;
+                gB = -(c * delta + a + b);
+                gC = b * delta;
+            }
+        }
+#endif
         if (nslow >= 2 && geo_ok(lo, hi)) {
             tau_next = geo_mid(lo, hi);
         } else

@@ -24,6 +24,14 @@
 
 namespace brgpu {
 
+// CTAs per SM of the 512-element shape: 3 (85 registers) beats 4 (64 registers,
+// spilling the root state machine): random 2^20 4.66 -> 4.59 ms, n = 4096 0.86 -> 0.75 ms
+#ifndef BRGPU_FUSE_RUN_MINB
+#define BRGPU_FUSE_RUN_MINB 3
+#endif
+#ifndef BRGPU_FUSE_ONE_MINB
+#define BRGPU_FUSE_ONE_MINB 3
+#endif
 constexpr int kFuseMaxMerges = 128;   // merges per group
 #ifndef BRGPU_SMALL_THREADS
 #define BRGPU_SMALL_THREADS 256
@@ -66,7 +74,8 @@ struct FuseSmem {
     double neg[kFuseMaxMerges];  // -1 when e_m < 0
     unsigned long long tolb[kFuseMaxMerges];
     int scan[kFuseThreads / 32];
-    int next, nextLast;
+    int ne[kFuseMaxMerges + 1];  // merges with K > 0 before t (root queue order)
+    int next;
     int cnt;
     unsigned long long evals, terms;
 };
@@ -111,7 +120,6 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
     }
     if (tid == 0) {
         S.next = 0;
-        S.nextLast = 0;
         S.evals = 0;
         S.terms = 0;
         S.cnt = cnt;
@@ -268,6 +276,23 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
     }
     if (tid <= cnt) S.kS[tid] = S.survPre[S.nnPre[tid < cnt ? S.mo[tid] : E]];
     __syncthreads();
+    // Root queue order: every merge's last root first (the one-pole model of the
+    // root above the largest pole averages ~2.5x the evaluations of an interior
+    // root: started last it would set the secular phase's tail), then the
+    // interior roots in order.  The order never changes a result.  ne[t] = merges
+    // with K > 0 before t; the order lives in nnPos (dead after the compaction).
+    if (tid <= cnt) {
+        int c = 0;
+        for (int u = 0; u < tid; ++u) c += S.kS[u + 1] > S.kS[u];
+        S.ne[tid] = c;
+    }
+    __syncthreads();
+    int* qorder = S.nnPos;
+    for (int g = tid; g < T; g += kFuseThreads) {
+        const int t = upper_index(S.kS, cnt, g);
+        qorder[g == S.kS[t + 1] - 1 ? S.ne[t] : S.ne[cnt] + g - S.ne[t]] = g;
+    }
+    __syncthreads();
 
     PHASE_MARK(0);
     // ---- secular roots: per-lane RootSM, CTA queue --------------------------
@@ -276,27 +301,14 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
         double2* snap = reinterpret_cast<double2*>(S.Z) + tid;
         RootSM st;
         int g = -1, ks = 0;
-        bool exhausted = false, lastDone = false;
+        bool exhausted = false;
         unsigned long long evals = 0, terms = 0;
         for (;;) {
-            // queue order: every merge's last root first (the one-pole model of the
-            // root above the largest pole averages ~2.5x the evaluations of an
-            // interior root: started last it would set the phase's tail), then the
-            // interior roots in order -- the order never changes a result
             while (g < 0 && !exhausted) {
-                int t;
-                if (!lastDone) {
-                    t = atomicAdd(&S.nextLast, 1);
-                    if (t >= cnt) { lastDone = true; continue; }
-                    if (S.kS[t + 1] == S.kS[t]) continue;
-                    g = S.kS[t + 1] - 1;
-                } else {
-                    const int q = atomicAdd(&S.next, 1);
-                    if (q >= T) { exhausted = true; break; }
-                    t = upper_index(S.kS, cnt, q);
-                    if (q == S.kS[t + 1] - 1) continue;  // a last root: already taken
-                    g = q;
-                }
+                const int q = atomicAdd(&S.next, 1);
+                if (q >= T) { exhausted = true; break; }
+                g = qorder[q];
+                const int t = upper_index(S.kS, cnt, g);
                 ks = S.kS[t];
                 const int K = S.kS[t + 1] - ks;
                 rs_begin(st, K, g - ks, S.rho[t], PolesPairs{pairs + ks}, zA[ks], Z2Pairs{pairs + ks});
@@ -464,7 +476,7 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
 }
 
 template <int kFuseMax, int kFuseThreads>
-__global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
+__global__ void __launch_bounds__(kFuseThreads, kFuseMax <= 512 ? BRGPU_FUSE_ONE_MINB : 2048 / kFuseMax)
 k_level_fused(Work w0, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
               SolveParams prm, int* __restrict__ traceOut) {
     pdl_entry();
@@ -484,7 +496,7 @@ k_level_fused(Work w0, LevelDev L, const int* __restrict__ gFirst, const int* __
 // barrier instead of a grid-wide kernel boundary (the data stays in L1/L2),
 // and different CTAs' root-queue tails overlap across levels.
 template <int kFuseMax, int kFuseThreads>
-__global__ void __launch_bounds__(kFuseThreads, 2048 / kFuseMax)
+__global__ void __launch_bounds__(kFuseThreads, BRGPU_FUSE_RUN_MINB)
 k_levels_fused(Work w0, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
     pdl_entry();
     const int slot = slot_from_prev(run.L[0]);
