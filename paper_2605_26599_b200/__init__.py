@@ -225,7 +225,9 @@ class Solver:
         self._opt(_native.OPT_SUBTREE, int(o.subtree))
         self._opt(_native.OPT_EXACT_PASSES, int(o.exact_passes))
         self._opt(_native.OPT_ROOT_SPLIT, int(o.root_split))
-        self._opt(_native.OPT_SPARSE, int(o.sparse))
+        if o.sparse or getattr(self, "_sparse_on", False):  # opt-in tier: set once enabled
+            self._opt(_native.OPT_SPARSE, int(o.sparse))
+            self._sparse_on = bool(o.sparse)
         if self.nranks == 1:
             self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o

@@ -97,8 +97,9 @@ def lib() -> C.CDLL:
     L.brgpu_get_stats.argtypes = [hp, C.POINTER(Stats)]
     L.brgpu_set_trace.argtypes = [hp, C.c_int]
     L.brgpu_get_trace.argtypes = [hp, C.POINTER(Trace), C.c_int64, C.POINTER(C.c_int64)]
-    L.brgpu_set_secular_trace.argtypes = [hp, C.c_int]
-    L.brgpu_get_secular_trace.argtypes = [hp, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
+    if hasattr(L, "brgpu_set_secular_trace"):  # (older A/B builds lack the trace entry points)
+        L.brgpu_set_secular_trace.argtypes = [hp, C.c_int]
+        L.brgpu_get_secular_trace.argtypes = [hp, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_int64)]
     L.brgpu_version.restype = C.c_char_p
     L.brgpu_get_timing.argtypes = [hp, C.POINTER(Timing)]
     L.brgpu_profile_kernels.argtypes = [hp, C.c_int64, _dp, _dp, C.POINTER(C.c_double),

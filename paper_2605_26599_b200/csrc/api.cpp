@@ -46,7 +46,6 @@ void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n,
                         int* launches, Prof* prof);
 void launch_level_sparse(cudaStream_t s, const Work& w, const LevelDev& L, int n, const SolveParams& prm,
                          int* blockCnt, int* traceOut, int* launches, Prof* prof);
-void launch_state_home(cudaStream_t s, const Work& w, const LevelDev& E, int n, int sms, int* launches);
 void init_sparse_attributes();
 void launch_dump_active(cudaStream_t s, const Work& w, const LevelDev& L, int n, double* out, double* rho,
                         int* launches);
@@ -55,8 +54,7 @@ int sparse_groups_max(int n, int M, int span);
 int sparse_min_merge();
 int sparse_flag_grid(int n, int sms);
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
-                   const unsigned long long* sbits, double* lam, const double* alt, const LevelDev& E,
-                   int* launches, Prof* prof);
+                   const unsigned long long* sbits, double* lam, int* launches, Prof* prof);
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,
                        int nruns, int* launches, Prof* prof);
 void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
@@ -722,10 +720,8 @@ LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh, const LevelHost* pre
     L.M = lh.M;
     L.allSplit = lh.minSize > kSplitMinSizeHost ? 1 : 0;
     L.maxSize = lh.maxSize;
-    // plans without sparse levels keep the state in slot 0: no control words
-    L.ctl = p->anySp ? p->d_ctl + lh.ctl : nullptr;
-    L.pctl = p->anySp && prev ? p->d_ctl + prev->ctl : nullptr;
-    L.pcap = (prev && prev->sp) ? prev->spCap : 0;
+    (void)prev;
+    L.ctl = lh.sp ? p->d_ctl + lh.ctl : nullptr;
     L.spCap = lh.sp ? lh.spCap : 0;
     L.spStatic = lh.spStatic;
     L.spSpan = lh.spSpan;
@@ -740,19 +736,6 @@ LevelDev level_dev(Handle* h, Plan* p, const LevelHost& lh, const LevelHost* pre
         L.spTileSplit = p->d_spTiles + (p->n / 1024 + 2);
     }
     return L;
-}
-
-// Words describing the state slot after the last level of `levels` (the
-// previous-level fields only), for k_rescale / k_state_home.
-LevelDev end_words(Plan* p, const std::vector<LevelHost>& levels) {
-    LevelDev E{};
-    if (!levels.empty()) {
-        const LevelHost& lh = p->dbgStop > 0 && &levels == &p->levels && (size_t)p->dbgStop <= levels.size()
-                                  ? levels[(size_t)p->dbgStop - 1] : levels.back();
-        E.pctl = p->anySp ? p->d_ctl + lh.ctl : nullptr;
-        E.pcap = lh.sp ? lh.spCap : 0;
-    }
-    return E;
 }
 
 SolveParams solve_params(Handle* h, int n) {
@@ -871,8 +854,6 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     if (h->sig)
         launch_sigma_leaves(s, h->sig->dev, p->maxLeaf, h->sig->dTask, p->d_tOff, p->d_tSize, h->w, launches);
     run_levels(h, p, p->levels, launches, prof);
-    // a phase exchange moves (lam, blo, bhi): bring the state home to slot 0
-    if (p->nranks > 1) launch_state_home(s, h->w, end_words(p, p->levels), n, h->sms, launches);
 }
 
 // Stage B: shared top merges (roots split across ranks when enabled),
@@ -891,8 +872,7 @@ void finish_stage_b(Handle* h, Plan* p, int* launches, Prof* prof) {
     cudaStream_t s = h->stream;
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
-    const LevelDev E = end_words(p, p->levels2.empty() ? p->levels : p->levels2);
-    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, h->w.D, E, launches, prof);
+    launch_finish(s, n, p->d_bstart, nblk, h->sbits, h->w.lam, launches, prof);
     if (h->sig)
         launch_sigma_final(s, h->sig->dev, h->w.lam, p->d_bstart, nblk, h->sig->dBlk, h->sig->maxBlock,
                            h->sig->out, n, launches);

@@ -20,7 +20,6 @@
 #include "launch.cuh"
 #include "numerics.cuh"
 #include "grid_common.cuh"
-#include "level_state.cuh"
 
 namespace brgpu {
 
@@ -477,12 +476,9 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
 
 template <int kFuseMax, int kFuseThreads>
 __global__ void __launch_bounds__(kFuseThreads, kFuseMax <= 512 ? BRGPU_FUSE_ONE_MINB : 2048 / kFuseMax)
-k_level_fused(Work w0, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
+k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
               SolveParams prm, int* __restrict__ traceOut) {
     pdl_entry();
-    const int slot = slot_from_prev(L);  // first (only) kernel of the level: publish the state slot
-    if (blockIdx.x == 0 && threadIdx.x == 0 && L.ctl) L.ctl[0] = slot;
-    const Work w = with_slot(w0, slot);
     extern __shared__ __align__(16) unsigned char fuse_raw[];
     using Smem = FuseSmem<kFuseMax, kFuseThreads>;
     Smem& S = *reinterpret_cast<Smem*>(fuse_raw);
@@ -497,13 +493,8 @@ k_level_fused(Work w0, LevelDev L, const int* __restrict__ gFirst, const int* __
 // and different CTAs' root-queue tails overlap across levels.
 template <int kFuseMax, int kFuseThreads>
 __global__ void __launch_bounds__(kFuseThreads, BRGPU_FUSE_RUN_MINB)
-k_levels_fused(Work w0, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
+k_levels_fused(Work w, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
     pdl_entry();
-    const int slot = slot_from_prev(run.L[0]);
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-        for (int l = 0; l < run.nlev; ++l)
-            if (run.L[l].ctl) run.L[l].ctl[0] = slot;
-    const Work w = with_slot(w0, slot);
     extern __shared__ __align__(16) unsigned char fuse_raw[];
     using Smem = FuseSmem<kFuseMax, kFuseThreads>;
     Smem& S = *reinterpret_cast<Smem*>(fuse_raw);

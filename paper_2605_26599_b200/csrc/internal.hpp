@@ -72,15 +72,10 @@ struct LevelDev {
     int M;
     int allSplit;              // every merge of the level is larger than kSplitMinSize (warp tier only)
     int maxSize;               // largest merge of the level
-    // Level control words (sparse.cu).  The node state of a level lives in one
-    // of two slots -- (lam, blo, bhi) or (D, R0, R1) -- because the sparse
-    // path writes its parents out of place; ctl[0] = slot at the start of this
-    // level (written by the level's first kernel from the previous level's
-    // words), ctl[1] = largest non-negligible count of a merge (k_sp_flag),
-    // ctl[2] = k_sp_flag's grid-barrier counter.  Null ctl: slot 0 throughout.
+    // Level control words of a sparse-capable level (sparse.cu): ctl[1] = largest
+    // non-negligible count of a merge (k_sp_flag), ctl[2] = k_sp_flag's
+    // grid-barrier counter, ctl[3] = the level's total non-negligible count.
     int* ctl;
-    const int* pctl;  // previous level's words (null: first level of a phase, slot 0)
-    int pcap;         // previous level's sparse cap (0: it always ran dense / fused)
     int spCap;        // this level's sparse cap C: sparse iff every merge has NN <= C (0: dense only)
     int spStatic;     // every merge has size <= C: sparse always, no dense kernels launched
     int spSpan;       // k_sp_solve group key span (host-chosen from the previous solve's profile)

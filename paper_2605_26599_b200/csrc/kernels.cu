@@ -316,10 +316,9 @@ constexpr int kPrepVec = 4;  // merge tiles per k_merge_prep CTA: the whole leve
 //    memory first);
 //  * the merge-path diagonal split at each tile's first position (warp k for
 //    tile k, 32-ary search), kept in split[tile] for k_merge_nn.
-__global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w0, LevelDev L, int n, int* __restrict__ split) {
+__global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w, LevelDev L, int n, int* __restrict__ split) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ unsigned long long s_max[kPrepVec][kMergeTile / 32];
     __shared__ int s_m[kPrepVec][kMergeTile / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -396,12 +395,11 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_prep(Work w0, LevelDev L, 
 // loaded coalesced at once, placed by searches in shared memory and written
 // back coalesced in merged order.  The tile's flag count (order-free: the same
 // elements) is published before the placement so the look-back overlaps it.
-__global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w0, LevelDev L, int n, double tol_scale,
+__global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int n, double tol_scale,
                                                          const int* __restrict__ split,
                                                          unsigned long long* state, int* ticket) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     // inputs (lam, blo, bhi), then the merged tile (D, Z, R0 alias them; R1)
     __shared__ double s_v[kMergeTile], s_b0[kMergeTile], s_b1[kMergeTile], s_R1[kMergeTile];
     double* s_D = s_v;
@@ -512,10 +510,9 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w0, LevelDev L, in
 #define BRGPU_WALK_BATCH 8
 #endif
 constexpr int kWalkBatch = BRGPU_WALK_BATCH;  // NN entries loaded per step of a long segment walk
-__global__ void k_segment_walk(Work w0, LevelDev L, int n, double tol_scale) {
+__global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int NN = w.nnPre[n];
     if (q >= NN) return;
@@ -587,11 +584,10 @@ __global__ void k_segment_walk(Work w0, LevelDev L, int n, double tol_scale) {
 
 // survivor prefix over NN indices + compacted active problem (deflate.cpp:100-105),
 // one pass; tile 0 always runs so survPre[NN] is written even when NN == 0
-__global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w0, LevelDev L, int n,
+__global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, int n,
                                                           unsigned long long* state, int* ticket) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ int s_tile, s_pref;
     const int NN = w.nnPre[n];
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
@@ -634,12 +630,8 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w0, LevelDev L, i
 __global__ void k_level_zero(LevelDev L, unsigned long long* __restrict__ st, int words, int* __restrict__ modes,
                              int modes0) {
     pdl_entry();
+    if (!dense_entry(L)) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (L.spCap == 0) {
-        if (i == 0 && L.ctl) L.ctl[0] = slot_from_prev(L);
-    } else if (level_sparse(L)) {
-        return;
-    }
     if (i < L.M) L.mTol[i] = 0ULL;
     if (i < words) st[i] = 0ULL;
     if (i == 0) *modes = modes0;
@@ -647,10 +639,9 @@ __global__ void k_level_zero(LevelDev L, unsigned long long* __restrict__ st, in
 
 // Which secular tiers a level needs (merges with K > 0): bit0 lane-per-root,
 // bit1 warp-per-root.  Kernels of an absent tier exit on their first load.
-__global__ void k_level_modes(Work w0, LevelDev L) {
+__global__ void k_level_modes(Work w, LevelDev L) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     int bits = 0;
     if (m < L.M) {
@@ -711,10 +702,9 @@ constexpr int kSecBigLevel = 1 << 21;
 // as soon as its root converges.  Evaluations are branch-free pole loops over
 // shared-memory (d, z^2) pairs (one LDS.128 per term, broadcast within a merge).
 template <int MINB>
-__global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w0, LevelDev L, int n, int patched) {
+__global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ double2 s_snap[kSecBlock];
     __shared__ int s_next;
@@ -837,10 +827,9 @@ __global__ void k_selftest_rcp(long long count, unsigned long long seed, unsigne
 // The roots' (d_origin, tau, d_j) triples stream through shared memory in
 // tiles of kWin covering the CTA's window (one tile when it fits), in root
 // order, so the product order is the checker's.
-__global__ void __launch_bounds__(kSecBlock) k_zhat(Work w0, LevelDev L, int n) {
+__global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ double s_dorg[kWin], s_tau[kWin], s_dj[kWin];
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -907,10 +896,9 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w0, LevelDev L, int n) 
 // y = zhat/Delta_j / ||zhat/Delta_j|| streamed (never stored),
 // plus placement of lambda_j in the parent's ascending order.  Poles (d, zhat,
 // r0, r1) stream through shared memory in tiles, in pole order.
-__global__ void __launch_bounds__(kSecBlock) k_rows(Work w0, LevelDev L, int n) {
+__global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ double s_d[kWin], s_zh[kWin], s_r0[kWin], s_r1[kWin];
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -993,10 +981,9 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w0, LevelDev L, int n) 
 }
 
 // deflated columns: parent position t + #{roots < D}
-__global__ void k_deflated_out(Work w0, LevelDev L, int n) {
+__global__ void k_deflated_out(Work w, LevelDev L, int n) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const int m = find_merge(L, k);
@@ -1027,10 +1014,9 @@ __global__ void k_deflated_out(Work w0, LevelDev L, int n) {
 
 // Secular-problem trace (brgpu_set_secular_trace): the level's active problem
 // (dA, zA before the refreshed weights replace zA) and rho per merge.
-__global__ void k_dump_active(Work w0, LevelDev L, int n, double* __restrict__ out, double* __restrict__ rho) {
+__global__ void k_dump_active(Work w, LevelDev L, int n, double* __restrict__ out, double* __restrict__ rho) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     const int T = w.survPre[w.nnPre[n]];
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < T; g += gridDim.x * blockDim.x) {
         out[2 * g] = w.dA[g];
@@ -1047,10 +1033,9 @@ void launch_dump_active(cudaStream_t s, const Work& w, const LevelDev& L, int n,
 }
 
 // per-merge (nn, K) for the trace
-__global__ void k_level_trace(Work w0, LevelDev L, int* __restrict__ out) {
+__global__ void k_level_trace(Work w, LevelDev L, int* __restrict__ out) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= L.M) return;
     const int off = L.mOff[m], end = off + L.mSize[m];
@@ -1063,26 +1048,13 @@ __global__ void k_level_trace(Work w0, LevelDev L, int* __restrict__ out) {
 // rescale + cross-block merge
 // ---------------------------------------------------------------------------
 __global__ void k_rescale(int n, const int* __restrict__ bstart, int nblk,
-                          const unsigned long long* __restrict__ sbits, double* __restrict__ lam,
-                          const double* __restrict__ alt, LevelDev E) {
+                          const unsigned long long* __restrict__ sbits, double* __restrict__ lam) {
     pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double* src = slot_from_prev(E) ? alt : lam;  // the last level may have left the state in slot 1
     const int b = nblk == 1 ? 0 : find_block(bstart, nblk, i);
     const double s = block_scale_of(sbits[b]);
-    lam[i] = src[i] * s;
-}
-
-// State back to slot 0 (lam, blo, bhi) before a phase exchange (multi-rank plans).
-__global__ void k_state_home(Work w, LevelDev E, int n) {
-    pdl_entry();
-    if (!slot_from_prev(E)) return;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        w.lam[i] = w.D[i];
-        w.blo[i] = w.R0[i];
-        w.bhi[i] = w.R1[i];
-    }
+    lam[i] = lam[i] * s;
 }
 
 // one pass of a bottom-up stable merge sort over runs [rs[r], rs[r+1])
@@ -1339,16 +1311,10 @@ void launch_level_trace(cudaStream_t s, const Work& w, const LevelDev& L, int n,
 }
 
 void launch_finish(cudaStream_t s, int n, const int* bstart, int nblk,
-                   const unsigned long long* sbits, double* lam, const double* alt, const LevelDev& E,
-                   int* launches, Prof* prof) {
-    launch_pdl(k_rescale, cdiv(n, 256), 256, 0, s, n, bstart, nblk, sbits, lam, alt, E);
+                   const unsigned long long* sbits, double* lam, int* launches, Prof* prof) {
+    launch_pdl(k_rescale, cdiv(n, 256), 256, 0, s, n, bstart, nblk, sbits, lam);
     *launches += 1;
     PMARK(BRGPU_K_FINISH);
-}
-
-void launch_state_home(cudaStream_t s, const Work& w, const LevelDev& E, int n, int sms, int* launches) {
-    launch_pdl(k_state_home, sms * 4, 256, 0, s, w, E, n);
-    *launches += 1;
 }
 
 void launch_merge_runs(cudaStream_t s, int n, const double* src, double* dst, const int* rs,

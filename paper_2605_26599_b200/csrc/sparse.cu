@@ -200,18 +200,14 @@ __global__ void __launch_bounds__(kFlagThreads) k_sp_flag(Work w0, LevelDev L, i
     __shared__ int s_red[kFlagThreads / 32];
     __shared__ int s_wt[kFlagRows][kFlagThreads / 32];
     __shared__ FlagTab T;
-    const int slot = slot_from_prev(L);
-    const Work w = with_slot(w0, slot);
+    const Work& w = w0;  // the children are in (lam, blo, bhi)
     const int G = (int)gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int per = nsc * kFlagChunk;  // the launcher sizes the grid: G * per >= n
     const int c0 = (int)min((long long)n, (long long)blockIdx.x * per), c1 = min(n, c0 + per);
     unsigned* bar = reinterpret_cast<unsigned*>(L.ctl + 2);
 
     // ---- phase 0: level words, per-merge accumulators, group table ---------
-    if (blockIdx.x == 0 && tid == 0) {
-        L.ctl[0] = slot;
-        L.ctl[1] = 0;
-    }
+    if (blockIdx.x == 0 && tid == 0) L.ctl[1] = 0;
     for (int m = blockIdx.x * kFlagThreads + tid; m < L.M; m += G * kFlagThreads) {
         L.mTol[m] = 0ULL;
         L.spNN[m] = 0;
@@ -908,7 +904,7 @@ struct PlaceSmem {
     double roots[kPlaceStage];
     int pre[kPlaceStage];
     unsigned char sflag[kPlaceStage];
-    int nseg, split0, split1, stRoots, stNN, sparse, slot;
+    int nseg, split0, split1, stRoots, stNN, sparse;
     // per segment
     int soff[kPlaceSegs], snl[kPlaceSegs], ssize[kPlaceSegs], scs[kPlaceSegs], snn[kPlaceSegs], sK[kPlaceSegs];
     int sh[kPlaceSegs], slen[kPlaceSegs], si0[kPlaceSegs], sla[kPlaceSegs], sqb[kPlaceSegs];
@@ -943,14 +939,14 @@ __global__ void __launch_bounds__(kPlaceThreads) k_sp_place(Work w0, LevelDev L,
     const int t = threadIdx.x;
     if (t == 0) {  // one thread reads the level and tile words (grid-wide hot lines)
         S.sparse = level_sparse(L);
-        S.slot = level_slot(L);
         S.split0 = L.spTileSplit[blockIdx.x];
         S.split1 = L.spTileSplit[blockIdx.x + 1];
     }
     __syncthreads();
     if (!S.sparse) return;
-    const int slot = S.slot;
-    const Work wi = with_slot(w0, slot), wo = with_slot(w0, slot ^ 1);
+    // children in (lam, blo, bhi); parents to (D, R0, R1), copied back by k_sp_home
+    const Work& wi = w0;
+    struct { double *lam, *blo, *bhi; } wo = {w0.D, w0.R0, w0.R1};
     const int p0 = blockIdx.x * kPlaceTile;
     const int pend = min(n, p0 + kPlaceTile);
 
@@ -1171,6 +1167,33 @@ __global__ void __launch_bounds__(kPlaceThreads) k_sp_place(Work w0, LevelDev L,
     }
 }
 
+// Parents back to (lam, blo, bhi): every level boundary keeps the state there,
+// so the dense and fused kernels never need to know which path a level took.
+__global__ void __launch_bounds__(256) k_sp_home(Work w, LevelDev L, int n) {
+    pdl_entry();
+    __shared__ int s_sp;
+    if (threadIdx.x == 0) s_sp = level_sparse(L);
+    __syncthreads();
+    if (!s_sp) return;
+    const int n2 = n >> 1;  // 16-byte vectors
+    const double2* __restrict__ D = reinterpret_cast<const double2*>(w.D);
+    const double2* __restrict__ R0 = reinterpret_cast<const double2*>(w.R0);
+    const double2* __restrict__ R1 = reinterpret_cast<const double2*>(w.R1);
+    double2* lam = reinterpret_cast<double2*>(w.lam);
+    double2* blo = reinterpret_cast<double2*>(w.blo);
+    double2* bhi = reinterpret_cast<double2*>(w.bhi);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) {
+        lam[i] = D[i];
+        blo[i] = R0[i];
+        bhi[i] = R1[i];
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        w.lam[n - 1] = w.D[n - 1];
+        w.blo[n - 1] = w.R0[n - 1];
+        w.bhi[n - 1] = w.R1[n - 1];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -1211,8 +1234,9 @@ void launch_level_sparse(cudaStream_t s, const Work& w, const LevelDev& L, int n
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SPSOLVE);
     launch_pdl(k_sp_place, (n + kPlaceTile - 1) / kPlaceTile, kPlaceThreads, sizeof(PlaceSmem), s, w, L, n,
                prm.tol_scale);
+    launch_pdl(k_sp_home, std::max(1, std::min((n / 2 + 255) / 256, prm.sms * 8)), 256, 0, s, w, L, n);
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SPPLACE);
-    *launches += 3;
+    *launches += 4;
 }
 
 static_assert(sizeof(SpSmem<kSpCap, kSpThreads>) <= 227 * 1024, "k_sp_solve shared memory");

@@ -32,10 +32,9 @@ __device__ __forceinline__ void tile_load(double2* dst, const double* __restrict
 }
 
 __global__ void __launch_bounds__(kTiledThreads, 2)
-k_secular_tiled(Work w0, LevelDev L, int n, int patched, int G) {
+k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ double2 s_tile[2][kTile2];
     __shared__ double2 s_snap[kTiledThreads];
     __shared__ int s_next;

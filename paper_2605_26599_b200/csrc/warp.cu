@@ -118,10 +118,9 @@ __device__ __forceinline__ void sec_terms2(const double2* __restrict__ tp, int& 
 // chunk's pole window through shared memory once for all its warps' roots.
 template <int NS>
 __global__ void __launch_bounds__(kSecWThreads, NS == 1 ? BRGPU_SECW_MINB : BRGPU_SECW2_MINB)
-k_secular_warp(Work w0, LevelDev L, int n, int patched) {
+k_secular_warp(Work w, LevelDev L, int n, int patched) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     extern __shared__ __align__(16) double2 s_tiles[];  // two tiles of kSecWTile pairs (dynamic)
     __shared__ int s_next;
     if (!L.allSplit && !(*w.levelModes & 2)) return;
@@ -308,10 +307,9 @@ struct WarpZhatPole {
 #ifndef BRGPU_ZHAT_MINB
 #define BRGPU_ZHAT_MINB 5  // CTAs per SM (48 registers): C3 zhat 2.97 -> 2.91 ms
 #endif
-__global__ void __launch_bounds__(kWarpThreads, BRGPU_ZHAT_MINB) k_zhat_warp(Work w0, LevelDev L, int n) {
+__global__ void __launch_bounds__(kWarpThreads, BRGPU_ZHAT_MINB) k_zhat_warp(Work w, LevelDev L, int n) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     __shared__ double s_dorg[kWarpTile], s_tau[kWarpTile], s_dj[kWarpTile];
     if (!L.allSplit && !(*w.levelModes & 2)) return;
     const int T = w.survPre[w.nnPre[n]];
@@ -478,10 +476,9 @@ struct WarpRowRoot {
 #ifndef BRGPU_ROWS_MINB
 #define BRGPU_ROWS_MINB 4  // CTAs per SM (64 registers): C3 rows 3.14 -> 3.02 ms
 #endif
-__global__ void __launch_bounds__(kWarpThreads, BRGPU_ROWS_MINB) k_rows_warp(Work w0, LevelDev L, int n) {
+__global__ void __launch_bounds__(kWarpThreads, BRGPU_ROWS_MINB) k_rows_warp(Work w, LevelDev L, int n) {
     pdl_entry();
-    Work w;
-    if (!dense_entry(w0, L, w)) return;
+    if (!dense_entry(L)) return;
     // two buffers of (d, zhat, r0, r1) tiles: the next tile streams in by
     // cp.async while the current one is consumed
     __shared__ __align__(16) double s_rt[2][4][kRowsTile];

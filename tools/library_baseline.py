@@ -10,7 +10,7 @@ PAPER.md:2031-2055) next to this repo's BR solver, on the same inputs.
 
 Families: the paper's four (uniform, normal, Toeplitz (2, 0.25), clustered;
 PAPER.md:1916) plus BASELINE's random sym-uniform, at N = 4096, 16384 and the
-largest N whose dense n x n fits the 32-bit cuSOLVER dense API (32768; the paper used 49,152); dsterf only to
+largest N whose syevd workspace fits the 32-bit cuSOLVER dense API (24576; the paper used 49,152); dsterf only to
 16384).  Writes one JSON document (stdout and --out).
 
     python tools/library_baseline.py --out profiles/r02/library_baseline.json
@@ -71,7 +71,7 @@ def br_values(solver, d, e, reps: int = 5) -> tuple[float, np.ndarray]:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="")
-    ap.add_argument("--sizes", default="4096,16384,32768")
+    ap.add_argument("--sizes", default="4096,16384,24576")
     a = ap.parse_args()
     import scipy.linalg as sl
     import torch
