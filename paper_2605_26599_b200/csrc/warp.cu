@@ -142,9 +142,44 @@ k_secular_warp(Work w, LevelDev L, int n, int patched) {
     // a window that fits one tile is loaded once for all evaluation rounds;
     // a larger one streams through the two tiles every round
     const bool resident = P1 - P0 <= kSecWTile;
-    if (resident) tile_fetch(s_tiles, w, P0, P1);
+    if (resident) {
+        tile_fetch(s_tiles, w, P0, P1);
+        cp_async_wait_all();
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    if (resident) {
+        // the whole window is in shared memory: every warp runs its roots to
+        // convergence on its own (no per-evaluation block barriers; the few-root
+        // top levels of random inputs were bound by those rounds)
+        unsigned long long ev = 0, tm = 0;
+        for (;;) {
+            int qq = 0;
+            if (lane == 0) qq = atomicAdd(&s_next, 1);
+            qq = __shfl_sync(0xffffffffu, qq, 0);
+            if (c0 + qq >= c1) break;
+            const int gg = c0 + qq;
+            if (!owns(w, gg)) continue;  // another rank's root (root-range split)
+            const int m = w.aMerge[gg];
+            int kss, ke;
+            merge_active(w, L, m, kss, ke);
+            if (!split_mode(L.mSize[m], ke - kss)) continue;  // lane-per-root tier owns it
+            const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+            int o;
+            double tu;
+            root_warp(s_tiles + (kss - P0), w.zA + kss, ke - kss, gg - kss, rho, w.exact != 0, patched != 0,
+                      w.status, o, tu, ev, tm);
+            if (lane == 0) {
+                w.org[gg] = o;
+                w.tau[gg] = tu;
+            }
+        }
+        if (lane == 0 && ev) {
+            atomicAdd(&w.counters[0], ev);
+            atomicAdd(&w.counters[1], tm);
+        }
+        return;
+    }
 
     RootSM st[NS];
     int g[NS], ks[NS];
@@ -505,7 +540,7 @@ __global__ void __launch_bounds__(kWarpThreads, BRGPU_ROWS_MINB) k_rows_warp(Wor
                     R.dorg = w.dA[R.ks + w.org[R.g]];
                     R.tau = w.tau[R.g];
                     const double lam = R.dorg + R.tau;
-                    const int pos = j + count_leq(w.D + off, size, lam) - count_leq(w.dA + R.ks, R.K, lam);
+                    const int pos = j + warp_count_leq(w.D + off, size, lam) - warp_count_leq(w.dA + R.ks, R.K, lam);
                     R.p = off + pos;
                     if (lane == 0) {
                         w.lam[R.p] = lam;
