@@ -97,6 +97,26 @@ def traffic_bytes(config: str, kernel: str):
     return None
 
 
+def library_baseline() -> dict:
+    """The GPU library baseline of SURVEY §8(f)-4 from the committed measurement
+    (tools/library_baseline.py; cusolverDnXstedc is absent from this image)."""
+    out = {"cusolverDnXstedc": "absent from this image's cuSOLVER 11.7 (CUDA 12.9); PAPER.md:1914 used CUDA 13.2",
+           "measured": "profiles/r02/library_baseline.json: cuSOLVER syevd (values only) on the tridiagonal "
+                       "stored densely, tools/library_baseline.py"}
+    try:
+        rows = json.loads((ROOT / "profiles" / "r02" / "library_baseline.json").read_text())["rows"]
+        big = max(r["n"] for r in rows if "cusolver_syevd_s" in r)
+        sel = [r for r in rows if r["n"] == big and "cusolver_syevd_s" in r]
+        out["largest_n"] = big
+        out["syevd_s"] = {r["family"]: round(r["cusolver_syevd_s"], 4) for r in sel}
+        out["syevd_over_br"] = {r["family"]: round(r["syevd_over_br"], 1) for r in sel}
+        out["syevd_workspace_bytes"] = sel[0].get("syevd_workspace_bytes")
+        out["br_workspace_bytes"] = sel[0].get("br_workspace_bytes")
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
+
+
 def _env_int(k, d):
     try:
         return int(os.environ.get(k, d))
@@ -482,11 +502,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
             "hbm_peak_source": hb_src,
             "cpu_baseline": cpu,
             "cpu_variants": variants,
-            "library_baseline": {
-                "cusolverDnXstedc": "absent from this image's cuSOLVER 11.7 (CUDA 12.9); PAPER.md:1914 "
-                                    "used CUDA 13.2",
-                "measured": "profiles/r02/library_baseline.json (cuSOLVER dense syevd jobz=N on the "
-                            "tridiagonal, tools/library_baseline.py)"},
+            "library_baseline": library_baseline(),
             "clocks": clocks,
             "gpu_launches": launches * args.steps,
             "kernel_profile_ms": {k: round(v[0], 4) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])},
