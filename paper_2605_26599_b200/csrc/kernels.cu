@@ -510,12 +510,7 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int
 #define BRGPU_WALK_BATCH 8
 #endif
 constexpr int kWalkBatch = BRGPU_WALK_BATCH;  // NN entries loaded per step of a long segment walk
-__global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
-    pdl_entry();
-    if (!dense_entry(L)) return;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    const int NN = w.nnPre[n];
-    if (q >= NN) return;
+__device__ __forceinline__ void walk_one(const Work& w, const LevelDev& L, int q, double tol_scale) {
     const int k = w.nnPos[q];
     const int m = find_merge(L, k);
     const int off = L.mOff[m];
@@ -582,6 +577,17 @@ __global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     }
 }
 
+// Grid-stride over the NN list: the grid is sized for the worst case (n) but
+// random inputs keep ~100 NN entries per merge, so a bounded grid walks them
+// without launching thousands of empty CTAs.
+__global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
+    pdl_entry();
+    if (!dense_entry(L)) return;
+    const int NN = w.nnPre[n];
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < NN; q += gridDim.x * blockDim.x)
+        walk_one(w, L, q, tol_scale);
+}
+
 // survivor prefix over NN indices + compacted active problem (deflate.cpp:100-105),
 // one pass; tile 0 always runs so survPre[NN] is written even when NN == 0
 __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, int n,
@@ -590,38 +596,43 @@ __global__ void __launch_bounds__(kScanBlock) k_surv_scan(Work w, LevelDev L, in
     if (!dense_entry(L)) return;
     __shared__ int s_tile, s_pref;
     const int NN = w.nnPre[n];
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile > 0 && tile * kScanBlock >= NN) return;  // uniform per CTA
-    const int q = tile * kScanBlock + threadIdx.x;
-    const int f = q < NN ? w.survFlag[q] : 0;
-    if (q < NN && !f) {  // group member: rotation-chain update from its prefix (k_segment_walk)
-        const int k = w.nnPos[q];
-        double x0 = w.R0[k], x1 = w.R1[k];
-        group_member(w.lam[k], w.blo[k], w.bhi[k], w.Z[k], x0, x1);
-        w.R0[k] = x0;
-        w.R1[k] = x1;
-        w.Z[k] = 0.0;
-    }
-    int tot;
-    const int ex = block_exclusive_scan<kScanBlock>(f, tot);
-    const int base = cta_lookback(state, tile, tot, &s_pref);
-    const int g = base + ex;
-    if (q < NN) {
-        w.survPre[q] = g;
-        if (f) {
+    // persistent: tiles in ticket order (the look-back waits only on earlier
+    // tickets, held by resident CTAs); tile 0 always runs so survPre[NN] is written
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile > 0 && tile * kScanBlock >= NN) break;  // uniform per CTA
+        const int q = tile * kScanBlock + threadIdx.x;
+        const int f = q < NN ? w.survFlag[q] : 0;
+        if (q < NN && !f) {  // group member: rotation-chain update from its prefix (k_segment_walk)
             const int k = w.nnPos[q];
-            const double z = w.Z[k];
-            w.dA[g] = w.D[k];
-            w.zA[g] = z;
-            w.z2A[g] = z * z;
-            w.r0A[g] = w.R0[k];
-            w.r1A[g] = w.R1[k];
-            w.aMerge[g] = find_merge(L, k);
+            double x0 = w.R0[k], x1 = w.R1[k];
+            group_member(w.lam[k], w.blo[k], w.bhi[k], w.Z[k], x0, x1);
+            w.R0[k] = x0;
+            w.R1[k] = x1;
+            w.Z[k] = 0.0;
         }
+        int tot;
+        const int ex = block_exclusive_scan<kScanBlock>(f, tot);
+        const int base = cta_lookback(state, tile, tot, &s_pref);
+        const int g = base + ex;
+        if (q < NN) {
+            w.survPre[q] = g;
+            if (f) {
+                const int k = w.nnPos[q];
+                const double z = w.Z[k];
+                w.dA[g] = w.D[k];
+                w.zA[g] = z;
+                w.z2A[g] = z * z;
+                w.r0A[g] = w.R0[k];
+                w.r1A[g] = w.R1[k];
+                w.aMerge[g] = find_merge(L, k);
+            }
+        }
+        if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= NN) w.survPre[NN] = base + tot;
+        __syncthreads();  // s_tile / s_pref reuse
     }
-    if (threadIdx.x == kScanBlock - 1 && (tile + 1) * kScanBlock >= NN) w.survPre[NN] = base + tot;
 }
 
 // Start of a grid-tier level: zero the per-merge scale words, the look-back
@@ -1237,9 +1248,9 @@ void launch_level_part(cudaStream_t s, const Work& w, const LevelDev& L, int n, 
         launch_pdl(k_merge_nn, mtiles, kMergeTile, 0, s, w, L, n, prm.tol_scale, w.org, st1, tk);
         PMARK(BRGPU_K_NNFLAG);
         if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 0, &nl);
-        launch_pdl(k_segment_walk, cdiv(n, 256), 256, 0, s, w, L, n, prm.tol_scale);
+        launch_pdl(k_segment_walk, min(cdiv(n, 256), prm.sms * 8), 256, 0, s, w, L, n, prm.tol_scale);
         PMARK(BRGPU_K_WALK);
-        launch_pdl(k_surv_scan, ntiles, kScanBlock, 0, s, w, L, n, st2, tk + 1);
+        launch_pdl(k_surv_scan, min(ntiles, prm.sms * 2), kScanBlock, 0, s, w, L, n, st2, tk + 1);
         PMARK(BRGPU_K_SURVWRITE);
         if (prm.sigma) launch_sigma_stage(s, w, L, *prm.sigma, L.maxSize, 1, &nl);
         nl += 4;
