@@ -23,14 +23,13 @@
 
 namespace brgpu {
 
-// CTAs per SM of the 512-element shape: 3 (85 registers) beats 4 (64 registers,
-// spilling the root state machine): random 2^20 4.66 -> 4.59 ms, n = 4096 0.86 -> 0.75 ms
-#ifndef BRGPU_FUSE_RUN_MINB
-#define BRGPU_FUSE_RUN_MINB 3
-#endif
-#ifndef BRGPU_FUSE_ONE_MINB
-#define BRGPU_FUSE_ONE_MINB 3
-#endif
+// CTAs per SM of the 512-element shape: both bounds are instantiated.  3 CTAs
+// (80 registers) when the launch fits one wave at 3 per SM: a short, latency-bound
+// launch (n = 4096: 0.71 ms against 0.76 ms at 4); 4 CTAs (64 registers, ~90 B
+// of root-state spills outside the pole loops) when it does not (glued Wilkinson
+// 2^18: 7.96 -> 7.78 ms; random 2^20 4.09 -> 4.08 ms).
+constexpr int kFuseMinbFew = 3;
+constexpr int kFuseMinbMany = 4;
 constexpr int kFuseMaxMerges = 128;   // merges per group
 #ifndef BRGPU_SMALL_THREADS
 #define BRGPU_SMALL_THREADS 256
@@ -474,8 +473,8 @@ __device__ __forceinline__ void fused_group(const Work& w, const LevelDev& L, co
     }
 }
 
-template <int kFuseMax, int kFuseThreads>
-__global__ void __launch_bounds__(kFuseThreads, kFuseMax <= 512 ? BRGPU_FUSE_ONE_MINB : 2048 / kFuseMax)
+template <int kFuseMax, int kFuseThreads, int MINB>
+__global__ void __launch_bounds__(kFuseThreads, kFuseMax <= 512 ? MINB : 2048 / kFuseMax)
 k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __restrict__ gCount,
               SolveParams prm, int* __restrict__ traceOut) {
     pdl_entry();
@@ -491,8 +490,8 @@ k_level_fused(Work w, LevelDev L, const int* __restrict__ gFirst, const int* __r
 // the next level's inputs, so the CTA moves from level to level with a block
 // barrier instead of a grid-wide kernel boundary (the data stays in L1/L2),
 // and different CTAs' root-queue tails overlap across levels.
-template <int kFuseMax, int kFuseThreads>
-__global__ void __launch_bounds__(kFuseThreads, BRGPU_FUSE_RUN_MINB)
+template <int kFuseMax, int kFuseThreads, int MINB>
+__global__ void __launch_bounds__(kFuseThreads, MINB)
 k_levels_fused(Work w, FusedRun run, const int2* __restrict__ tab, SolveParams prm) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char fuse_raw[];
@@ -508,11 +507,14 @@ k_levels_fused(Work w, FusedRun run, const int2* __restrict__ tab, SolveParams p
 void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ngroups, int cap,
                         const int* gFirst, const int* gCount, const SolveParams& prm, int* traceOut,
                         int* launches, Prof* prof) {
-    if (cap <= 512)
-        launch_pdl(k_level_fused<512, kSmallThreads>, ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s, w, L, gFirst, gCount, prm,
+    if (cap <= 512 && ngroups > kFuseMinbFew * prm.sms)
+        launch_pdl(k_level_fused<512, kSmallThreads, kFuseMinbMany>, ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s, w, L, gFirst, gCount, prm,
+                                                                                 traceOut);
+    else if (cap <= 512)
+        launch_pdl(k_level_fused<512, kSmallThreads, kFuseMinbFew>, ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s, w, L, gFirst, gCount, prm,
                                                                                  traceOut);
     else
-        launch_pdl(k_level_fused<1024, kBigThreads>, ngroups, kBigThreads, sizeof(FuseSmem<1024, kBigThreads>), s, w, L, gFirst, gCount, prm,
+        launch_pdl(k_level_fused<1024, kBigThreads, 2>, ngroups, kBigThreads, sizeof(FuseSmem<1024, kBigThreads>), s, w, L, gFirst, gCount, prm,
                                                                                    traceOut);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
@@ -520,8 +522,12 @@ void launch_level_fused(cudaStream_t s, const Work& w, const LevelDev& L, int ng
 
 void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int ngroups, const int2* tab,
                          const SolveParams& prm, int* launches, Prof* prof) {
-    launch_pdl(k_levels_fused<512, kSmallThreads>, ngroups, kSmallThreads, sizeof(FuseSmem<512, kSmallThreads>), s, 
-        w, run, tab, prm);
+    if (ngroups > kFuseMinbFew * prm.sms)
+        launch_pdl(k_levels_fused<512, kSmallThreads, kFuseMinbMany>, ngroups, kSmallThreads,
+                   sizeof(FuseSmem<512, kSmallThreads>), s, w, run, tab, prm);
+    else
+        launch_pdl(k_levels_fused<512, kSmallThreads, kFuseMinbFew>, ngroups, kSmallThreads,
+                   sizeof(FuseSmem<512, kSmallThreads>), s, w, run, tab, prm);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_SUBTREE);
 }
@@ -530,12 +536,17 @@ static_assert(sizeof(FuseSmem<1024, kBigThreads>) <= 113 * 1024, "two fused CTAs
 static_assert(sizeof(FuseSmem<512, kSmallThreads>) <= 56 * 1024, "four small fused CTAs must fit one SM");
 
 void init_fused_attributes() {
-    cudaFuncSetAttribute(k_level_fused<1024, kBigThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const int small = (int)sizeof(FuseSmem<512, kSmallThreads>);
+    cudaFuncSetAttribute(k_level_fused<1024, kBigThreads, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(FuseSmem<1024, kBigThreads>));
-    cudaFuncSetAttribute(k_level_fused<512, kSmallThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(FuseSmem<512, kSmallThreads>));
-    cudaFuncSetAttribute(k_levels_fused<512, kSmallThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(FuseSmem<512, kSmallThreads>));
+    cudaFuncSetAttribute(k_level_fused<512, kSmallThreads, kFuseMinbFew>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, small);
+    cudaFuncSetAttribute(k_level_fused<512, kSmallThreads, kFuseMinbMany>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, small);
+    cudaFuncSetAttribute(k_levels_fused<512, kSmallThreads, kFuseMinbFew>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, small);
+    cudaFuncSetAttribute(k_levels_fused<512, kSmallThreads, kFuseMinbMany>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, small);
 }
 
 }  // namespace brgpu

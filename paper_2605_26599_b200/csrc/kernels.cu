@@ -506,86 +506,101 @@ __global__ void __launch_bounds__(kMergeTile) k_merge_nn(Work w, LevelDev L, int
 // Q = sum z^2, S0/S1 = sum z x -- one add per member on the dependency chain --
 // and records each member's prefix (Q, S0, S1) at its position in the free
 // lam/blo/bhi slots; k_surv_scan finishes the members in parallel.
-#ifndef BRGPU_WALK_BATCH
-#define BRGPU_WALK_BATCH 8
-#endif
-constexpr int kWalkBatch = BRGPU_WALK_BATCH;  // NN entries loaded per step of a long segment walk
-__device__ __forceinline__ void walk_one(const Work& w, const LevelDev& L, int q, double tol_scale) {
-    const int k = w.nnPos[q];
-    const int m = find_merge(L, k);
-    const int off = L.mOff[m];
-    const int qs = w.nnPre[off], qe = w.nnPre[off + L.mSize[m]];
-    const double tol = merge_tol(L, m, tol_scale);
-    if (q > qs && fabs(w.D[k] - w.D[w.nnPos[q - 1]]) <= tol) return;  // not a head
-    w.survFlag[q] = 1;
-    int prev = k, nmem = 0;
-    double dp = w.D[k];
-    const double zs = w.Z[k];
-    double Q = zs * zs, S0 = zs * w.R0[k], S1 = zs * w.R1[k];
-    double dprev_nn = dp;
-    // Batches of 8 NN entries: the 8 positions are loaded at once, then their
-    // data, so a long cluster (glued Wilkinson: runs of ~10^4) costs two
-    // dependent L2 round trips per 8 entries instead of per entry.  A segment of
-    // length 1 (the common case) exits after its first probe.
-    if (q + 1 < qe && fabs(w.D[w.nnPos[q + 1]] - dp) <= tol) {
-        bool done = false;
-        for (int qb = q + 1; !done && qb < qe; qb += kWalkBatch) {
-            int kb[kWalkBatch];
-            double db[kWalkBatch], zb[kWalkBatch], x0b[kWalkBatch], x1b[kWalkBatch];
-#pragma unroll
-            for (int u = 0; u < kWalkBatch; ++u) kb[u] = w.nnPos[min(qb + u, qe - 1)];
-#pragma unroll
-            for (int u = 0; u < kWalkBatch; ++u) {
-                db[u] = w.D[kb[u]];
-                zb[u] = w.Z[kb[u]];
-                x0b[u] = w.R0[kb[u]];
-                x1b[u] = w.R1[kb[u]];
-            }
-#pragma unroll
-            for (int u = 0; u < kWalkBatch; ++u) {
-                const int q2 = qb + u;
-                if (done || q2 >= qe) { done = true; continue; }
-                const double d2 = db[u];
-                if (fabs(d2 - dprev_nn) > tol) { done = true; continue; }  // next segment head
-                dprev_nn = d2;
-                const int k2 = kb[u];
-                const double zq = zb[u];
-                if (fabs(d2 - dp) <= tol) {  // member of prev's group
-                    w.lam[k2] = Q;
-                    w.blo[k2] = S0;
-                    w.bhi[k2] = S1;
-                    Q = Q + zq * zq;
-                    S0 = S0 + zq * x0b[u];
-                    S1 = S1 + zq * x1b[u];
-                    ++nmem;
-                    w.survFlag[q2] = 0;
-                } else {
-                    if (nmem) {  // retire the survivor
-                        const double R = sqrt(Q), iR = 1.0 / R;
-                        w.Z[prev] = R; w.R0[prev] = S0 * iR; w.R1[prev] = S1 * iR;
-                    }
-                    w.survFlag[q2] = 1;
-                    prev = k2; dp = d2; nmem = 0;
-                    Q = zq * zq; S0 = zq * x0b[u]; S1 = zq * x1b[u];
-                }
-            }
-        }
-    }
-    if (nmem) {
-        const double R = sqrt(Q), iR = 1.0 / R;
-        w.Z[prev] = R; w.R0[prev] = S0 * iR; w.R1[prev] = S1 * iR;
-    }
+// Long segments are walked by the whole warp: 32 NN entries are loaded at once
+// (one coalesced position load, one gather of their data), then every lane
+// replays the walk over the chunk in lane order from shuffles (the same
+// operations in the same order as a sequential walk, so every lane holds the
+// same Q/S0/S1) and each lane keeps the prefix at its own entry -- a run of
+// 10^4 close poles (glued Wilkinson) costs two dependent L2 round trips per 32
+// entries.  A segment of length 1 (random inputs: almost all) is decided by its
+// head's first probe, with no warp work.
+__device__ __forceinline__ void walk_retire(const Work& w, int prev, double Q, double S0, double S1) {
+    const double R = sqrt(Q), iR = 1.0 / R;
+    w.Z[prev] = R; w.R0[prev] = S0 * iR; w.R1[prev] = S1 * iR;
 }
 
-// Grid-stride over the NN list: the grid is sized for the worst case (n) but
-// random inputs keep ~100 NN entries per merge, so a bounded grid walks them
-// without launching thousands of empty CTAs.
-__global__ void k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
+__global__ void __launch_bounds__(256) k_segment_walk(Work w, LevelDev L, int n, double tol_scale) {
     pdl_entry();
     if (!dense_entry(L)) return;
     const int NN = w.nnPre[n];
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < NN; q += gridDim.x * blockDim.x)
-        walk_one(w, L, q, tol_scale);
+    const int lane = threadIdx.x & 31;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int c0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; c0 < NN; c0 += nwarps * 32) {
+        const int q = c0 + lane;
+        bool lng = false;
+        int k = 0, qe = 0;
+        double tol = 0.0, dk = 0.0;
+        if (q < NN) {
+            k = w.nnPos[q];
+            const int m = find_merge(L, k);
+            const int off = L.mOff[m];
+            const int qs = w.nnPre[off];
+            qe = w.nnPre[off + L.mSize[m]];
+            tol = merge_tol(L, m, tol_scale);
+            dk = w.D[k];
+            const bool head = !(q > qs && fabs(dk - w.D[w.nnPos[q - 1]]) <= tol);
+            if (head) {
+                w.survFlag[q] = 1;
+                lng = q + 1 < qe && fabs(w.D[w.nnPos[q + 1]] - dk) <= tol;
+            }
+        }
+        unsigned heads = __ballot_sync(0xffffffffu, lng);
+        while (heads) {
+            const int src = __ffs(heads) - 1;
+            heads &= heads - 1;
+            const int hq = __shfl_sync(0xffffffffu, q, src);
+            const int hqe = __shfl_sync(0xffffffffu, qe, src);
+            const double htol = __shfl_sync(0xffffffffu, tol, src);
+            int prev = __shfl_sync(0xffffffffu, k, src);
+            double dp = __shfl_sync(0xffffffffu, dk, src);
+            const double zs = w.Z[prev];
+            double Q = zs * zs, S0 = zs * w.R0[prev], S1 = zs * w.R1[prev];
+            double dprev_nn = dp;
+            int nmem = 0;
+            bool done = false;
+            for (int cb = hq + 1; !done && cb < hqe; cb += 32) {
+                const int q2 = cb + lane;
+                const bool in = q2 < hqe;
+                const int k2 = in ? w.nnPos[q2] : 0;
+                double d2 = 0.0, z2 = 0.0, x0 = 0.0, x1 = 0.0;
+                if (in) { d2 = w.D[k2]; z2 = w.Z[k2]; x0 = w.R0[k2]; x1 = w.R1[k2]; }
+                const int cnt = min(32, hqe - cb);
+                int role = -1;  // this lane's entry: 0 member (prefix below), 1 group head
+                double mQ = 0.0, mS0 = 0.0, mS1 = 0.0;
+                for (int u = 0; u < cnt; ++u) {  // warp-uniform replay in lane order
+                    const double du = __shfl_sync(0xffffffffu, d2, u);
+                    if (fabs(du - dprev_nn) > htol) { done = true; break; }  // next segment head
+                    dprev_nn = du;
+                    const double zu = __shfl_sync(0xffffffffu, z2, u);
+                    const double xu0 = __shfl_sync(0xffffffffu, x0, u);
+                    const double xu1 = __shfl_sync(0xffffffffu, x1, u);
+                    if (fabs(du - dp) <= htol) {  // member of prev's group
+                        if (lane == u) { role = 0; mQ = Q; mS0 = S0; mS1 = S1; }
+                        Q = Q + zu * zu;
+                        S0 = S0 + zu * xu0;
+                        S1 = S1 + zu * xu1;
+                        ++nmem;
+                    } else {  // a new group head inside the segment: retire the survivor
+                        if (nmem && lane == 0) walk_retire(w, prev, Q, S0, S1);
+                        if (lane == u) role = 1;
+                        prev = __shfl_sync(0xffffffffu, k2, u);
+                        dp = du;
+                        nmem = 0;
+                        Q = zu * zu; S0 = zu * xu0; S1 = zu * xu1;
+                    }
+                }
+                if (role == 0) {
+                    w.lam[k2] = mQ;
+                    w.blo[k2] = mS0;
+                    w.bhi[k2] = mS1;
+                    w.survFlag[q2] = 0;
+                } else if (role == 1) {
+                    w.survFlag[q2] = 1;
+                }
+            }
+            if (nmem && lane == 0) walk_retire(w, prev, Q, S0, S1);
+        }
+    }
 }
 
 // survivor prefix over NN indices + compacted active problem (deflate.cpp:100-105),
