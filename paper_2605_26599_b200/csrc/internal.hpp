@@ -45,7 +45,7 @@ struct Work {
     int* nnPos;      // NN index -> sorted position
     int* survPre;    // exclusive prefix of survivor flags over NN indices (n+1)
     int* aMerge;     // active index -> merge id (within level)
-    int* org;        // root origin (merge-local pole index)
+    int* org;        // root origin (level-global active pole index; k_rows reuses it for the parent position)
     uint8_t* nnFlag;
     uint8_t* survFlag;
     int* tileCnt;    // per-1024 tile counts (scan scratch)

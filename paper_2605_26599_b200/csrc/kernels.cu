@@ -722,6 +722,7 @@ constexpr int kSecWinQ = BRGPU_SEC_WIN;
 #endif
 constexpr int kSecMinbSmall = BRGPU_SEC_MINB_SMALL;  // k_secular CTAs per SM below kSecBigLevel elements
 constexpr int kSecBigLevel = 1 << 21;
+constexpr int kSecMeta = 256;  // merges of a chunk staged in shared memory (more: global lookups)
 // Secular roots (secular.cpp:80-241, tau-relative stop when patched).
 // A CTA owns a chunk of roots; each lane runs one root's iteration as a
 // resumable state machine (RootSM) and pulls the next root from a CTA queue
@@ -733,24 +734,51 @@ __global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w, LevelDev L,
     if (!dense_entry(L)) return;
     __shared__ double2 s_dz[kSecWinQ];
     __shared__ double2 s_snap[kSecBlock];
-    __shared__ int s_next;
+    // per-merge table of the chunk's merges (active range start, rho, size):
+    // the root queue and the iteration then touch no global metadata
+    __shared__ int s_ks[kSecMeta + 1], s_sz[kSecMeta];
+    __shared__ double s_rho[kSecMeta];
+    __shared__ int s_next, s_nextLast;
     if (!(*w.levelModes & 1)) return;
     const int T = w.survPre[w.nnPre[n]];
     const int R = max(kSecBlock, (T + (int)gridDim.x - 1) / (int)gridDim.x);
     const int c0 = blockIdx.x * R;
     if (c0 >= T) return;  // uniform per CTA
     const int c1 = min(c0 + R, T);
-    if (!chunk_has_mode(w, L, c0, c1, false)) return;  // all roots belong to warp.cu
-    const Window win = range_window(w, L, c0, c1, kSecWinQ);
+    const int m0 = w.aMerge[c0];
+    const int nm = w.aMerge[c1 - 1] - m0 + 1;
+    const bool meta = nm <= kSecMeta;  // uniform per CTA
+    Window win;
+    if (meta) {
+        int lane_mode = 0;
+        for (int t = threadIdx.x; t <= nm; t += kSecBlock) {
+            const int m = m0 + min(t, nm - 1);
+            const int off = L.mOff[m], size = L.mSize[m];
+            s_ks[t] = w.survPre[w.nnPre[t < nm ? off : off + size]];
+            if (t < nm) {
+                s_sz[t] = size;
+                s_rho[t] = fabs(w.ew[off + L.mNL[m] - 1]);
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nm; t += kSecBlock) {
+            const int K = s_ks[t + 1] - s_ks[t];
+            lane_mode |= K > 0 && !split_mode(s_sz[t], K);
+        }
+        if (!__syncthreads_or(lane_mode)) return;  // all roots belong to warp.cu
+        win.P0 = s_ks[0];
+        win.P1 = s_ks[nm];
+        win.fits = win.P1 - win.P0 <= kSecWinQ;
+    } else {
+        if (!chunk_has_mode(w, L, c0, c1, false)) return;  // all roots belong to warp.cu
+        win = range_window(w, L, c0, c1, kSecWinQ);
+    }
     if (!win.fits) return;  // large-K chunk: k_secular_tiled (tiled.cu) owns it
     for (int i = threadIdx.x; i < win.P1 - win.P0; i += kSecBlock)
         s_dz[i] = make_double2(w.dA[win.P0 + i], w.z2A[win.P0 + i]);
-    __shared__ int s_nextLast, s_m0, s_nm;
     if (threadIdx.x == 0) {
         s_next = 0;
         s_nextLast = 0;
-        s_m0 = w.aMerge[c0];
-        s_nm = w.aMerge[c1 - 1] - s_m0 + 1;
     }
     __syncthreads();
 
@@ -765,29 +793,37 @@ __global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w, LevelDev L,
         // one-pole iteration averages ~2.5x the evaluations of an interior root),
         // then the interior roots in order -- never changes a result
         while (g < 0 && !exhausted) {
-            int m, ke, gg;
+            int m = 0, t = 0, ke, gg;
             if (!lastDone) {
-                const int t = atomicAdd(&s_nextLast, 1);
-                if (t >= s_nm) { lastDone = true; continue; }
-                m = s_m0 + t;
-                active_range(w, L, m, ks, ke);
+                t = atomicAdd(&s_nextLast, 1);
+                if (t >= nm) { lastDone = true; continue; }
+                m = m0 + t;
+                if (meta) { ks = s_ks[t]; ke = s_ks[t + 1]; } else active_range(w, L, m, ks, ke);
                 gg = ke - 1;
                 if (gg < c0 || gg >= c1 || gg < ks) continue;  // not in this chunk (or K = 0)
             } else {
                 const int q = atomicAdd(&s_next, 1);
                 if (c0 + q >= c1) { exhausted = true; break; }
                 gg = c0 + q;
-                m = w.aMerge[gg];
-                active_range(w, L, m, ks, ke);
+                if (meta) {
+                    t = upper_index(s_ks, nm, gg);
+                    ks = s_ks[t];
+                    ke = s_ks[t + 1];
+                } else {
+                    m = w.aMerge[gg];
+                    active_range(w, L, m, ks, ke);
+                }
                 if (gg == ke - 1) continue;  // a last root: already taken
             }
             if (!owns(w, gg)) continue;  // another rank's root (root-range split)
-            if (split_mode(L.mSize[m], ke - ks)) continue;  // warp-per-root tier (warp.cu)
+            const int K = ke - ks;
+            if (split_mode(meta ? s_sz[t] : L.mSize[m], K)) continue;  // warp-per-root tier (warp.cu)
             g = gg;
-            const double rho = fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
-            rs_begin(st, ke - ks, g - ks, rho, PolesPtr{w.dA + ks}, w.zA[ks], Z2Ptr{w.z2A + ks});
+            const double rho = meta ? s_rho[t] : fabs(w.ew[L.mOff[m] + L.mNL[m] - 1]);
+            const double2* pz = s_dz + (ks - win.P0);
+            rs_begin(st, K, g - ks, rho, PolesPairs{pz}, K == 1 ? w.zA[ks] : 0.0, Z2Pairs{pz});
             if (st.phase == kRsDone) {
-                w.org[g] = st.org;
+                w.org[g] = ks + st.org;
                 w.tau[g] = st.tau;
                 g = -1;
             }
@@ -810,10 +846,10 @@ __global__ void __launch_bounds__(kSecBlock, MINB) k_secular(Work w, LevelDev L,
             ev.pole = pole;
             ++evals;
             terms += (unsigned long long)K;
-            rs_consume(st, ev, PolesPtr{w.dA + ks}, Z2Ptr{w.z2A + ks}, patched != 0);
+            rs_consume(st, ev, PolesPairs{s_dz + (ks - win.P0)}, Z2Pairs{s_dz + (ks - win.P0)}, patched != 0);
             if (st.phase == kRsDone || st.phase == kRsFail) {
                 if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
-                w.org[g] = st.org;
+                w.org[g] = ks + st.org;
                 w.tau[g] = st.tau;
                 g = -1;
             }
@@ -884,9 +920,7 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
         const int thi = min(tlo + kWin, win.P1);
         __syncthreads();
         for (int r = tlo + threadIdx.x; r < thi; r += kSecBlock) {
-            int rks, rke;
-            active_range(w, L, w.aMerge[r], rks, rke);
-            s_dorg[r - tlo] = w.dA[rks + w.org[r]];
+            s_dorg[r - tlo] = w.dA[w.org[r]];
             s_tau[r - tlo] = w.tau[r];
             s_dj[r - tlo] = w.dA[r];
         }
@@ -909,7 +943,7 @@ __global__ void __launch_bounds__(kSecBlock) k_zhat(Work w, LevelDev L, int n) {
         const int* __restrict__ org = w.org + ks;
         prod = 1.0;
         for (int j = 0; j < K; ++j) {
-            const double del = (di - dA[org[j]]) - tau[j];
+            const double del = (di - w.dA[org[j]]) - tau[j];
             if (j == i) prod = prod * del;
             else prod = prod * (del * __drcp_rn(di - dA[j]));
         }
@@ -948,7 +982,7 @@ __global__ void __launch_bounds__(kSecBlock) k_rows(Work w, LevelDev L, int n) {
         K = ke - ks;
         const int j = g - ks;
         const int off = L.mOff[m], size = L.mSize[m];
-        dorg = w.dA[ks + w.org[g]];
+        dorg = w.dA[w.org[g]];
         tau = w.tau[g];
         const double lam = dorg + tau;
         // parent position: j + #{deflated <= lam} = j + #{D <= lam} - #{dA <= lam}

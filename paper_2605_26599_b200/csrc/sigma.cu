@@ -157,7 +157,7 @@ __global__ void k_sig_out(Work w, LevelDev L, SigmaDev sg) {
     const double* dA = w.dA + ks;
     if (u < K) {
         const int g = ks + u;
-        const double dorg = dA[w.org[g]], tau = w.tau[g];
+        const double dorg = w.dA[w.org[g]], tau = w.tau[g];
         const double lam = dorg + tau;
         const int pos = u + count_leq(w.D + off, size, lam) - count_leq(dA, K, lam);
         const double* zh = w.zA + ks;
@@ -182,7 +182,7 @@ __global__ void k_sig_out(Work w, LevelDev L, SigmaDev sg) {
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         const int g = ks + mid;
-        if (dA[w.org[g]] + w.tau[g] < v) lo = mid + 1; else hi = mid;
+        if (w.dA[w.org[g]] + w.tau[g] < v) lo = mid + 1; else hi = mid;
     }
     Sr[off + t + lo] = X[k];
 }

@@ -80,7 +80,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
             const double rho = fabs(w.ew[off + L.mNL[m] - 1]);
             rs_begin(st, ke - ks, g - ks, rho, PolesPtr{w.dA + ks}, w.zA[ks], Z2Ptr{w.z2A + ks});
             if (st.phase == kRsDone) {
-                w.org[g] = st.org;
+                w.org[g] = ks + st.org;
                 w.tau[g] = st.tau;
                 g = -1;
             }
@@ -147,7 +147,7 @@ k_secular_tiled(Work w, LevelDev L, int n, int patched, int G) {
             rs_consume(st, ev, PolesPtr{w.dA + ks}, Z2Ptr{w.z2A + ks}, patched != 0);
             if (st.phase == kRsDone || st.phase == kRsFail) {
                 if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
-                w.org[g] = st.org;
+                w.org[g] = ks + st.org;
                 w.tau[g] = st.tau;
                 g = -1;
             }

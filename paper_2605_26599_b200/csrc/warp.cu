@@ -170,7 +170,7 @@ k_secular_warp(Work w, LevelDev L, int n, int patched) {
             root_warp(s_tiles + (kss - P0), w.zA + kss, ke - kss, gg - kss, rho, w.exact != 0, patched != 0,
                       w.status, o, tu, ev, tm);
             if (lane == 0) {
-                w.org[gg] = o;
+                w.org[gg] = kss + o;
                 w.tau[gg] = tu;
             }
         }
@@ -211,7 +211,7 @@ k_secular_warp(Work w, LevelDev L, int n, int patched) {
                 }
                 rs_begin_zsq(st[q], K, j, rho, PolesPtr{w.dA + ks[q]}, w.zA[ks[q]], zsq, w.z2A[ks[q] + K - 1]);
                 if (st[q].phase == kRsDone) {
-                    if (lane == 0) { w.org[gg] = st[q].org; w.tau[gg] = st[q].tau; }
+                    if (lane == 0) { w.org[gg] = ks[q] + st[q].org; w.tau[gg] = st[q].tau; }
                     g[q] = -1;
                 }
             }
@@ -308,7 +308,7 @@ k_secular_warp(Work w, LevelDev L, int n, int patched) {
             if (S.phase == kRsDone || S.phase == kRsFail) {
                 if (lane == 0) {
                     if (S.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
-                    w.org[g[q]] = S.org;
+                    w.org[g[q]] = ks[q] + S.org;
                     w.tau[g[q]] = S.tau;
                 }
                 g[q] = -1;
@@ -384,9 +384,7 @@ __global__ void __launch_bounds__(kWarpThreads, BRGPU_ZHAT_MINB) k_zhat_warp(Wor
             const int thi = min(tlo + kWarpTile, P1);
             __syncthreads();
             for (int r = tlo + (int)threadIdx.x; r < thi; r += kWarpThreads) {
-                int rks, rke;
-                merge_active(w, L, w.aMerge[r], rks, rke);
-                s_dorg[r - tlo] = w.dA[rks + w.org[r]];
+                s_dorg[r - tlo] = w.dA[w.org[r]];
                 s_tau[r - tlo] = w.tau[r];
                 s_dj[r - tlo] = w.dA[r];
             }
@@ -457,7 +455,7 @@ __global__ void __launch_bounds__(kWarpThreads, BRGPU_ZHAT_MINB) k_zhat_warp(Wor
             if (!P.fast) {  // exact redo
                 P.prod = 1.0;
                 for (int jg = P.ks + lane; jg < P.ks + P.K; jg += 32) {
-                    const double del = (P.di - w.dA[P.ks + w.org[jg]]) - w.tau[jg];
+                    const double del = (P.di - w.dA[w.org[jg]]) - w.tau[jg];
                     if (jg - P.ks == P.i) P.prod = P.prod * del;
                     else P.prod = P.prod * (del * __drcp_rn(P.di - w.dA[jg]));
                 }
@@ -537,7 +535,7 @@ __global__ void __launch_bounds__(kWarpThreads, BRGPU_ROWS_MINB) k_rows_warp(Wor
                     R.K = ke - R.ks;
                     const int j = R.g - R.ks;
                     const int off = L.mOff[m], size = L.mSize[m];
-                    R.dorg = w.dA[R.ks + w.org[R.g]];
+                    R.dorg = w.dA[w.org[R.g]];
                     R.tau = w.tau[R.g];
                     const double lam = R.dorg + R.tau;
                     const int pos = j + warp_count_leq(w.D + off, size, lam) - warp_count_leq(w.dA + R.ks, R.K, lam);
