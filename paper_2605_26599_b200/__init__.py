@@ -136,6 +136,7 @@ class BrOptions:
     exact_passes: bool = False  # test hook: every pole pass through the exact-reciprocal path
     root_split: bool = True  # multi-rank: split the shared top merges' roots across ranks
     sparse: bool = False  # opt-in: grid levels with <= C non-negligible poles per merge run the sparse pipeline
+    live: bool = True  # top levels of large single-block solves on live lists (live.cu); dense fallback
 
 
 @dataclass
@@ -228,6 +229,9 @@ class Solver:
         if o.sparse or getattr(self, "_sparse_on", False):  # opt-in tier: set once enabled
             self._opt(_native.OPT_SPARSE, int(o.sparse))
             self._sparse_on = bool(o.sparse)
+        if not o.live or getattr(self, "_live_off", False):  # default on: set only once turned off
+            self._opt(_native.OPT_LIVE, int(o.live))
+            self._live_off = not o.live
         if self.nranks == 1:
             self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o

@@ -23,6 +23,7 @@ OPT_VIRTUAL_RANKS = 6
 OPT_EXACT_PASSES = 7
 OPT_ROOT_SPLIT = 8
 OPT_SPARSE = 9
+OPT_LIVE = 10
 
 
 class Stats(C.Structure):
@@ -58,7 +59,7 @@ EXPORTS = [
     "brgpu_phase_cycles", "brgpu_eigvals_dense_device", "brgpu_eigvals_rows",
 ]
 
-NCLASS = 20
+NCLASS = 22
 
 
 class Timing(C.Structure):

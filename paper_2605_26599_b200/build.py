@@ -34,7 +34,7 @@ NVCC_FLAGS = [
 CXX_FLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", f"-I{CUDA_HOME / 'include'}",
              f"-I{ROOT / 'include'}"]
 
-CU_SOURCES = ["kernels.cu", "fused.cu", "tiled.cu", "warp.cu", "sigma.cu", "sparse.cu"]
+CU_SOURCES = ["kernels.cu", "fused.cu", "tiled.cu", "warp.cu", "sigma.cu", "sparse.cu", "live.cu"]
 CPP_SOURCES = ["api.cpp"]
 
 

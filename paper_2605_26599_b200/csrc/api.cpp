@@ -20,6 +20,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -64,6 +65,22 @@ void launch_levels_fused(cudaStream_t s, const Work& w, const FusedRun& run, int
                          const SolveParams& prm, int* launches, Prof* prof);
 void init_fused_attributes();
 void init_warp_attributes();
+void launch_live_init(cudaStream_t s, const Work& w, const LiveDev& V, const int2* front, int nfront,
+                      double tol_scale, int* launches, Prof* prof);
+void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
+                       const SolveParams& prm, int* traceOut, int* launches, Prof* prof);
+void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int sms, int* launches, Prof* prof);
+int live_buckets(int n);
+void init_live_attributes();
+// Live-list tier (live.cu): single-block solves of at least kLiveMinN elements
+// run every level above the last fused / small one on live lists when all those
+// levels' merges are >= kLiveMinSize (random 2^20: levels 4..16)
+#ifndef BRGPU_LIVE_MIN_SIZE
+#define BRGPU_LIVE_MIN_SIZE 1024
+#endif
+constexpr int kLiveMinSize = BRGPU_LIVE_MIN_SIZE;
+constexpr int kLiveMinN = 1 << 15;
+constexpr int kRetryDense = 1000;  // internal: the live tier fell back, redo the solve densely
 #ifndef BRGPU_FUSE_MAX_ELEMS
 #define BRGPU_FUSE_MAX_ELEMS 1024
 #endif
@@ -77,7 +94,7 @@ constexpr int kGridManyMinSize = BRGPU_GRID_MANY_MIN_SIZE;  // ... when their me
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
 constexpr int kSpMinSpan = 16;        // smallest k_sp_solve group key span (group table size)
 #ifndef BRGPU_SPLIT_MIN_SIZE
-#define BRGPU_SPLIT_MIN_SIZE 8192
+#define BRGPU_SPLIT_MIN_SIZE (1 << 30)
 #endif
 constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
 constexpr int kFuseMaxMergesHost = 128;
@@ -126,6 +143,7 @@ struct LevelHost {
     int spCap = 0;     // sparse iff every merge has NN <= spCap
     int spSpan = 0;    // k_sp_solve group key span
     int ctl = 0;       // index of the level's control words (4 ints)
+    bool live = false; // live-list level (live.cu)
 };
 
 struct Plan {
@@ -175,6 +193,15 @@ struct Plan {
     int* h_ctl = nullptr;  // pinned copy of the control words after a solve (deflation profile)
     int dbgStop = 0;       // debug (BRGPU_DEBUG_STOP_LEVEL): run only the first k levels of phase 1
     bool anySp = false;
+    // live-list tier: first live level (index in `levels`, -1: none), frontier
+    // nodes (off, size) entering it, control words + key words, final-sort buckets
+    bool liveWanted = false;
+    int liveLev = -1;
+    std::vector<int> liveFront;
+    int2* d_liveFront = nullptr;
+    int* d_liveCtl = nullptr;
+    unsigned long long* d_liveKeys = nullptr;
+    int liveNb = 0;
     cudaGraphExec_t graph = nullptr;
     bool graph_trace = false;
     uint64_t graph_gen = 0;
@@ -192,6 +219,8 @@ struct Handle {
     int use_graph = 1;
     int subtree = 1;
     int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
+    int live = 1;    // live-list top levels (BRGPU_OPT_LIVE)
+    int liveVeto = 0;  // order n whose last live-tier solve fell back (dense plans for it)
     int strace = 0;  // secular-problem trace (brgpu_set_secular_trace): grid tier, dump per level
     double* strBuf = nullptr;  // per level 2n doubles (d, z) + rho per merge
     int64_t strCap = 0;
@@ -432,7 +461,7 @@ void plan_fused_runs(Plan* p) {
 // subtree; smaller blocks go to ranks in contiguous chunks of the total size.
 std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
                                 const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0,
-                                int sms = 148, bool sparse = false) {
+                                int sms = 148, bool sparse = false, bool live = false) {
     auto p = std::make_unique<Plan>();
     p->n = n;
     p->sms = sms;
@@ -497,6 +526,34 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
     add_levels(p.get(), mine, fuse, p->levels);
     add_levels(p.get(), top, fuse, p->levels2);
     plan_fused_runs(p.get());
+    // live-list tier: the top run of non-fused levels whose merges are all >= kLiveMinSize
+    p->liveWanted = live;
+    if (live && nranks == 1 && nblk == 1 && segs.size() == 2 && n >= kLiveMinN) {
+        size_t li = p->levels.size();
+        while (li > 0 && !p->levels[li - 1].fused && p->levels[li - 1].minSize >= kLiveMinSize) --li;
+        if (li < p->levels.size()) {
+            p->liveLev = (int)li;
+            std::set<std::pair<int, int>> liveM;
+            for (size_t l = li; l < p->levels.size(); ++l) {
+                LevelHost& lh = p->levels[l];
+                lh.live = true;
+                for (int q = 0; q < lh.M; ++q) liveM.emplace(p->mOff[(size_t)(lh.m0 + q)], p->mSize[(size_t)(lh.m0 + q)]);
+            }
+            std::vector<std::pair<int, int>> front;
+            for (size_t l = li; l < p->levels.size(); ++l) {
+                const LevelHost& lh = p->levels[l];
+                for (int q = 0; q < lh.M; ++q) {
+                    const int o = p->mOff[(size_t)(lh.m0 + q)], sz = p->mSize[(size_t)(lh.m0 + q)];
+                    const int nl = p->mNL[(size_t)(lh.m0 + q)];
+                    if (!liveM.count({o, nl})) front.emplace_back(o, nl);
+                    if (!liveM.count({o + nl, sz - nl})) front.emplace_back(o + nl, sz - nl);
+                }
+            }
+            std::sort(front.begin(), front.end());
+            for (auto& f : front) { p->liveFront.push_back(f.first); p->liveFront.push_back(f.second); }
+            p->liveNb = live_buckets(n);
+        }
+    }
     // control words per level; phase-1 grid levels may run the sparse pipeline
     // (sparse.cu); the shared top merges of a multi-rank plan stay dense (their
     // roots are split across ranks by the dense kernels)
@@ -505,7 +562,7 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
         for (LevelHost& lh : p->levels) {
             lh.ctl = 4 * ci++;
             // k_sp_place bounds its merge segments per tile by the smallest merge
-            lh.sp = sparse && !lh.fused && lh.minSize >= sparse_min_merge() ? 1 : 0;
+            lh.sp = sparse && !lh.fused && !lh.live && lh.minSize >= sparse_min_merge() ? 1 : 0;
             lh.spCap = sparse_cap();
             lh.spSpan = 2 * sparse_cap() - lh.spCap;
             lh.spStatic = lh.sp && lh.maxSize <= lh.spCap ? 1 : 0;
@@ -579,6 +636,9 @@ int upload_plan(Handle* h, Plan* p) {
     const size_t oSpGroup = put(std::vector<int>(anySp ? (size_t)ngMax + 1 : 0, 0));
     const size_t oBlk = put(std::vector<int>(anySp ? (size_t)sparse_flag_grid(p->n, p->sms) : 0, 0));
     const size_t oTiles = put(std::vector<int>(anySp ? 2 * (size_t)(p->n / 1024 + 2) : 0, 0));
+    const size_t oFront = put(p->liveFront);  // int2 pairs
+    const size_t oLiveCtl = put(std::vector<int>(p->liveLev >= 0 ? 4 : 0, 0));
+    const size_t oLiveKeys = put(std::vector<int>(p->liveLev >= 0 ? 4 : 0, 0));  // 2 u64 (16-byte aligned offsets)
     if (anySp) CUDA_TRY(h, cudaMallocHost(&p->h_ctl, sizeof(int) * (size_t)p->nctl));
     p->devInts = buf.size();
     CUDA_TRY(h, cudaMalloc(&p->dev, sizeof(int) * std::max<size_t>(buf.size(), 1)));
@@ -595,6 +655,9 @@ int upload_plan(Handle* h, Plan* p) {
     p->d_spGroup = p->dev + oSpGroup;
     p->d_blockCnt = p->dev + oBlk;
     p->d_spTiles = p->dev + oTiles;
+    p->d_liveFront = reinterpret_cast<int2*>(p->dev + oFront);
+    p->d_liveCtl = p->dev + oLiveCtl;
+    p->d_liveKeys = reinterpret_cast<unsigned long long*>(p->dev + oLiveKeys);
     return BRGPU_OK;
 }
 
@@ -780,6 +843,25 @@ void set_split(Handle* h, const SplitCfg* sc, SolveParams& prm) {
 
 int exchange_allgather(Handle* h, const SplitCfg& sc, int arrays);
 
+// live-list tier state (live.cu) in arrays the dense tiers no longer use above
+// the frontier: counts in nnPre, dead maxima in D / Z / R0, the pool in R1, the
+// sort's scatter buffer in dA and its bucket tables in nnPos / survPre
+LiveDev live_dev(Handle* h, Plan* p) {
+    LiveDev V{};
+    V.cnt = h->w.nnPre;
+    V.dLam = h->w.D;
+    V.dBlo = h->w.Z;
+    V.dBhi = h->w.R0;
+    V.pool = h->w.R1;
+    V.tmp = h->w.dA;
+    V.bcount = h->w.nnPos;
+    V.bcur = h->w.survPre;
+    V.ctl = p->d_liveCtl;
+    V.keys = p->d_liveKeys;
+    V.nb = p->liveNb;
+    return V;
+}
+
 void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* launches, Prof* prof,
                 const SplitCfg* sc = nullptr) {
     cudaStream_t s = h->stream;
@@ -811,6 +893,16 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
             continue;
         }
         const LevelDev L = level_dev(h, p, lh, prev);
+        if (lh.live) {
+            const LiveDev V = live_dev(h, p);
+            set_split(h, nullptr, prm);
+            if ((int)li == p->liveLev)
+                launch_live_init(s, h->w, V, p->d_liveFront, (int)p->liveFront.size() / 2, prm.tol_scale,
+                                 launches, prof);
+            launch_level_live(s, h->w, L, V, prm, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
+            if (li + 1 == levels.size()) launch_live_sort(s, V, n, h->w.lam, h->sms, launches, prof);
+            continue;
+        }
         if (lh.fused) {
             set_split(h, nullptr, prm);
             launch_level_fused(s, h->w, L, lh.G, lh.cap, p->d_gFirst + lh.g0, p->d_gCount + lh.g0, prm,
@@ -847,6 +939,7 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     const int n = p->n;
     const int nblk = (int)p->bstart.size() - 1;
     if (p->anySp) cudaMemsetAsync(p->d_ctl, 0, sizeof(int) * (size_t)p->nctl, s);  // level words (barrier counters)
+    if (p->liveLev >= 0) cudaMemsetAsync(p->d_liveCtl, 0, sizeof(int) * 8, s);   // live words + key words
     launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
                    p->d_cut, launches, prof);
     launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,
@@ -1125,11 +1218,12 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     if (h->virt > 1) return solve_virtual(h, n, bstart, segs);
     Plan* p = h->plan.get();
     const bool sig = h->sig != nullptr;
+    const bool wantLive = !sig && h->live != 0 && !h->strace && h->subtree != 0 && h->liveVeto != n;
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs ||
-        p->sigma != sig) {
+        p->sigma != sig || p->liveWanted != wantLive) {
         if (h->plan) free_plan(h->plan.get());
         h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0 && !h->strace, h->nranks,
-                            h->rank, h->sms, !sig && h->sparse != 0 && !h->strace);
+                            h->rank, h->sms, !sig && h->sparse != 0 && !h->strace, wantLive);
         p = h->plan.get();
         if (sig) {  // every merge propagates the requested rows: no root-only mode
             p->sigma = true;
@@ -1243,9 +1337,16 @@ void adapt_sparse(Handle* h, Plan* p) {
 int finish_solve(Handle* h) {
     cudaStream_t s = h->stream;
     ledger_peak(h);
+    Plan* lp = h->virt <= 1 && h->plan && h->plan->liveLev >= 0 ? h->plan.get() : nullptr;
+    h->hsmall[2] = 0;
     CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (lp) CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 2, lp->d_liveCtl + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
+    if (lp && h->hsmall[2]) {  // the live tier could not prove this solve exact: redo it densely
+        h->liveVeto = lp->n;
+        return kRetryDense;
+    }
     if (h->virt <= 1) adapt_sparse(h, h->plan.get());
     {
         // both pairs are recorded on every path; a failure here must not leave a
@@ -1328,7 +1429,11 @@ int solve_device(Handle* h, int64_t n64, const double* d, const double* e, doubl
         CUDA_TRY(h, cudaMemcpyAsync(w_out, h->w.lam, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     else if (w_out != h->w.lam)
         CUDA_TRY(h, cudaMemcpyAsync(w_out, h->w.lam, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    return finish_solve(h);
+    r = finish_solve(h);
+    // the live tier fell back (liveVeto = n: the next plan is dense); inputs
+    // staged in the workspace (brgpu_eigvals) are re-staged by the caller
+    if (r == kRetryDense && d != h->w.D && e != h->w.Z) return solve_device(h, n64, d, e, w_out, w_host);
+    return r;
 }
 
 }  // namespace
@@ -1387,6 +1492,7 @@ int brgpu_create(brgpu_handle** out, int device) {
     brgpu::init_fused_attributes();
     brgpu::init_sparse_attributes();
     brgpu::init_warp_attributes();
+    brgpu::init_live_attributes();
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     h->sec_grid = h->sms * brgpu::sec_ctas_per_sm();
     *out = hh;
@@ -1456,6 +1562,7 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
             return BRGPU_OK;
         case BRGPU_OPT_ROOT_SPLIT: set_plan_opt(h, h->root_split, v != 0); return BRGPU_OK;
         case BRGPU_OPT_SPARSE: set_plan_opt(h, h->sparse, v != 0); return BRGPU_OK;
+        case BRGPU_OPT_LIVE: set_plan_opt(h, h->live, v != 0); h->liveVeto = 0; return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -1478,6 +1585,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_ROOT_SPLIT: *v = h->root_split; return BRGPU_OK;
         case BRGPU_OPT_EXACT_PASSES: *v = h->exact; return BRGPU_OK;
         case BRGPU_OPT_SPARSE: *v = h->sparse; return BRGPU_OK;
+        case BRGPU_OPT_LIVE: *v = h->live; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }
 }
@@ -1521,9 +1629,14 @@ int brgpu_eigvals(brgpu_handle* hh, int64_t n, const double* d, const double* e,
     // host buffers are staged in workspace arrays that are dead until the first
     // merge (D, Z), so the host path needs no memory beyond the 15N arena
     cudaStream_t s = h->stream;
-    CUDA_TRY(h, cudaMemcpyAsync(h->w.D, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-    if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->w.Z, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, s));
-    return solve_device(h, n, h->w.D, h->w.Z, w, true);
+    int r = BRGPU_OK;
+    for (int attempt = 0; attempt < 2; ++attempt) {  // a live-tier fallback re-stages the input
+        CUDA_TRY(h, cudaMemcpyAsync(h->w.D, d, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        if (n > 1) CUDA_TRY(h, cudaMemcpyAsync(h->w.Z, e, sizeof(double) * (n - 1), cudaMemcpyHostToDevice, s));
+        r = solve_device(h, n, h->w.D, h->w.Z, w, true);
+        if (r != kRetryDense) break;
+    }
+    return r;
 }
 
 int brgpu_eigvals_device(brgpu_handle* hh, int64_t n, const double* d, const double* e, double* w,
@@ -1765,7 +1878,8 @@ const char* brgpu_kernel_class_name(int c) {
     static const char* names[BRGPU_NCLASS] = {
         "prepare(scale+cuts)", "leaf", "merge_tol", "merge_scatter", "nn_flag", "scan_tiles",
         "nn_write", "segment_walk", "surv_count", "surv_write", "secular", "zhat", "rows",
-        "deflated_out", "trace", "finish", "fused_level", "sparse_flag", "sparse_solve", "sparse_place"};
+        "deflated_out", "trace", "finish", "fused_level", "sparse_flag", "sparse_solve", "sparse_place",
+        "live_level", "live_sort"};
     return (c >= 0 && c < BRGPU_NCLASS) ? names[c] : "?";
 }
 

@@ -102,6 +102,25 @@ struct SigmaDev {
     double* Z0;      // merged z before the close-pole walk (stride doubles)
 };
 
+// Live-list tier (live.cu): the top levels of a large single-block solve keep,
+// per node, only the elements with a boundary-row entry above the deflation
+// threshold ("live"), sorted, at the start of the node's position range; the
+// other ("dead") eigenvalues go to a pool, summarised per node by three maxima.
+// Per-node words are indexed by the node's first position.
+struct LiveDev {
+    int* cnt;        // live count per node
+    double* dLam;    // max |lambda| of the node's dead elements
+    double* dBlo;    // max |first row| of the node's dead elements
+    double* dBhi;    // max |last row| of the node's dead elements
+    double* pool;    // dead eigenvalues, then the root's list (n values, any order)
+    double* tmp;     // bucket-sort scatter buffer (n)
+    int* bcount;     // bucket counts (nb), bucket starts (nb + 1)
+    int* bcur;       // bucket cursors (nb)
+    int* ctl;        // [0] pool fill, [1] fallback (redo the solve on the dense tiers)
+    unsigned long long* keys;  // [0] ~min key, [1] max key of the pool (order-preserving)
+    int nb;          // buckets of the final sort
+};
+
 // A run of consecutive fused levels launched as one kernel (k_levels_fused).
 constexpr int kMaxFusedRun = 8;
 struct FusedRun {

@@ -1,0 +1,804 @@
+// live.cu -- live-list tier for the top levels of a large single-block solve.
+//
+// Above the bottom levels of a deflation-heavy input (random n = 2^20: every
+// merge from size 256 up keeps K ~ 100 active poles of its 256 .. 2^20
+// elements), almost every element is a pole whose two boundary-row entries are
+// below the deflation tolerance of every later merge: it deflates by small z
+// (deflate.cpp:31-41) at every level up to the root and its eigenvalue never
+// changes.  The dense grid tier still moves every element through ~15 launches
+// per level.  This tier keeps, per node, only the LIVE elements (a boundary-row
+// entry above theta = tol/2 of the merge that produced them), in the node's
+// order, at the start of the node's position range; the eigenvalues of the
+// other (dead) elements go to a pool, and three maxima per node summarise them
+// (|lambda|, |first row|, |last row|):
+//  * a merge's tolerance 8u max(|D|, |z|) (deflate.cpp:55-60) is order-free:
+//    the live elements' terms plus the children's dead maxima (|lambda| of
+//    both, the left child's last row, the right child's first row) -- the dense
+//    value exactly;
+//  * the dead elements are small-z deflations iff the left child's dead
+//    last-row maximum and the right child's dead first-row maximum are <= tol.
+//    Checked per merge; when it fails (or a merge's live lists exceed shared
+//    memory, or a bucket of the final sort overflows) the fallback word is set
+//    and api.cpp redoes the solve on the dense tiers;
+//  * the non-negligible elements, their merged order (the dense merge restricted
+//    to the live elements is the stable merge of the live lists), the close-pole
+//    walk, the secular problem, refreshed weights and boundary rows are then
+//    those of the dense tiers -- same operations in the same order, so every
+//    root, weight and row is bit-identical -- and the parent's live list is the
+//    restriction of the parent's order (deflated first on ties);
+//  * merges larger than kSplitMinSize use the 32-way split arithmetic of the
+//    warp tier (root_warp, lane-strided products / sums + xor butterflies).
+// At the root the live list joins the pool (n values), which a bucket sort
+// (value buckets, rank sort per bucket in shared memory) puts in order.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.hpp"
+#include "launch.cuh"
+#include "numerics.cuh"
+#include "grid_common.cuh"
+
+namespace brgpu {
+
+constexpr int kLiveMax = 512;      // live elements of one merge (both children)
+constexpr int kLiveThreads = 256;
+constexpr int kLiveInitThreads = 256;
+constexpr int kBucketCap = 4096;   // elements of one final-sort bucket (shared memory)
+constexpr int kBucketThreads = 256;
+
+struct LiveSmem {
+    double D[kLiveMax];
+    double Z[kLiveMax];
+    double R0[kLiveMax];
+    double R1[kLiveMax];
+    double in[3 * kLiveMax];   // inputs (lam, blo, bhi); then active (d, z^2) pairs + z / z-hat
+    double r0A[kLiveMax];
+    double r1A[kLiveMax];
+    double tau[kLiveMax];
+    double oLam[kLiveMax];     // parent outputs at their live-order positions
+    double oR0[kLiveMax];
+    double oR1[kLiveMax];
+    int org[kLiveMax];
+    int nnPre[kLiveMax + 1];
+    int nnPos[kLiveMax];
+    int survPre[kLiveMax + 1];
+    unsigned char flag[kLiveMax];
+    unsigned char surv[kLiveMax];
+    int scan[kLiveThreads / 32];
+    unsigned long long tolb;
+    unsigned long long dmx[3];  // demoted maxima bits: |lambda|, |first row|, |last row|
+    double dead[6];             // children's dead maxima: L (lam, blo, bhi), R (lam, blo, bhi)
+    int cntL, cntR, next, bail;
+    unsigned long long evals, terms;
+};
+
+__device__ __forceinline__ unsigned long long dbits(double v) {
+    return (unsigned long long)__double_as_longlong(v);
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+__device__ __forceinline__ void live_fail(const LiveDev& V) { atomicExch(&V.ctl[1], 1); }
+
+// warp-aggregated append of v to the pool
+__device__ __forceinline__ void pool_push(const LiveDev& V, bool push, double v) {
+    const unsigned m = __ballot_sync(0xffffffffu, push);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&V.ctl[0], __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (push) V.pool[base + __popc(m & ((1u << lane) - 1u))] = v;
+}
+
+template <int BLOCK>
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double r = red[0];
+#pragma unroll
+    for (int q = 1; q < BLOCK / 32; ++q) r = fmax(r, red[q]);
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Entry of the tier: every frontier node (a child of a live merge computed by
+// the dense tiers) keeps its live elements, in order, at the start of its range.
+// theta = half the smallest tolerance a later merge can have on the node's own
+// |lambda| scale; the per-merge check makes the choice a performance matter only.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev V, const int2* __restrict__ front,
+                                                                double tol_scale) {
+    pdl_entry();
+    __shared__ double s_red[kLiveInitThreads / 32];
+    // the final sort's bucket counts are zeroed here (the dense levels used the array)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * V.nb + 2; i += gridDim.x * blockDim.x)
+        V.bcount[i] = 0;
+    const int2 f = front[blockIdx.x];
+    const int off = f.x, size = f.y;
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < size; i += kLiveInitThreads) mx = fmax(mx, fabs(w.lam[off + i]));
+    mx = block_max<kLiveInitThreads>(mx, s_red);
+    const double theta = 0.5 * (8.0 * kU * mx * tol_scale);
+    double dl = 0.0, d0 = 0.0, d1 = 0.0;
+    int out = 0;
+    for (int c0 = 0; c0 < size; c0 += kLiveInitThreads) {
+        const int i = c0 + threadIdx.x;
+        const bool valid = i < size;
+        double v = 0.0, b0 = 0.0, b1 = 0.0;
+        if (valid) {
+            v = w.lam[off + i];
+            b0 = w.blo[off + i];
+            b1 = w.bhi[off + i];
+        }
+        const bool live = valid && fmax(fabs(b0), fabs(b1)) > theta;
+        const bool dead = valid && !live;
+        pool_push(V, dead, v);
+        if (dead) {
+            dl = fmax(dl, fabs(v));
+            d0 = fmax(d0, fabs(b0));
+            d1 = fmax(d1, fabs(b1));
+        }
+        int tot;
+        const int ex = block_exclusive_scan<kLiveInitThreads>(live ? 1 : 0, tot);  // all loads of the chunk are done
+        if (live) {
+            const int p = off + out + ex;
+            w.lam[p] = v;
+            w.blo[p] = b0;
+            w.bhi[p] = b1;
+        }
+        out += tot;
+    }
+    dl = block_max<kLiveInitThreads>(dl, s_red);
+    d0 = block_max<kLiveInitThreads>(d0, s_red);
+    d1 = block_max<kLiveInitThreads>(d1, s_red);
+    if (threadIdx.x == 0) {
+        V.cnt[off] = out;
+        V.dLam[off] = dl;
+        V.dBlo[off] = d0;
+        V.dBhi[off] = d1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One merge of a live level per CTA (the fused tier's shared-memory pipeline on
+// the children's live lists; fused.cu holds the commented dense original).
+// ---------------------------------------------------------------------------
+template <bool SPLIT>
+__device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, const LiveDev& V, const int m,
+                                           const SolveParams& prm, int* __restrict__ traceOut, LiveSmem& S) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int base = L.mOff[m], nlFull = L.mNL[m];
+    const bool isRoot = (L.mFlags[m] & kMergeRoot) != 0;
+    if (tid == 0) {
+        const int cl = V.cnt[base], cr = V.cnt[base + nlFull];
+        S.cntL = cl;
+        S.cntR = cr;
+        S.dead[0] = V.dLam[base];
+        S.dead[1] = V.dBlo[base];
+        S.dead[2] = V.dBhi[base];
+        S.dead[3] = V.dLam[base + nlFull];
+        S.dead[4] = V.dBlo[base + nlFull];
+        S.dead[5] = V.dBhi[base + nlFull];
+        // tolerance terms of the dead elements: |lambda| of both children, |z| =
+        // the left child's last row, the right child's first row
+        S.tolb = dbits(fmax(fmax(S.dead[0], S.dead[3]), fmax(S.dead[2], S.dead[4])));
+        S.dmx[0] = S.dmx[1] = S.dmx[2] = 0ULL;
+        S.next = 0;
+        S.evals = 0;
+        S.terms = 0;
+        S.bail = *(volatile int*)&V.ctl[1] != 0 || cl + cr > kLiveMax;
+        if (cl + cr > kLiveMax) live_fail(V);
+    }
+    __syncthreads();
+    if (S.bail) return;
+    const int nl = S.cntL, E = S.cntL + S.cntR;
+    const double em = w.ew[base + nlFull - 1];
+    const double rho = fabs(em);
+    const bool neg = em < 0;
+    double* lamIn = S.in;
+    double* bloIn = S.in + kLiveMax;
+    double* bhiIn = S.in + 2 * kLiveMax;
+    for (int i = tid; i < E; i += kLiveThreads) {
+        const int src = i < nl ? base + i : base + nlFull + (i - nl);
+        lamIn[i] = w.lam[src];
+        bloIn[i] = w.blo[src];
+        bhiIn[i] = w.bhi[src];
+    }
+    __syncthreads();
+
+    // ---- tolerance: max(|D|, |z|) over the live and dead elements ------------
+    {
+        double v = 0.0;
+        for (int i = tid; i < E; i += kLiveThreads)
+            v = fmax(v, fmax(fabs(lamIn[i]), fabs(i < nl ? bhiIn[i] : bloIn[i])));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0 && v > 0.0) atomicMax(&S.tolb, dbits(v));
+    }
+    __syncthreads();
+    const double tol = 8.0 * kU * bitsd(S.tolb) * prm.tol_scale;
+    if (!(S.dead[2] <= tol && S.dead[4] <= tol)) {  // a dead element would be non-negligible
+        if (tid == 0) live_fail(V);
+        return;
+    }
+
+    // ---- stable merge of the two sorted live lists + z -----------------------
+    for (int i = tid; i < E; i += kLiveThreads) {
+        const double v = lamIn[i];
+        int sp;
+        double z, r0, r1;
+        if (i < nl) {
+            sp = i + count_less(lamIn + nl, E - nl, v);
+            const double b = bhiIn[i];
+            z = neg ? -b : b;
+            r0 = bloIn[i];
+            r1 = 0.0;
+        } else {
+            sp = (i - nl) + count_leq(lamIn, nl, v);
+            z = bloIn[i];
+            r0 = 0.0;
+            r1 = bhiIn[i];
+        }
+        S.D[sp] = v;
+        S.Z[sp] = z;
+        S.R0[sp] = r0;
+        S.R1[sp] = r1;
+    }
+    __syncthreads();
+
+    // ---- small-z flags + NN compaction ---------------------------------------
+    for (int i = tid; i < E; i += kLiveThreads) S.flag[i] = fabs(S.Z[i]) > tol;
+    __syncthreads();
+    const int NN = cta_scan_flags<kLiveThreads>(S.flag, E, S.nnPre, S.scan);
+    for (int i = tid; i < E; i += kLiveThreads)
+        if (S.flag[i]) S.nnPos[S.nnPre[i]] = i;
+    __syncthreads();
+
+    // ---- close-pole deflation (k_segment_walk / fused.cu arithmetic) ---------
+    {
+        double* pQ = lamIn;
+        double* pS0 = bloIn;
+        double* pS1 = bhiIn;
+        for (int q = tid; q < NN; q += kLiveThreads) {
+            const int k = S.nnPos[q];
+            if (q > 0 && fabs(S.D[k] - S.D[S.nnPos[q - 1]]) <= tol) continue;  // not a head
+            S.surv[q] = 1;
+            int prev = k, nmem = 0;
+            double dp = S.D[k];
+            const double zs = S.Z[k];
+            double Q = zs * zs, S0 = zs * S.R0[k], S1 = zs * S.R1[k];
+            double dprev_nn = dp;
+            for (int q2 = q + 1; q2 < NN; ++q2) {
+                const int k2 = S.nnPos[q2];
+                const double d2 = S.D[k2];
+                if (fabs(d2 - dprev_nn) > tol) break;
+                dprev_nn = d2;
+                const double zq = S.Z[k2];
+                if (fabs(d2 - dp) <= tol) {
+                    pQ[k2] = Q;
+                    pS0[k2] = S0;
+                    pS1[k2] = S1;
+                    Q = Q + zq * zq;
+                    S0 = S0 + zq * S.R0[k2];
+                    S1 = S1 + zq * S.R1[k2];
+                    ++nmem;
+                    S.surv[q2] = 0;
+                } else {
+                    if (nmem) {
+                        const double R = sqrt(Q), iR = 1.0 / R;
+                        S.Z[prev] = R; S.R0[prev] = S0 * iR; S.R1[prev] = S1 * iR;
+                    }
+                    S.surv[q2] = 1;
+                    prev = k2; dp = d2; nmem = 0;
+                    Q = zq * zq; S0 = zq * S.R0[k2]; S1 = zq * S.R1[k2];
+                }
+            }
+            if (nmem) {
+                const double R = sqrt(Q), iR = 1.0 / R;
+                S.Z[prev] = R; S.R0[prev] = S0 * iR; S.R1[prev] = S1 * iR;
+            }
+        }
+        __syncthreads();
+        for (int q = tid; q < NN; q += kLiveThreads) {
+            if (S.surv[q]) continue;
+            const int k = S.nnPos[q];
+            double x0 = S.R0[k], x1 = S.R1[k];
+            group_member(pQ[k], pS0[k], pS1[k], S.Z[k], x0, x1);
+            S.R0[k] = x0;
+            S.R1[k] = x1;
+            S.Z[k] = 0.0;
+        }
+    }
+    __syncthreads();
+
+    // ---- survivor compaction: active (d, z^2) pairs, z, rows ------------------
+    const int T = cta_scan_flags<kLiveThreads>(S.surv, NN, S.survPre, S.scan);
+    double2* pairs = reinterpret_cast<double2*>(S.in);  // aliases lam/blo inputs (dead)
+    double* zA = S.in + 2 * kLiveMax;                    // aliases the bhi input (dead)
+    for (int q = tid; q < NN; q += kLiveThreads) {
+        if (!S.surv[q]) continue;
+        const int g = S.survPre[q], k = S.nnPos[q];
+        const double z = S.Z[k];
+        pairs[g] = make_double2(S.D[k], z * z);
+        zA[g] = z;
+        S.r0A[g] = S.R0[k];
+        S.r1A[g] = S.R1[k];
+    }
+    __syncthreads();
+
+    // ---- secular roots ---------------------------------------------------------
+    unsigned long long evals = 0, terms = 0;
+    if (SPLIT) {  // warp per root, split arithmetic (k_secular_warp's resident path)
+        for (int g = wid; g < T; g += kLiveThreads / 32) {
+            int o;
+            double tu;
+            root_warp(pairs, zA, T, g, rho, w.exact != 0, prm.patched != 0, w.status, o, tu, evals, terms);
+            if (lane == 0) {
+                S.org[g] = o;
+                S.tau[g] = tu;
+            }
+        }
+        if (lane) evals = terms = 0;  // every lane counted the warp's evaluations
+    } else {  // lane per root, CTA queue: the last root first, then the interior ones
+        double2* snap = reinterpret_cast<double2*>(S.Z) + tid;  // S.Z is dead after the compaction
+        RootSM st;
+        int g = -1;
+        bool exhausted = false;
+        for (;;) {
+            while (g < 0 && !exhausted) {
+                const int q = atomicAdd(&S.next, 1);
+                if (q >= T) { exhausted = true; break; }
+                g = q == 0 ? T - 1 : q - 1;
+                rs_begin(st, T, g, rho, PolesPairs{pairs}, zA[0], Z2Pairs{pairs});
+                if (st.phase == kRsDone) {
+                    S.org[g] = st.org;
+                    S.tau[g] = st.tau;
+                    g = -1;
+                }
+            }
+            if (!__any_sync(0xffffffffu, g >= 0)) break;
+            if (g >= 0) {
+                double sum, sum_abs, sum_d, psi;
+                bool pole = false;
+                const SmemPairs P{pairs};
+                if (!w.exact && eval_guard(P, st.K, st.j, st.dorg, st.tau))
+                    eval_fast(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi, snap);
+                else
+                    pole = eval_pass_exact(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi);
+                Ev ev;
+                ev.f = 1.0 + st.rho * sum;
+                ev.fp = st.rho * sum_d;
+                ev.abs_sum = st.rho * sum_abs;
+                ev.psi = st.rho * psi;
+                ev.pole = pole;
+                ++evals;
+                terms += (unsigned long long)st.K;
+                rs_consume(st, ev, PolesPairs{pairs}, Z2Pairs{pairs}, prm.patched != 0);
+                if (st.phase == kRsDone || st.phase == kRsFail) {
+                    if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                    S.org[g] = st.org;
+                    S.tau[g] = st.tau;
+                    g = -1;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        evals += __shfl_xor_sync(0xffffffffu, evals, o);
+        terms += __shfl_xor_sync(0xffffffffu, terms, o);
+    }
+    if (lane == 0 && evals) {
+        atomicAdd(&w.counters[0], evals);
+        atomicAdd(&w.counters[1], terms);
+    }
+    __syncthreads();
+
+    double* sDorg = S.Z;  // d[origin] per root (S.Z is dead after the compaction)
+    for (int g = tid; g < T; g += kLiveThreads) sDorg[g] = pairs[S.org[g]].x;
+    __syncthreads();
+
+    // ---- Gu-Eisenstat refreshed weights (non-root merges, K > 1) -------------
+    if (prm.zhat && !isRoot && T > 1) {
+        if (SPLIT) {  // warp per pole: lane-strided products + xor butterfly (k_zhat_warp)
+            for (int i = wid; i < T; i += kLiveThreads / 32) {
+                const double di = pairs[i].x;
+                double prod = 1.0;
+                if (!w.exact && zhat_guard(PolesPairs{pairs}, T, i)) {
+                    for (int j = lane; j < T; j += 32) {
+                        const double del = (di - sDorg[j]) - S.tau[j];
+                        prod = prod * (j == i ? del : del * rcp_nr(di - pairs[j].x));
+                    }
+                } else {
+                    for (int j = lane; j < T; j += 32) {
+                        const double del = (di - sDorg[j]) - S.tau[j];
+                        if (j == i) prod = prod * del;
+                        else prod = prod * (del * __drcp_rn(di - pairs[j].x));
+                    }
+                }
+                const double W = bfly_mul(prod);
+                if (lane == 0) {
+                    const double mag = sqrt(fmax(0.0, -W));
+                    zA[i] = zA[i] >= 0.0 ? mag : -mag;
+                }
+            }
+        } else {
+            for (int i = tid; i < T; i += kLiveThreads) {
+                const double di = pairs[i].x;
+                double prod = 1.0;
+                if (!w.exact && zhat_guard(PolesPairs{pairs}, T, i)) {
+#pragma unroll 4
+                    for (int j = 0; j < T; ++j) {
+                        const double del = (di - sDorg[j]) - S.tau[j];
+                        const double dd = di - pairs[j].x;
+                        const double f = (j == i) ? del : del * rcp_nr(dd);
+                        prod = prod * f;
+                    }
+                } else {
+                    for (int j = 0; j < T; ++j) {
+                        const double del = (di - pairs[S.org[j]].x) - S.tau[j];
+                        if (j == i) prod = prod * del;
+                        else prod = prod * (del * __drcp_rn(di - pairs[j].x));
+                    }
+                }
+                const double mag = sqrt(fmax(0.0, -prod));
+                zA[i] = zA[i] >= 0.0 ? mag : -mag;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- roots: position in the parent's live order + boundary rows ----------
+    auto root_pos = [&](int j, double lam) {
+        int lo = 0, hi = T;  // #{dA <= lam}
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (!(lam < pairs[mid].x)) lo = mid + 1; else hi = mid;
+        }
+        return j + count_leq(S.D, E, lam) - lo;
+    };
+    if (SPLIT && !isRoot) {  // warp per root: lane-strided sums + butterflies (k_rows_warp)
+        for (int j = wid; j < T; j += kLiveThreads / 32) {
+            const double dorg = sDorg[j], tau = S.tau[j];
+            const double lam = dorg + tau;
+            const int pos = root_pos(j, lam);
+            double nn = 0.0, s0 = 0.0, s1 = 0.0;
+            if (!w.exact && eval_guard(SmemPairs{pairs}, T, j, dorg, tau)) {
+                for (int i = lane; i < T; i += 32) {
+                    const double y = zA[i] * rcp_nr((pairs[i].x - dorg) - tau);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(S.r0A[i], y, s0);
+                    s1 = __fma_rn(S.r1A[i], y, s1);
+                }
+            } else {
+                bool zero = false;
+                for (int i = lane; i < T; i += 32) {
+                    const double del = (pairs[i].x - dorg) - tau;
+                    zero |= (del == 0.0);
+                    const double y = zA[i] * __drcp_rn(del);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(S.r0A[i], y, s0);
+                    s1 = __fma_rn(S.r1A[i], y, s1);
+                }
+                if (__any_sync(0xffffffffu, zero) && lane == 0) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+            }
+            const double NNs = bfly_add(nn), S0 = bfly_add(s0), S1 = bfly_add(s1);
+            if (lane == 0) {
+                const double inv = 1.0 / sqrt(NNs);
+                S.oLam[pos] = lam;
+                S.oR0[pos] = S0 * inv;
+                S.oR1[pos] = S1 * inv;
+            }
+        }
+    } else {
+        for (int j = tid; j < T; j += kLiveThreads) {
+            const double dorg = sDorg[j], tau = S.tau[j];
+            const double lam = dorg + tau;
+            const int pos = root_pos(j, lam);
+            S.oLam[pos] = lam;
+            if (isRoot) continue;
+            double nn = 0.0, s0 = 0.0, s1 = 0.0;
+            if (!w.exact && eval_guard(SmemPairs{pairs}, T, j, dorg, tau)) {
+#pragma unroll 4
+                for (int i = 0; i < T; ++i) {
+                    const double y = zA[i] * rcp_nr((pairs[i].x - dorg) - tau);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(S.r0A[i], y, s0);
+                    s1 = __fma_rn(S.r1A[i], y, s1);
+                }
+            } else {
+                bool zero = false;
+                for (int i = 0; i < T; ++i) {
+                    const double del = (pairs[i].x - dorg) - tau;
+                    zero |= (del == 0.0);
+                    const double y = zA[i] * __drcp_rn(del);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(S.r0A[i], y, s0);
+                    s1 = __fma_rn(S.r1A[i], y, s1);
+                }
+                if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+            }
+            const double inv = 1.0 / sqrt(nn);
+            S.oR0[pos] = s0 * inv;
+            S.oR1[pos] = s1 * inv;
+        }
+    }
+    // deflated live elements: t + #{roots < D}
+    for (int k = tid; k < E; k += kLiveThreads) {
+        const int q = S.nnPre[k];
+        if (S.flag[k] && S.surv[q]) continue;  // survivor: its column became a root
+        const int tt = k - S.survPre[q];
+        const double v = S.D[k];
+        int lo = 0, hi = T;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const double lj = sDorg[mid] + S.tau[mid];
+            if (lj < v) lo = mid + 1; else hi = mid;
+        }
+        S.oLam[tt + lo] = v;
+        S.oR0[tt + lo] = S.R0[k];
+        S.oR1[tt + lo] = S.R1[k];
+    }
+    __syncthreads();
+
+    // ---- parent's live list: demote outputs with both rows <= tol / 2 --------
+    if (isRoot) {  // the root's eigenvalues join the pool for the final sort
+        for (int c0 = 0; c0 < E; c0 += kLiveThreads) {
+            const int i = c0 + tid;
+            pool_push(V, i < E, i < E ? S.oLam[i] : 0.0);
+        }
+    } else {
+        const double theta = 0.5 * tol;
+        int out = 0;
+        double dl = 0.0, d0 = 0.0, d1 = 0.0;
+        for (int c0 = 0; c0 < E; c0 += kLiveThreads) {
+            const int i = c0 + tid;
+            const bool valid = i < E;
+            double v = 0.0, b0 = 0.0, b1 = 0.0;
+            if (valid) { v = S.oLam[i]; b0 = S.oR0[i]; b1 = S.oR1[i]; }
+            const bool live = valid && fmax(fabs(b0), fabs(b1)) > theta;
+            const bool dead = valid && !live;
+            pool_push(V, dead, v);
+            if (dead) {
+                dl = fmax(dl, fabs(v));
+                d0 = fmax(d0, fabs(b0));
+                d1 = fmax(d1, fabs(b1));
+            }
+            int tot;
+            const int ex = block_exclusive_scan<kLiveThreads>(live ? 1 : 0, tot);
+            if (live) {
+                const int p = base + out + ex;
+                w.lam[p] = v;
+                w.blo[p] = b0;
+                w.bhi[p] = b1;
+            }
+            out += tot;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            dl = fmax(dl, __shfl_xor_sync(0xffffffffu, dl, o));
+            d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+            d1 = fmax(d1, __shfl_xor_sync(0xffffffffu, d1, o));
+        }
+        if (lane == 0) {
+            if (dl > 0.0) atomicMax(&S.dmx[0], dbits(dl));
+            if (d0 > 0.0) atomicMax(&S.dmx[1], dbits(d0));
+            if (d1 > 0.0) atomicMax(&S.dmx[2], dbits(d1));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // parent rows of the children's dead elements: left (first row, 0), right (0, last row)
+            V.cnt[base] = out;
+            V.dLam[base] = fmax(fmax(S.dead[0], S.dead[3]), bitsd(S.dmx[0]));
+            V.dBlo[base] = fmax(S.dead[1], bitsd(S.dmx[1]));
+            V.dBhi[base] = fmax(S.dead[5], bitsd(S.dmx[2]));
+        }
+    }
+    if (traceOut && tid == 0) {
+        traceOut[2 * m] = NN;
+        traceOut[2 * m + 1] = T;
+    }
+}
+
+// MODE 0: lane arithmetic, 1: split arithmetic (every merge > kSplitMinSize),
+// 2: per merge (a level with merges on both sides of the rule)
+template <int MODE>
+__global__ void __launch_bounds__(kLiveThreads, 3)
+k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ traceOut) {
+    pdl_entry();
+    extern __shared__ __align__(16) unsigned char live_raw[];
+    LiveSmem& S = *reinterpret_cast<LiveSmem*>(live_raw);
+    const int m = blockIdx.x;
+    if (MODE == 2) {
+        if (L.mSize[m] > kSplitMinSize) live_merge<true>(w, L, V, m, prm, traceOut, S);
+        else live_merge<false>(w, L, V, m, prm, traceOut, S);
+    } else {
+        live_merge<MODE == 1>(w, L, V, m, prm, traceOut, S);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Final order: bucket sort of the pool (n values).  Buckets split the value
+// range uniformly (a monotone bucket function, so concatenated buckets are in
+// order); each bucket is rank-sorted in shared memory (ties by pool index:
+// equal doubles are interchangeable).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long okey(double v) {
+    const unsigned long long b = dbits(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double okey_val(unsigned long long k) {
+    return bitsd((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k);
+}
+struct Buckets {
+    double vmin, scale;
+    int nb;
+    __device__ __forceinline__ int operator()(double x) const {
+        if (!(scale > 0.0)) return 0;
+        const double t = (x - vmin) * scale;
+        return t >= (double)(nb - 1) ? nb - 1 : (int)t;
+    }
+};
+__device__ __forceinline__ Buckets buckets_of(const LiveDev& V) {
+    Buckets B;
+    B.nb = V.nb;
+    B.vmin = okey_val(~V.keys[0]);
+    const double vmax = okey_val(V.keys[1]);
+    B.scale = vmax > B.vmin ? (double)V.nb / (vmax - B.vmin) : 0.0;
+    if (!(B.scale < 1e300)) B.scale = 0.0;  // (vmax - vmin) underflow: one bucket
+    return B;
+}
+
+__global__ void k_live_bounds(LiveDev V, int n) {
+    pdl_entry();
+    if (V.ctl[1]) return;
+    unsigned long long lo = 0ULL, hi = 0ULL;  // lo holds ~min
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const unsigned long long k = okey(V.pool[i]);
+        lo = ~k > lo ? ~k : lo;
+        hi = k > hi ? k : hi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a > lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&V.keys[0], lo);
+        atomicMax(&V.keys[1], hi);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && V.ctl[0] != n) live_fail(V);  // every value reached the pool
+}
+
+constexpr int kHistShared = 8192;
+__global__ void k_live_hist(LiveDev V, int n) {
+    pdl_entry();
+    if (V.ctl[1]) return;
+    __shared__ int s_h[kHistShared];
+    const Buckets B = buckets_of(V);
+    const bool sh = B.nb <= kHistShared;
+    if (sh)
+        for (int b = threadIdx.x; b < B.nb; b += blockDim.x) s_h[b] = 0;
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int b = B(V.pool[i]);
+        if (sh) atomicAdd(&s_h[b], 1); else atomicAdd(&V.bcount[b], 1);
+    }
+    __syncthreads();
+    if (sh)
+        for (int b = threadIdx.x; b < B.nb; b += blockDim.x)
+            if (s_h[b]) atomicAdd(&V.bcount[b], s_h[b]);
+}
+
+// exclusive scan of the bucket counts (one CTA): starts in bcount[nb ..], cursors in bcur
+__global__ void __launch_bounds__(1024) k_live_scan(LiveDev V) {
+    pdl_entry();
+    if (V.ctl[1]) return;
+    __shared__ int s_wt[32];
+    const int nb = V.nb;
+    const int per = (nb + 1023) / 1024;
+    const int i0 = threadIdx.x * per;
+    int local = 0, big = 0;
+    for (int k = 0; k < per; ++k)
+        if (i0 + k < nb) {
+            const int c = V.bcount[i0 + k];
+            local += c;
+            big = max(big, c);
+        }
+    if (__syncthreads_or(big > kBucketCap)) {
+        if (threadIdx.x == 0) live_fail(V);
+        return;
+    }
+    int tot;
+    int run = cta_excl_scan<1024>(local, tot, s_wt);
+    for (int k = 0; k < per; ++k)
+        if (i0 + k < nb) {
+            V.bcount[nb + i0 + k] = run;
+            V.bcur[i0 + k] = run;
+            run += V.bcount[i0 + k];
+        }
+    if (threadIdx.x == 0) V.bcount[2 * nb] = tot;
+}
+
+__global__ void k_live_scatter(LiveDev V, int n) {
+    pdl_entry();
+    if (V.ctl[1]) return;
+    const Buckets B = buckets_of(V);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double x = V.pool[i];
+        V.tmp[atomicAdd(&V.bcur[B(x)], 1)] = x;
+    }
+}
+
+__global__ void __launch_bounds__(kBucketThreads) k_live_bucket(LiveDev V, double* __restrict__ out) {
+    pdl_entry();
+    if (V.ctl[1]) return;
+    __shared__ double s_v[kBucketCap];
+    const int b = blockIdx.x;
+    const int start = V.bcount[V.nb + b], cnt = V.bcount[b];
+    for (int i = threadIdx.x; i < cnt; i += kBucketThreads) s_v[i] = V.tmp[start + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += kBucketThreads) {
+        const double x = s_v[i];
+        int r = 0;
+        for (int j = 0; j < cnt; ++j) {
+            const double y = s_v[j];
+            r += (y < x) || (y == x && j < i);
+        }
+        out[start + r] = x;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+void launch_live_init(cudaStream_t s, const Work& w, const LiveDev& V, const int2* front, int nfront,
+                      double tol_scale, int* launches, Prof* prof) {
+    launch_pdl(k_live_init, nfront, kLiveInitThreads, 0, s, w, V, front, tol_scale);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
+}
+
+void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
+                       const SolveParams& prm, int* traceOut, int* launches, Prof* prof) {
+    if (L.allSplit)
+        launch_pdl(k_live_level<1>, L.M, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut);
+    else if (L.maxSize > kSplitMinSize)
+        launch_pdl(k_live_level<2>, L.M, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut);
+    else
+        launch_pdl(k_live_level<0>, L.M, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
+}
+
+void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int sms, int* launches, Prof* prof) {
+    const int g = sms * 4;
+    launch_pdl(k_live_bounds, g, 256, 0, s, V, n);
+    launch_pdl(k_live_hist, g, 256, 0, s, V, n);
+    launch_pdl(k_live_scan, 1, 1024, 0, s, V);
+    launch_pdl(k_live_scatter, g, 256, 0, s, V, n);
+    launch_pdl(k_live_bucket, V.nb, kBucketThreads, 0, s, V, out);
+    *launches += 5;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE_SORT);
+}
+
+int live_buckets(int n) { return n / 128 > 1 ? n / 128 : 1; }
+int live_max_elems() { return kLiveMax; }
+
+void init_live_attributes() {
+    cudaFuncSetAttribute(k_live_level<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
+    cudaFuncSetAttribute(k_live_level<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
+    cudaFuncSetAttribute(k_live_level<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
+}
+
+static_assert(sizeof(LiveSmem) <= 75 * 1024, "three live CTAs per SM");
+
+}  // namespace brgpu
