@@ -174,6 +174,22 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
                                            const SolveParams& prm, int* __restrict__ traceOut, LiveSmem& S) {
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
+#ifdef BRGPU_LIVE_PROF
+    // phase cycles of the few-merge (latency-bound) levels, summed over CTAs in
+    // counters[4..7]: deflation / secular / refreshed weights / rows + output
+    long long ph_t = clock64();
+#define LIVE_MARK(k)                                                                          \
+    do {                                                                                      \
+        __syncthreads();                                                                      \
+        if (tid == 0 && gridDim.x <= 64) {                                                    \
+            const long long t_ = clock64();                                                   \
+            atomicAdd(&w.counters[4 + (k)], (unsigned long long)(t_ - ph_t));                 \
+            ph_t = t_;                                                                        \
+        }                                                                                     \
+    } while (0)
+#else
+#define LIVE_MARK(k) do {} while (0)
+#endif
     const int base = L.mOff[m], nlFull = L.mNL[m];
     const bool isRoot = (L.mFlags[m] & kMergeRoot) != 0;
     if (tid == 0) {
@@ -333,6 +349,7 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
     }
     __syncthreads();
 
+    LIVE_MARK(0);
     // ---- secular roots ---------------------------------------------------------
     unsigned long long evals = 0, terms = 0;
     if (SPLIT) {  // warp per root, split arithmetic (k_secular_warp's resident path)
@@ -405,6 +422,7 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
     for (int g = tid; g < T; g += kLiveThreads) sDorg[g] = pairs[S.org[g]].x;
     __syncthreads();
 
+    LIVE_MARK(1);
     // ---- Gu-Eisenstat refreshed weights (non-root merges, K > 1) -------------
     if (prm.zhat && !isRoot && T > 1) {
         if (SPLIT) {  // warp per pole: lane-strided products + xor butterfly (k_zhat_warp)
@@ -455,6 +473,7 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
         __syncthreads();
     }
 
+    LIVE_MARK(2);
     // ---- roots: position in the parent's live order + boundary rows ----------
     auto root_pos = [&](int j, double lam) {
         int lo = 0, hi = T;  // #{dA <= lam}
@@ -601,6 +620,8 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
             V.dBhi[base] = fmax(S.dead[5], bitsd(S.dmx[2]));
         }
     }
+    LIVE_MARK(3);
+#undef LIVE_MARK
     if (traceOut && tid == 0) {
         traceOut[2 * m] = NN;
         traceOut[2 * m + 1] = T;
