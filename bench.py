@@ -421,7 +421,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
         peak = fp64_peak(dev)
         pk = peak["lane_ops_per_s"] / 1e12
         # FP64 work per kernel class: algorithmic lane-ops from the live unit counts
-        grid_terms = stats["pole_terms"] - stats["pole_terms_fused"]
+        live_terms = stats.get("pole_terms_live", 0.0)
+        grid_terms = stats["pole_terms"] - stats["pole_terms_fused"] - live_terms
 
         def work(ops):
             return {
@@ -430,6 +431,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
                 "rows": ops["rows"] * stats["k2_nonroot_grid"],
                 "fused_level": (ops["secular"] * stats["pole_terms_fused"]
                                 + (ops["zhat"] + ops["rows"]) * stats["k2_nonroot_fused"]),
+                "live_level": (ops["secular"] * live_terms
+                               + (ops["zhat"] + ops["rows"]) * stats.get("k2_nonroot_live", 0.0)),
             }
         wc, ws = work(OPS_CONTRACT), work(OPS_SASS)
         fp64 = {}
@@ -456,7 +459,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
                         "peak_source": "measured DFMA probe (libbrprobe.so), burst; MEASURED_PEAKS.json "
                                        "has no FP64 entry",
                         "work_note": "SURVEY.md §8(d) counts: 13 per secular pole term, 10 per z-hat "
-                                     "term, 11 per row term; fused_level = all three of the SMEM levels"}
+                                     "term, 11 per row term; fused_level / live_level = all three of those "
+                                     "shared-memory levels"}
             else:
                 hb, _ = hbm_peak()
                 byts = BYTES_PER_ELEM.get(dom, 0) * N * dom_launch
@@ -508,7 +512,8 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int) -> None:
             "kernel_profile_ms": {k: round(v[0], 4) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])},
             "work": {k: stats[k] for k in ("sum_k", "sum_k2", "max_k", "pole_terms", "pole_terms_fused", "evals",
                                            "merges", "height", "k2_nonroot_fused", "k2_nonroot_grid",
-                                           "nn_grid", "k_grid")},
+                                           "nn_grid", "k_grid", "evals_live", "pole_terms_live",
+                                           "k2_nonroot_live") if k in stats},
             "fp64_peak_probe": peak,
             "sorted_output": ok,
             "ledger": vars(s.ledger()),

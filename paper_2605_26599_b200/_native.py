@@ -34,7 +34,8 @@ class Stats(C.Structure):
                 ("max_k", C.c_int64), ("kernel_launches", C.c_int32), ("graph_replayed", C.c_int32),
                 ("evals_fused", C.c_int64), ("pole_terms_fused", C.c_double),
                 ("k2_nonroot_fused", C.c_double), ("k2_nonroot_grid", C.c_double),
-                ("nn_grid", C.c_int64), ("k_grid", C.c_int64)]
+                ("nn_grid", C.c_int64), ("k_grid", C.c_int64),
+                ("evals_live", C.c_int64), ("pole_terms_live", C.c_double), ("k2_nonroot_live", C.c_double)]
 
 
 class Ledger(C.Structure):

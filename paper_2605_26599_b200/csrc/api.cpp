@@ -81,6 +81,9 @@ void init_live_attributes();
 constexpr int kLiveMinSize = BRGPU_LIVE_MIN_SIZE;
 constexpr int kLiveMinN = 1 << 15;
 constexpr int kRetryDense = 1000;  // internal: the live tier fell back, redo the solve densely
+// work counters (Work::counters): [0,1] grid-tier evaluations / pole terms, [2,3]
+// fused tier, [4..7] phase cycles of profiling builds, [8,9] live tier
+constexpr int kCounters = 12;
 #ifndef BRGPU_FUSE_MAX_ELEMS
 #define BRGPU_FUSE_MAX_ELEMS 1024
 #endif
@@ -716,13 +719,13 @@ int ensure_work(Handle* h, int64_t n) {
         w.levelModes = ib + 5 * c + 2 + 2 * ntiles + 1;
     }
     uint8_t* bb = nullptr;
-    CUDA_TRY(h, cudaMalloc(&bb, 3 * c + 64));
+    CUDA_TRY(h, cudaMalloc(&bb, 3 * c + 128));
     w.nnFlag = bb; w.survFlag = bb + c; h->split = bb + 2 * c;
     w.counters = reinterpret_cast<unsigned long long*>(bb + 3 * c);  // 8-byte aligned (c%8==0? pad)
     h->cap = c;
     ++h->bufgen;
     h->ledger_doubles = nd;
-    h->ledger_ints = ni + (3 * c + 64 + 3) / 4;
+    h->ledger_ints = ni + (3 * c + 128 + 3) / 4;
     h->peak_doubles = std::max(h->peak_doubles, h->ledger_doubles);
     h->peak_ints = std::max(h->peak_ints, h->ledger_ints);
     h->limit_n = c;
@@ -1256,7 +1259,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     }
     if (int r = ensure_buf_sizes(h, p)) return r;
     CUDA_TRY(h, cudaMemsetAsync(h->sbits, 0, sizeof(unsigned long long) * bstart.size(), s));
-    CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * 8, s));
+    CUDA_TRY(h, cudaMemsetAsync(h->w.counters, 0, sizeof(unsigned long long) * kCounters, s));
     int launches = 0;
     const bool want_graph = h->use_graph != 0 && h->prof == nullptr && !sig;
     CUDA_TRY(h, cudaEventRecord(h->tev[2], s));
@@ -1341,7 +1344,7 @@ int finish_solve(Handle* h) {
     h->hsmall[2] = 0;
     CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 1, h->w.status, sizeof(int), cudaMemcpyDeviceToHost, s));
     if (lp) CUDA_TRY(h, cudaMemcpyAsync(h->hsmall + 2, lp->d_liveCtl + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * kCounters, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
     if (lp && h->hsmall[2]) {  // the live tier could not prove this solve exact: redo it densely
         h->liveVeto = lp->n;
@@ -1367,8 +1370,10 @@ int finish_solve(Handle* h) {
         h->timing.exchange_ms = x;
         h->timing.phase2_ms = p2;
     }
-    h->stats.evals = (int64_t)(h->hcnt[0] + h->hcnt[2]);
-    h->stats.pole_terms = (double)(h->hcnt[1] + h->hcnt[3]);
+    h->stats.evals = (int64_t)(h->hcnt[0] + h->hcnt[2] + h->hcnt[8]);
+    h->stats.pole_terms = (double)(h->hcnt[1] + h->hcnt[3] + h->hcnt[9]);
+    h->stats.evals_live = (int64_t)h->hcnt[8];
+    h->stats.pole_terms_live = (double)h->hcnt[9];
     h->stats.evals_fused = (int64_t)h->hcnt[2];
     h->stats.pole_terms_fused = (double)h->hcnt[3];
     if (h->trace && h->plan) {
@@ -1377,12 +1382,12 @@ int finish_solve(Handle* h) {
         std::vector<int> tb(2 * M);
         if (M) CUDA_TRY(h, cudaMemcpy(tb.data(), h->traceBuf, sizeof(int) * 2 * M, cudaMemcpyDeviceToHost));
         h->traceRecs.resize(M);
-        double sk2 = 0, szt = 0, k2f = 0, k2g = 0;
+        double sk2 = 0, szt = 0, k2f = 0, k2g = 0, k2l = 0;
         int64_t sk = 0, snn = 0, mk = 0, nng = 0, kg = 0;
-        std::vector<char> fusedMerge(M, 0);
+        std::vector<char> fusedMerge(M, 0);  // 1 fused tier, 2 live tier
         for (const auto* lv : {&p->levels, &p->levels2})
             for (const LevelHost& lh : *lv)
-                for (int q = 0; q < lh.M; ++q) fusedMerge[(size_t)(lh.m0 + q)] = lh.fused;
+                for (int q = 0; q < lh.M; ++q) fusedMerge[(size_t)(lh.m0 + q)] = lh.fused ? 1 : lh.live ? 2 : 0;
         for (size_t m = 0; m < M; ++m) {
             brgpu_trace& t = h->traceRecs[m];
             t.level = p->mLevel[m];
@@ -1395,7 +1400,7 @@ int finish_solve(Handle* h) {
             if (!fusedMerge[m]) { nng += t.nn; kg += t.k; }
             if (!t.is_root) {
                 szt += (double)t.k * (double)t.k;
-                (fusedMerge[m] ? k2f : k2g) += (double)t.k * (double)t.k;
+                (fusedMerge[m] == 1 ? k2f : fusedMerge[m] == 2 ? k2l : k2g) += (double)t.k * (double)t.k;
             }
             mk = std::max<int64_t>(mk, t.k);
         }
@@ -1404,6 +1409,7 @@ int finish_solve(Handle* h) {
         h->stats.rotations = snn - sk;
         h->stats.k2_nonroot_fused = k2f;
         h->stats.k2_nonroot_grid = k2g;
+        h->stats.k2_nonroot_live = k2l;
         h->stats.nn_grid = nng;
         h->stats.k_grid = kg;
     }
@@ -1480,7 +1486,7 @@ int brgpu_create(brgpu_handle** out, int device) {
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMallocHost(&h->hsmall, sizeof(int) * 4) != cudaSuccess ||
-        cudaMallocHost(&h->hcnt, sizeof(unsigned long long) * 4) != cudaSuccess ||
+        cudaMallocHost(&h->hcnt, sizeof(unsigned long long) * kCounters) != cudaSuccess ||
         cudaMalloc(&h->dsmall, sizeof(int) * 4) != cudaSuccess ||
         cudaEventCreate(&h->tev[0]) != cudaSuccess || cudaEventCreate(&h->tev[1]) != cudaSuccess ||
         cudaEventCreate(&h->tev[2]) != cudaSuccess || cudaEventCreate(&h->tev[3]) != cudaSuccess ||

@@ -412,9 +412,9 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
         evals += __shfl_xor_sync(0xffffffffu, evals, o);
         terms += __shfl_xor_sync(0xffffffffu, terms, o);
     }
-    if (lane == 0 && evals) {
-        atomicAdd(&w.counters[0], evals);
-        atomicAdd(&w.counters[1], terms);
+    if (lane == 0 && evals) {  // live-tier work counters (api.cpp kCounters)
+        atomicAdd(&w.counters[8], evals);
+        atomicAdd(&w.counters[9], terms);
     }
     __syncthreads();
 
