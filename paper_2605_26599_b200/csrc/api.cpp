@@ -533,7 +533,9 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
     p->liveWanted = live;
     if (live && nranks == 1 && nblk == 1 && segs.size() == 2 && n >= kLiveMinN) {
         size_t li = p->levels.size();
-        while (li > 0 && !p->levels[li - 1].fused && p->levels[li - 1].minSize >= kLiveMinSize) --li;
+        while (li > 0 && !p->levels[li - 1].fused && p->levels[li - 1].minSize >= kLiveMinSize &&
+               p->levels[li - 1].maxSize <= kSplitMinSizeHost)  // live merges use lane arithmetic only
+            --li;
         if (li < p->levels.size()) {
             p->liveLev = (int)li;
             std::set<std::pair<int, int>> liveM;

@@ -26,12 +26,13 @@
 //    those of the dense tiers -- same operations in the same order, so every
 //    root, weight and row is bit-identical -- and the parent's live list is the
 //    restriction of the parent's order (deflated first on ties);
-//  * merges larger than kSplitMinSize use the 32-way split arithmetic of the
-//    warp tier (root_warp, lane-strided products / sums + xor butterflies).
+//  * a merge's live inputs (<= 512) keep K <= 1024: lane arithmetic (the split
+//    rule never applies; api.cpp keeps levels that could need it dense).
 // At the root the live list joins the pool (n values), which a bucket sort
 // (value buckets, rank sort per bucket in shared memory) puts in order.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.hpp"
@@ -46,6 +47,13 @@ constexpr int kLiveThreads = 256;
 constexpr int kLiveInitThreads = 256;
 constexpr int kBucketCap = 4096;   // elements of one final-sort bucket (shared memory)
 constexpr int kBucketThreads = 256;
+constexpr int kLiveCtasPerSm = 3;  // resident live CTAs per SM (launch bounds, shared memory)
+#ifndef BRGPU_LIVE_GROUP_MAX
+#define BRGPU_LIVE_GROUP_MAX 4
+#endif
+constexpr int kLiveGroupMax = BRGPU_LIVE_GROUP_MAX;
+
+constexpr int kLiveGroup = 4;      // merges of one batch
 
 struct LiveSmem {
     double D[kLiveMax];
@@ -66,11 +74,22 @@ struct LiveSmem {
     unsigned char flag[kLiveMax];
     unsigned char surv[kLiveMax];
     int scan[kLiveThreads / 32];
-    unsigned long long tolb;
-    unsigned long long dmx[3];  // demoted maxima bits: |lambda|, |first row|, |last row|
-    double dead[6];             // children's dead maxima: L (lam, blo, bhi), R (lam, blo, bhi)
-    int cntL, cntR, next, bail;
-    unsigned long long evals, terms;
+    // per merge of the batch
+    int mo[kLiveGroup + 1];    // local offsets (+ end)
+    int me[kLiveGroup];        // live inputs
+    int ml[kLiveGroup];        // ... of the left child
+    int mb[kLiveGroup];        // first position of the merge
+    int mnlF[kLiveGroup];      // left child's size
+    int kS[kLiveGroup + 1];    // active ranges
+    int ne[kLiveGroup + 1];    // merges with K > 0 before t (root queue order)
+    int outc[kLiveGroup];
+    double rho[kLiveGroup];
+    double tol[kLiveGroup];
+    double dead[6 * kLiveGroup];  // children's dead maxima: L (lam, blo, bhi), R (lam, blo, bhi)
+    unsigned long long tolb[kLiveGroup];
+    unsigned long long dmx[3 * kLiveGroup];  // demoted maxima bits: |lambda|, |first row|, |last row|
+    bool neg[kLiveGroup];
+    int next, bail, root, batch;
 };
 
 __device__ __forceinline__ unsigned long long dbits(double v) {
@@ -166,14 +185,17 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
 }
 
 // ---------------------------------------------------------------------------
-// One merge of a live level per CTA (the fused tier's shared-memory pipeline on
-// the children's live lists; fused.cu holds the commented dense original).
+// A batch of consecutive merges of a live level per CTA pass (live inputs of
+// the batch <= kLiveMax): the fused tier's shared-memory pipeline (fused.cu
+// holds the commented dense original) on the children's live lists.  A CTA owns
+// up to G merges and cuts them into batches greedily, so one CTA's 256 lanes
+// hold the roots of several merges of K ~ 100.
 // ---------------------------------------------------------------------------
-template <bool SPLIT>
-__device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, const LiveDev& V, const int m,
-                                           const SolveParams& prm, int* __restrict__ traceOut, LiveSmem& S) {
+__device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, const LiveDev& V, const int m0,
+                                           const int cnt, const SolveParams& prm, int* __restrict__ traceOut,
+                                           LiveSmem& S) {
     const int tid = threadIdx.x;
-    const int lane = tid & 31, wid = tid >> 5;
+    const int lane = tid & 31;
 #ifdef BRGPU_LIVE_PROF
     // phase cycles of the few-merge (latency-bound) levels, summed over CTAs in
     // counters[4..7]: deflation / secular / refreshed weights / rows + output
@@ -190,39 +212,53 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
 #else
 #define LIVE_MARK(k) do {} while (0)
 #endif
-    const int base = L.mOff[m], nlFull = L.mNL[m];
-    const bool isRoot = (L.mFlags[m] & kMergeRoot) != 0;
-    if (tid == 0) {
-        const int cl = V.cnt[base], cr = V.cnt[base + nlFull];
-        S.cntL = cl;
-        S.cntR = cr;
-        S.dead[0] = V.dLam[base];
-        S.dead[1] = V.dBlo[base];
-        S.dead[2] = V.dBhi[base];
-        S.dead[3] = V.dLam[base + nlFull];
-        S.dead[4] = V.dBlo[base + nlFull];
-        S.dead[5] = V.dBhi[base + nlFull];
+    // ---- batch metadata ---------------------------------------------------------
+    if (tid < cnt) {
+        const int m = m0 + tid;
+        const int base = L.mOff[m], nlF = L.mNL[m];
+        const int cl = V.cnt[base], cr = V.cnt[base + nlF];
+        S.mb[tid] = base;
+        S.mnlF[tid] = nlF;
+        S.ml[tid] = cl;
+        S.me[tid] = cl + cr;
+        const double em = w.ew[base + nlF - 1];
+        S.rho[tid] = fabs(em);
+        S.neg[tid] = em < 0;
+        double* dd = S.dead + 6 * tid;
+        dd[0] = V.dLam[base];
+        dd[1] = V.dBlo[base];
+        dd[2] = V.dBhi[base];
+        dd[3] = V.dLam[base + nlF];
+        dd[4] = V.dBlo[base + nlF];
+        dd[5] = V.dBhi[base + nlF];
         // tolerance terms of the dead elements: |lambda| of both children, |z| =
         // the left child's last row, the right child's first row
-        S.tolb = dbits(fmax(fmax(S.dead[0], S.dead[3]), fmax(S.dead[2], S.dead[4])));
-        S.dmx[0] = S.dmx[1] = S.dmx[2] = 0ULL;
+        S.tolb[tid] = dbits(fmax(fmax(dd[0], dd[3]), fmax(dd[2], dd[4])));
+        S.dmx[3 * tid] = S.dmx[3 * tid + 1] = S.dmx[3 * tid + 2] = 0ULL;
+    }
+    if (tid == 0) {
         S.next = 0;
-        S.evals = 0;
-        S.terms = 0;
-        S.bail = *(volatile int*)&V.ctl[1] != 0 || cl + cr > kLiveMax;
-        if (cl + cr > kLiveMax) live_fail(V);
+        S.root = (L.mFlags[m0] & kMergeRoot) != 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int o = 0;
+        for (int t = 0; t < cnt; ++t) { S.mo[t] = o; o += S.me[t]; }
+        S.mo[cnt] = o;
+        S.bail = *(volatile int*)&V.ctl[1] != 0 || o > kLiveMax;
+        if (o > kLiveMax) live_fail(V);
     }
     __syncthreads();
     if (S.bail) return;
-    const int nl = S.cntL, E = S.cntL + S.cntR;
-    const double em = w.ew[base + nlFull - 1];
-    const double rho = fabs(em);
-    const bool neg = em < 0;
+    const int E = S.mo[cnt];
+    const bool isRoot = S.root;
     double* lamIn = S.in;
     double* bloIn = S.in + kLiveMax;
     double* bhiIn = S.in + 2 * kLiveMax;
     for (int i = tid; i < E; i += kLiveThreads) {
-        const int src = i < nl ? base + i : base + nlFull + (i - nl);
+        const int t = upper_index(S.mo, cnt, i);
+        const int li = i - S.mo[t], nl = S.ml[t];
+        const int src = li < nl ? S.mb[t] + li : S.mb[t] + S.mnlF[t] + (li - nl);
         lamIn[i] = w.lam[src];
         bloIn[i] = w.blo[src];
         bhiIn[i] = w.bhi[src];
@@ -230,47 +266,65 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
     __syncthreads();
 
     // ---- tolerance: max(|D|, |z|) over the live and dead elements ------------
-    {
+    for (int b0 = 0; b0 < E; b0 += kLiveThreads) {
+        const int i = b0 + tid;
+        int t = -1;
         double v = 0.0;
-        for (int i = tid; i < E; i += kLiveThreads)
-            v = fmax(v, fmax(fabs(lamIn[i]), fabs(i < nl ? bhiIn[i] : bloIn[i])));
+        if (i < E) {
+            t = upper_index(S.mo, cnt, i);
+            v = fmax(fabs(lamIn[i]), fabs(i - S.mo[t] < S.ml[t] ? bhiIn[i] : bloIn[i]));
+        }
+        const int t0 = __shfl_sync(0xffffffffu, t, 0);
+        if (__all_sync(0xffffffffu, t == t0)) {  // one merge per warp: reduce, one shared atomic
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (lane == 0 && v > 0.0) atomicMax(&S.tolb, dbits(v));
+            for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0 && t0 >= 0 && v > 0.0) atomicMax(&S.tolb[t0], dbits(v));
+        } else if (t >= 0 && v > 0.0) {
+            atomicMax(&S.tolb[t], dbits(v));
+        }
     }
     __syncthreads();
-    const double tol = 8.0 * kU * bitsd(S.tolb) * prm.tol_scale;
-    if (!(S.dead[2] <= tol && S.dead[4] <= tol)) {  // a dead element would be non-negligible
-        if (tid == 0) live_fail(V);
-        return;
+    if (tid < cnt) {
+        const double tol = 8.0 * kU * bitsd(S.tolb[tid]) * prm.tol_scale;
+        S.tol[tid] = tol;
+        const double* dd = S.dead + 6 * tid;
+        if (!(dd[2] <= tol && dd[4] <= tol)) {  // a dead element would be non-negligible
+            S.bail = 1;
+            live_fail(V);
+        }
     }
+    __syncthreads();
+    if (S.bail) return;
 
-    // ---- stable merge of the two sorted live lists + z -----------------------
+    // ---- stable merge of each merge's two sorted live lists + z --------------
     for (int i = tid; i < E; i += kLiveThreads) {
+        const int t = upper_index(S.mo, cnt, i);
+        const int off = S.mo[t], nl = S.ml[t], Et = S.me[t];
+        const int li = i - off;
         const double v = lamIn[i];
         int sp;
         double z, r0, r1;
-        if (i < nl) {
-            sp = i + count_less(lamIn + nl, E - nl, v);
+        if (li < nl) {
+            sp = li + count_less(lamIn + off + nl, Et - nl, v);
             const double b = bhiIn[i];
-            z = neg ? -b : b;
+            z = S.neg[t] ? -b : b;
             r0 = bloIn[i];
             r1 = 0.0;
         } else {
-            sp = (i - nl) + count_leq(lamIn, nl, v);
+            sp = (li - nl) + count_leq(lamIn + off, nl, v);
             z = bloIn[i];
             r0 = 0.0;
             r1 = bhiIn[i];
         }
-        S.D[sp] = v;
-        S.Z[sp] = z;
-        S.R0[sp] = r0;
-        S.R1[sp] = r1;
+        S.D[off + sp] = v;
+        S.Z[off + sp] = z;
+        S.R0[off + sp] = r0;
+        S.R1[off + sp] = r1;
     }
     __syncthreads();
 
     // ---- small-z flags + NN compaction ---------------------------------------
-    for (int i = tid; i < E; i += kLiveThreads) S.flag[i] = fabs(S.Z[i]) > tol;
+    for (int i = tid; i < E; i += kLiveThreads) S.flag[i] = fabs(S.Z[i]) > S.tol[upper_index(S.mo, cnt, i)];
     __syncthreads();
     const int NN = cta_scan_flags<kLiveThreads>(S.flag, E, S.nnPre, S.scan);
     for (int i = tid; i < E; i += kLiveThreads)
@@ -284,14 +338,17 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
         double* pS1 = bhiIn;
         for (int q = tid; q < NN; q += kLiveThreads) {
             const int k = S.nnPos[q];
-            if (q > 0 && fabs(S.D[k] - S.D[S.nnPos[q - 1]]) <= tol) continue;  // not a head
+            const int t = upper_index(S.mo, cnt, k);
+            const int qs = S.nnPre[S.mo[t]], qe = S.nnPre[S.mo[t + 1]];
+            const double tol = S.tol[t];
+            if (q > qs && fabs(S.D[k] - S.D[S.nnPos[q - 1]]) <= tol) continue;  // not a head
             S.surv[q] = 1;
             int prev = k, nmem = 0;
             double dp = S.D[k];
             const double zs = S.Z[k];
             double Q = zs * zs, S0 = zs * S.R0[k], S1 = zs * S.R1[k];
             double dprev_nn = dp;
-            for (int q2 = q + 1; q2 < NN; ++q2) {
+            for (int q2 = q + 1; q2 < qe; ++q2) {
                 const int k2 = S.nnPos[q2];
                 const double d2 = S.D[k2];
                 if (fabs(d2 - dprev_nn) > tol) break;
@@ -347,33 +404,40 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
         S.r0A[g] = S.R0[k];
         S.r1A[g] = S.R1[k];
     }
+    if (tid <= cnt) S.kS[tid] = S.survPre[S.nnPre[S.mo[tid]]];
     __syncthreads();
-
+    // root queue: every merge's last root first, then the interior roots in order
+    // (the order never changes a result); ne[t] = merges with K > 0 before t
+    if (tid <= cnt) {
+        int c = 0;
+        for (int u = 0; u < tid; ++u) c += S.kS[u + 1] > S.kS[u];
+        S.ne[tid] = c;
+    }
+    __syncthreads();
+    int* qorder = S.nnPos;  // dead after the compaction
+    for (int g = tid; g < T; g += kLiveThreads) {
+        const int t = upper_index(S.kS, cnt, g);
+        qorder[g == S.kS[t + 1] - 1 ? S.ne[t] : S.ne[cnt] + g - S.ne[t]] = g;
+    }
+    __syncthreads();
     LIVE_MARK(0);
-    // ---- secular roots ---------------------------------------------------------
-    unsigned long long evals = 0, terms = 0;
-    if (SPLIT) {  // warp per root, split arithmetic (k_secular_warp's resident path)
-        for (int g = wid; g < T; g += kLiveThreads / 32) {
-            int o;
-            double tu;
-            root_warp(pairs, zA, T, g, rho, w.exact != 0, prm.patched != 0, w.status, o, tu, evals, terms);
-            if (lane == 0) {
-                S.org[g] = o;
-                S.tau[g] = tu;
-            }
-        }
-        if (lane) evals = terms = 0;  // every lane counted the warp's evaluations
-    } else {  // lane per root, CTA queue: the last root first, then the interior ones
+
+    // ---- secular roots: lane per root, CTA queue -----------------------------
+    {
         double2* snap = reinterpret_cast<double2*>(S.Z) + tid;  // S.Z is dead after the compaction
         RootSM st;
-        int g = -1;
+        int g = -1, ks = 0;
         bool exhausted = false;
+        unsigned long long evals = 0, terms = 0;
         for (;;) {
             while (g < 0 && !exhausted) {
                 const int q = atomicAdd(&S.next, 1);
                 if (q >= T) { exhausted = true; break; }
-                g = q == 0 ? T - 1 : q - 1;
-                rs_begin(st, T, g, rho, PolesPairs{pairs}, zA[0], Z2Pairs{pairs});
+                g = qorder[q];
+                const int t = upper_index(S.kS, cnt, g);
+                ks = S.kS[t];
+                const int K = S.kS[t + 1] - ks;
+                rs_begin(st, K, g - ks, S.rho[t], PolesPairs{pairs + ks}, zA[ks], Z2Pairs{pairs + ks});
                 if (st.phase == kRsDone) {
                     S.org[g] = st.org;
                     S.tau[g] = st.tau;
@@ -384,7 +448,7 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
             if (g >= 0) {
                 double sum, sum_abs, sum_d, psi;
                 bool pole = false;
-                const SmemPairs P{pairs};
+                const SmemPairs P{pairs + ks};
                 if (!w.exact && eval_guard(P, st.K, st.j, st.dorg, st.tau))
                     eval_fast(P, st.K, st.j, st.dorg, st.tau, sum, sum_abs, sum_d, psi, snap);
                 else
@@ -397,7 +461,7 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
                 ev.pole = pole;
                 ++evals;
                 terms += (unsigned long long)st.K;
-                rs_consume(st, ev, PolesPairs{pairs}, Z2Pairs{pairs}, prm.patched != 0);
+                rs_consume(st, ev, PolesPairs{pairs + ks}, Z2Pairs{pairs + ks}, prm.patched != 0);
                 if (st.phase == kRsDone || st.phase == kRsFail) {
                     if (st.phase == kRsFail) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
                     S.org[g] = st.org;
@@ -406,242 +470,205 @@ __device__ __forceinline__ void live_merge(const Work& w, const LevelDev& L, con
                 }
             }
         }
-    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        evals += __shfl_xor_sync(0xffffffffu, evals, o);
-        terms += __shfl_xor_sync(0xffffffffu, terms, o);
-    }
-    if (lane == 0 && evals) {  // live-tier work counters (api.cpp kCounters)
-        atomicAdd(&w.counters[8], evals);
-        atomicAdd(&w.counters[9], terms);
+        for (int o = 16; o > 0; o >>= 1) {
+            evals += __shfl_xor_sync(0xffffffffu, evals, o);
+            terms += __shfl_xor_sync(0xffffffffu, terms, o);
+        }
+        if (lane == 0 && evals) {  // live-tier work counters (api.cpp kCounters)
+            atomicAdd(&w.counters[8], evals);
+            atomicAdd(&w.counters[9], terms);
+        }
     }
     __syncthreads();
 
     double* sDorg = S.Z;  // d[origin] per root (S.Z is dead after the compaction)
-    for (int g = tid; g < T; g += kLiveThreads) sDorg[g] = pairs[S.org[g]].x;
+    for (int g = tid; g < T; g += kLiveThreads) sDorg[g] = pairs[S.kS[upper_index(S.kS, cnt, g)] + S.org[g]].x;
     __syncthreads();
-
     LIVE_MARK(1);
+
     // ---- Gu-Eisenstat refreshed weights (non-root merges, K > 1) -------------
-    if (prm.zhat && !isRoot && T > 1) {
-        if (SPLIT) {  // warp per pole: lane-strided products + xor butterfly (k_zhat_warp)
-            for (int i = wid; i < T; i += kLiveThreads / 32) {
-                const double di = pairs[i].x;
-                double prod = 1.0;
-                if (!w.exact && zhat_guard(PolesPairs{pairs}, T, i)) {
-                    for (int j = lane; j < T; j += 32) {
-                        const double del = (di - sDorg[j]) - S.tau[j];
-                        prod = prod * (j == i ? del : del * rcp_nr(di - pairs[j].x));
-                    }
-                } else {
-                    for (int j = lane; j < T; j += 32) {
-                        const double del = (di - sDorg[j]) - S.tau[j];
-                        if (j == i) prod = prod * del;
-                        else prod = prod * (del * __drcp_rn(di - pairs[j].x));
-                    }
-                }
-                const double W = bfly_mul(prod);
-                if (lane == 0) {
-                    const double mag = sqrt(fmax(0.0, -W));
-                    zA[i] = zA[i] >= 0.0 ? mag : -mag;
-                }
-            }
-        } else {
-            for (int i = tid; i < T; i += kLiveThreads) {
-                const double di = pairs[i].x;
-                double prod = 1.0;
-                if (!w.exact && zhat_guard(PolesPairs{pairs}, T, i)) {
+    if (prm.zhat && !isRoot) {
+        for (int g = tid; g < T; g += kLiveThreads) {
+            const int t = upper_index(S.kS, cnt, g);
+            const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
+            if (K == 1) continue;  // a lone pole keeps its z (the checker refreshes only K > 1)
+            const double di = pairs[g].x;
+            double prod = 1.0;
+            if (!w.exact && zhat_guard(PolesPairs{pairs + ks}, K, i)) {
 #pragma unroll 4
-                    for (int j = 0; j < T; ++j) {
-                        const double del = (di - sDorg[j]) - S.tau[j];
-                        const double dd = di - pairs[j].x;
-                        const double f = (j == i) ? del : del * rcp_nr(dd);
-                        prod = prod * f;
-                    }
-                } else {
-                    for (int j = 0; j < T; ++j) {
-                        const double del = (di - pairs[S.org[j]].x) - S.tau[j];
-                        if (j == i) prod = prod * del;
-                        else prod = prod * (del * __drcp_rn(di - pairs[j].x));
-                    }
+                for (int j = 0; j < K; ++j) {
+                    const double del = (di - sDorg[ks + j]) - S.tau[ks + j];
+                    const double dd = di - pairs[ks + j].x;
+                    const double f = (j == i) ? del : del * rcp_nr(dd);
+                    prod = prod * f;
                 }
-                const double mag = sqrt(fmax(0.0, -prod));
-                zA[i] = zA[i] >= 0.0 ? mag : -mag;
+            } else {
+                for (int j = 0; j < K; ++j) {
+                    const double del = (di - pairs[ks + S.org[ks + j]].x) - S.tau[ks + j];
+                    if (j == i) prod = prod * del;
+                    else prod = prod * (del * __drcp_rn(di - pairs[ks + j].x));
+                }
             }
+            const double mag = sqrt(fmax(0.0, -prod));
+            zA[g] = zA[g] >= 0.0 ? mag : -mag;
         }
         __syncthreads();
     }
-
     LIVE_MARK(2);
+
     // ---- roots: position in the parent's live order + boundary rows ----------
-    auto root_pos = [&](int j, double lam) {
-        int lo = 0, hi = T;  // #{dA <= lam}
+    for (int g = tid; g < T; g += kLiveThreads) {
+        const int t = upper_index(S.kS, cnt, g);
+        const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
+        const int off = S.mo[t];
+        const double dorg = sDorg[g], tau = S.tau[g];
+        const double lam = dorg + tau;
+        int lo = 0, hi = K;  // #{dA <= lam}
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (!(lam < pairs[mid].x)) lo = mid + 1; else hi = mid;
+            if (!(lam < pairs[ks + mid].x)) lo = mid + 1; else hi = mid;
         }
-        return j + count_leq(S.D, E, lam) - lo;
-    };
-    if (SPLIT && !isRoot) {  // warp per root: lane-strided sums + butterflies (k_rows_warp)
-        for (int j = wid; j < T; j += kLiveThreads / 32) {
-            const double dorg = sDorg[j], tau = S.tau[j];
-            const double lam = dorg + tau;
-            const int pos = root_pos(j, lam);
-            double nn = 0.0, s0 = 0.0, s1 = 0.0;
-            if (!w.exact && eval_guard(SmemPairs{pairs}, T, j, dorg, tau)) {
-                for (int i = lane; i < T; i += 32) {
-                    const double y = zA[i] * rcp_nr((pairs[i].x - dorg) - tau);
-                    nn = __fma_rn(y, y, nn);
-                    s0 = __fma_rn(S.r0A[i], y, s0);
-                    s1 = __fma_rn(S.r1A[i], y, s1);
-                }
-            } else {
-                bool zero = false;
-                for (int i = lane; i < T; i += 32) {
-                    const double del = (pairs[i].x - dorg) - tau;
-                    zero |= (del == 0.0);
-                    const double y = zA[i] * __drcp_rn(del);
-                    nn = __fma_rn(y, y, nn);
-                    s0 = __fma_rn(S.r0A[i], y, s0);
-                    s1 = __fma_rn(S.r1A[i], y, s1);
-                }
-                if (__any_sync(0xffffffffu, zero) && lane == 0) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
-            }
-            const double NNs = bfly_add(nn), S0 = bfly_add(s0), S1 = bfly_add(s1);
-            if (lane == 0) {
-                const double inv = 1.0 / sqrt(NNs);
-                S.oLam[pos] = lam;
-                S.oR0[pos] = S0 * inv;
-                S.oR1[pos] = S1 * inv;
-            }
-        }
-    } else {
-        for (int j = tid; j < T; j += kLiveThreads) {
-            const double dorg = sDorg[j], tau = S.tau[j];
-            const double lam = dorg + tau;
-            const int pos = root_pos(j, lam);
-            S.oLam[pos] = lam;
-            if (isRoot) continue;
-            double nn = 0.0, s0 = 0.0, s1 = 0.0;
-            if (!w.exact && eval_guard(SmemPairs{pairs}, T, j, dorg, tau)) {
+        const int p = off + j + count_leq(S.D + off, S.me[t], lam) - lo;
+        S.oLam[p] = lam;
+        if (isRoot) continue;
+        double nn = 0.0, s0 = 0.0, s1 = 0.0;
+        if (!w.exact && eval_guard(SmemPairs{pairs + ks}, K, j, dorg, tau)) {
 #pragma unroll 4
-                for (int i = 0; i < T; ++i) {
-                    const double y = zA[i] * rcp_nr((pairs[i].x - dorg) - tau);
-                    nn = __fma_rn(y, y, nn);
-                    s0 = __fma_rn(S.r0A[i], y, s0);
-                    s1 = __fma_rn(S.r1A[i], y, s1);
-                }
-            } else {
-                bool zero = false;
-                for (int i = 0; i < T; ++i) {
-                    const double del = (pairs[i].x - dorg) - tau;
-                    zero |= (del == 0.0);
-                    const double y = zA[i] * __drcp_rn(del);
-                    nn = __fma_rn(y, y, nn);
-                    s0 = __fma_rn(S.r0A[i], y, s0);
-                    s1 = __fma_rn(S.r1A[i], y, s1);
-                }
-                if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+            for (int i = 0; i < K; ++i) {
+                const double y = zA[ks + i] * rcp_nr((pairs[ks + i].x - dorg) - tau);
+                nn = __fma_rn(y, y, nn);
+                s0 = __fma_rn(S.r0A[ks + i], y, s0);
+                s1 = __fma_rn(S.r1A[ks + i], y, s1);
             }
-            const double inv = 1.0 / sqrt(nn);
-            S.oR0[pos] = s0 * inv;
-            S.oR1[pos] = s1 * inv;
+        } else {
+            bool zero = false;
+            for (int i = 0; i < K; ++i) {
+                const double del = (pairs[ks + i].x - dorg) - tau;
+                zero |= (del == 0.0);
+                const double y = zA[ks + i] * __drcp_rn(del);
+                nn = __fma_rn(y, y, nn);
+                s0 = __fma_rn(S.r0A[ks + i], y, s0);
+                s1 = __fma_rn(S.r1A[ks + i], y, s1);
+            }
+            if (zero) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
         }
+        const double inv = 1.0 / sqrt(nn);
+        S.oR0[p] = s0 * inv;
+        S.oR1[p] = s1 * inv;
     }
     // deflated live elements: t + #{roots < D}
     for (int k = tid; k < E; k += kLiveThreads) {
         const int q = S.nnPre[k];
         if (S.flag[k] && S.surv[q]) continue;  // survivor: its column became a root
-        const int tt = k - S.survPre[q];
+        const int t = upper_index(S.mo, cnt, k);
+        const int off = S.mo[t], ks = S.kS[t], K = S.kS[t + 1] - ks;
+        const int tt = (k - off) - (S.survPre[q] - ks);
         const double v = S.D[k];
-        int lo = 0, hi = T;
+        int lo = 0, hi = K;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            const double lj = sDorg[mid] + S.tau[mid];
+            const double lj = sDorg[ks + mid] + S.tau[ks + mid];
             if (lj < v) lo = mid + 1; else hi = mid;
         }
-        S.oLam[tt + lo] = v;
-        S.oR0[tt + lo] = S.R0[k];
-        S.oR1[tt + lo] = S.R1[k];
+        S.oLam[off + tt + lo] = v;
+        S.oR0[off + tt + lo] = S.R0[k];
+        S.oR1[off + tt + lo] = S.R1[k];
     }
     __syncthreads();
 
-    // ---- parent's live list: demote outputs with both rows <= tol / 2 --------
+    // ---- parents' live lists: demote outputs with both rows <= tol / 2 --------
     if (isRoot) {  // the root's eigenvalues join the pool for the final sort
         for (int c0 = 0; c0 < E; c0 += kLiveThreads) {
             const int i = c0 + tid;
             pool_push(V, i < E, i < E ? S.oLam[i] : 0.0);
         }
     } else {
-        const double theta = 0.5 * tol;
-        int out = 0;
-        double dl = 0.0, d0 = 0.0, d1 = 0.0;
-        for (int c0 = 0; c0 < E; c0 += kLiveThreads) {
-            const int i = c0 + tid;
-            const bool valid = i < E;
-            double v = 0.0, b0 = 0.0, b1 = 0.0;
-            if (valid) { v = S.oLam[i]; b0 = S.oR0[i]; b1 = S.oR1[i]; }
-            const bool live = valid && fmax(fabs(b0), fabs(b1)) > theta;
-            const bool dead = valid && !live;
-            pool_push(V, dead, v);
-            if (dead) {
-                dl = fmax(dl, fabs(v));
-                d0 = fmax(d0, fabs(b0));
-                d1 = fmax(d1, fabs(b1));
+        for (int t = 0; t < cnt; ++t) {
+            const int off = S.mo[t], Et = S.me[t], base = S.mb[t];
+            const double theta = 0.5 * S.tol[t];
+            int out = 0;
+            double dl = 0.0, d0 = 0.0, d1 = 0.0;
+            for (int c0 = 0; c0 < Et; c0 += kLiveThreads) {
+                const int i = c0 + tid;
+                const bool valid = i < Et;
+                double v = 0.0, b0 = 0.0, b1 = 0.0;
+                if (valid) { v = S.oLam[off + i]; b0 = S.oR0[off + i]; b1 = S.oR1[off + i]; }
+                const bool live = valid && fmax(fabs(b0), fabs(b1)) > theta;
+                const bool dead = valid && !live;
+                pool_push(V, dead, v);
+                if (dead) {
+                    dl = fmax(dl, fabs(v));
+                    d0 = fmax(d0, fabs(b0));
+                    d1 = fmax(d1, fabs(b1));
+                }
+                int tot;
+                const int ex = block_exclusive_scan<kLiveThreads>(live ? 1 : 0, tot);
+                if (live) {
+                    const int p = base + out + ex;
+                    w.lam[p] = v;
+                    w.blo[p] = b0;
+                    w.bhi[p] = b1;
+                }
+                out += tot;
             }
-            int tot;
-            const int ex = block_exclusive_scan<kLiveThreads>(live ? 1 : 0, tot);
-            if (live) {
-                const int p = base + out + ex;
-                w.lam[p] = v;
-                w.blo[p] = b0;
-                w.bhi[p] = b1;
-            }
-            out += tot;
-        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            dl = fmax(dl, __shfl_xor_sync(0xffffffffu, dl, o));
-            d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
-            d1 = fmax(d1, __shfl_xor_sync(0xffffffffu, d1, o));
-        }
-        if (lane == 0) {
-            if (dl > 0.0) atomicMax(&S.dmx[0], dbits(dl));
-            if (d0 > 0.0) atomicMax(&S.dmx[1], dbits(d0));
-            if (d1 > 0.0) atomicMax(&S.dmx[2], dbits(d1));
+            for (int o = 16; o > 0; o >>= 1) {
+                dl = fmax(dl, __shfl_xor_sync(0xffffffffu, dl, o));
+                d0 = fmax(d0, __shfl_xor_sync(0xffffffffu, d0, o));
+                d1 = fmax(d1, __shfl_xor_sync(0xffffffffu, d1, o));
+            }
+            if (lane == 0) {
+                if (dl > 0.0) atomicMax(&S.dmx[3 * t], dbits(dl));
+                if (d0 > 0.0) atomicMax(&S.dmx[3 * t + 1], dbits(d0));
+                if (d1 > 0.0) atomicMax(&S.dmx[3 * t + 2], dbits(d1));
+            }
+            if (tid == 0) S.outc[t] = out;
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid < cnt) {
             // parent rows of the children's dead elements: left (first row, 0), right (0, last row)
-            V.cnt[base] = out;
-            V.dLam[base] = fmax(fmax(S.dead[0], S.dead[3]), bitsd(S.dmx[0]));
-            V.dBlo[base] = fmax(S.dead[1], bitsd(S.dmx[1]));
-            V.dBhi[base] = fmax(S.dead[5], bitsd(S.dmx[2]));
+            const int base = S.mb[tid];
+            const double* dd = S.dead + 6 * tid;
+            V.cnt[base] = S.outc[tid];
+            V.dLam[base] = fmax(fmax(dd[0], dd[3]), bitsd(S.dmx[3 * tid]));
+            V.dBlo[base] = fmax(dd[1], bitsd(S.dmx[3 * tid + 1]));
+            V.dBhi[base] = fmax(dd[5], bitsd(S.dmx[3 * tid + 2]));
         }
     }
     LIVE_MARK(3);
 #undef LIVE_MARK
-    if (traceOut && tid == 0) {
-        traceOut[2 * m] = NN;
-        traceOut[2 * m + 1] = T;
+    if (traceOut && tid < cnt) {
+        traceOut[2 * (m0 + tid)] = S.nnPre[S.mo[tid + 1]] - S.nnPre[S.mo[tid]];
+        traceOut[2 * (m0 + tid) + 1] = S.kS[tid + 1] - S.kS[tid];
     }
 }
 
-// MODE 0: lane arithmetic, 1: split arithmetic (every merge > kSplitMinSize),
-// 2: per merge (a level with merges on both sides of the rule)
-template <int MODE>
+// A CTA owns merges [blockIdx.x * G, +G) of the level and processes them in
+// batches of consecutive merges whose live inputs fit kLiveMax.
 __global__ void __launch_bounds__(kLiveThreads, 3)
-k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ traceOut) {
+k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ traceOut, int G) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char live_raw[];
     LiveSmem& S = *reinterpret_cast<LiveSmem*>(live_raw);
-    const int m = blockIdx.x;
-    if (MODE == 2) {
-        if (L.mSize[m] > kSplitMinSize) live_merge<true>(w, L, V, m, prm, traceOut, S);
-        else live_merge<false>(w, L, V, m, prm, traceOut, S);
-    } else {
-        live_merge<MODE == 1>(w, L, V, m, prm, traceOut, S);
+    const int mEnd = min(L.M, (blockIdx.x + 1) * G);
+    for (int m = blockIdx.x * G; m < mEnd;) {
+        if (threadIdx.x == 0) {
+            int c = 0, sum = 0;
+            while (m + c < mEnd && c < kLiveGroup) {
+                const int base = L.mOff[m + c];
+                const int e = V.cnt[base] + V.cnt[base + L.mNL[m + c]];
+                if (c > 0 && sum + e > kLiveMax) break;
+                sum += e;
+                ++c;
+            }
+            S.batch = c;
+        }
+        __syncthreads();
+        const int c = S.batch;
+        live_group(w, L, V, m, c, prm, traceOut, S);
+        __syncthreads();
+        m += c;
     }
 }
 
@@ -790,12 +817,11 @@ void launch_live_init(cudaStream_t s, const Work& w, const LiveDev& V, const int
 
 void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
                        const SolveParams& prm, int* traceOut, int* launches, Prof* prof) {
-    if (L.allSplit)
-        launch_pdl(k_live_level<1>, L.M, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut);
-    else if (L.maxSize > kSplitMinSize)
-        launch_pdl(k_live_level<2>, L.M, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut);
-    else
-        launch_pdl(k_live_level<0>, L.M, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut);
+    // merges per CTA: a level of many merges packs up to kLiveGroup per CTA
+    // (a merge keeps K ~ 100 roots for 256 lanes), a few-merge level keeps one
+    const int per = std::max(1, std::min(kLiveGroup, L.M / (prm.sms * kLiveCtasPerSm)));
+    const int G = std::min(per, kLiveGroupMax);
+    launch_pdl(k_live_level, (L.M + G - 1) / G, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut, G);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
@@ -815,9 +841,7 @@ int live_buckets(int n) { return n / 128 > 1 ? n / 128 : 1; }
 int live_max_elems() { return kLiveMax; }
 
 void init_live_attributes() {
-    cudaFuncSetAttribute(k_live_level<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
-    cudaFuncSetAttribute(k_live_level<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
-    cudaFuncSetAttribute(k_live_level<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
+    cudaFuncSetAttribute(k_live_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
 }
 
 static_assert(sizeof(LiveSmem) <= 75 * 1024, "three live CTAs per SM");
