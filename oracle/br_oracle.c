@@ -307,19 +307,17 @@ static ev_t eval_shifted(int k, const double* d, const double* z, double rho, in
     return r;
 }
 
-/* ---- 32-way split arithmetic (GPU spec for merges of active rank K > 1024):
- * a warp owns one root / pole; lane l
+/* ---- 32-way split arithmetic (GPU spec for merges larger than 8192 or of
+ * active rank K > 1024): a warp owns one root / pole; lane l
  * accumulates the terms i = l, l+32, ... in increasing order; the 32 partials
  * are combined by the xor butterfly a[l] <- a[l] + a[l ^ off], off = 16..1
  * (every lane ends with the same value; this is lane 0's). */
 #define BRO_SPLIT 32
 #ifndef BRO_SPLIT_MIN_SIZE
-#define BRO_SPLIT_MIN_SIZE (1 << 30)  /* no size rule (round 2: 8192) */
+#define BRO_SPLIT_MIN_SIZE 8192
 #endif
 #define BRO_SPLIT_MIN_K 1024
-/* split iff the merge's active rank exceeds 1024 (the size rule -- merges
- * larger than 8192 -- was dropped: K <= 1024 roots run lane arithmetic at any
- * merge size, which the live-list tier solves lane-per-root) */
+/* split iff the merge is larger than 8192 or its active rank exceeds 1024 */
 
 static double bfly_add(double* a) {
     double b[BRO_SPLIT];

@@ -16,7 +16,7 @@ Q_parent = blockdiag(Q_L, Q_R) P G U with U formed explicitly and multiplied
 with BLAS -- independent of the BR path's streamed boundary-row dots, so the
 per-merge agreement is a real check, not an identity.  The reference declares
 full_dc_eigen (proj/include/br/oracle.hpp:53) but ships no implementation.
-Single irreducible block, lane (non-split) arithmetic: every merge K <= 1024.
+Single irreducible block, lane (non-split) arithmetic: n <= 8192.
 """
 from __future__ import annotations
 

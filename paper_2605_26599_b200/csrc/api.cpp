@@ -97,7 +97,7 @@ constexpr int kGridManyMinSize = BRGPU_GRID_MANY_MIN_SIZE;  // ... when their me
 constexpr int kFuseSmallElems = 512;  // small fused shape (fused.cu)
 constexpr int kSpMinSpan = 16;        // smallest k_sp_solve group key span (group table size)
 #ifndef BRGPU_SPLIT_MIN_SIZE
-#define BRGPU_SPLIT_MIN_SIZE (1 << 30)
+#define BRGPU_SPLIT_MIN_SIZE 8192
 #endif
 constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
 constexpr int kFuseMaxMergesHost = 128;
@@ -533,9 +533,7 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
     p->liveWanted = live;
     if (live && nranks == 1 && nblk == 1 && segs.size() == 2 && n >= kLiveMinN) {
         size_t li = p->levels.size();
-        while (li > 0 && !p->levels[li - 1].fused && p->levels[li - 1].minSize >= kLiveMinSize &&
-               p->levels[li - 1].maxSize <= kSplitMinSizeHost)  // live merges use lane arithmetic only
-            --li;
+        while (li > 0 && !p->levels[li - 1].fused && p->levels[li - 1].minSize >= kLiveMinSize) --li;
         if (li < p->levels.size()) {
             p->liveLev = (int)li;
             std::set<std::pair<int, int>> liveM;

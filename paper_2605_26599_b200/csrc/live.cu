@@ -26,8 +26,9 @@
 //    those of the dense tiers -- same operations in the same order, so every
 //    root, weight and row is bit-identical -- and the parent's live list is the
 //    restriction of the parent's order (deflated first on ties);
-//  * a merge's live inputs (<= 512) keep K <= 1024: lane arithmetic (the split
-//    rule never applies; api.cpp keeps levels that could need it dense).
+//  * merges larger than kSplitMinSize use the warp tier's 32-way split
+//    arithmetic (root_warp, lane-strided products / sums + xor butterflies), one
+//    merge per 1024-thread CTA so that every root / pole gets its own warp.
 // At the root the live list joins the pool (n values), which a bucket sort
 // (value buckets, rank sort per bucket in shared memory) puts in order.
 #include <cuda_runtime.h>
@@ -47,7 +48,11 @@ constexpr int kLiveThreads = 256;
 constexpr int kLiveInitThreads = 256;
 constexpr int kBucketCap = 4096;   // elements of one final-sort bucket (shared memory)
 constexpr int kBucketThreads = 256;
-constexpr int kLiveCtasPerSm = 3;  // resident live CTAs per SM (launch bounds, shared memory)
+constexpr int kLiveCtasPerSm = 3;
+#ifndef BRGPU_LIVE_SPLIT_THREADS
+#define BRGPU_LIVE_SPLIT_THREADS 1024
+#endif
+constexpr int kLiveSplitThreads = BRGPU_LIVE_SPLIT_THREADS;  // split-rule levels: a warp per root  // resident live CTAs per SM (launch bounds, shared memory)
 #ifndef BRGPU_LIVE_GROUP_MAX
 #define BRGPU_LIVE_GROUP_MAX 4
 #endif
@@ -73,7 +78,7 @@ struct LiveSmem {
     int survPre[kLiveMax + 1];
     unsigned char flag[kLiveMax];
     unsigned char surv[kLiveMax];
-    int scan[kLiveThreads / 32];
+    int scan[32];              // warp totals of a CTA scan (<= 1024 threads)
     // per merge of the batch
     int mo[kLiveGroup + 1];    // local offsets (+ end)
     int me[kLiveGroup];        // live inputs
@@ -191,11 +196,12 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
 // up to G merges and cuts them into batches greedily, so one CTA's 256 lanes
 // hold the roots of several merges of K ~ 100.
 // ---------------------------------------------------------------------------
+template <bool SPLIT, int NT>
 __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, const LiveDev& V, const int m0,
                                            const int cnt, const SolveParams& prm, int* __restrict__ traceOut,
                                            LiveSmem& S) {
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
+    const int lane = tid & 31, wid = tid >> 5;
 #ifdef BRGPU_LIVE_PROF
     // phase cycles of the few-merge (latency-bound) levels, summed over CTAs in
     // counters[4..7]: deflation / secular / refreshed weights / rows + output
@@ -255,7 +261,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     double* lamIn = S.in;
     double* bloIn = S.in + kLiveMax;
     double* bhiIn = S.in + 2 * kLiveMax;
-    for (int i = tid; i < E; i += kLiveThreads) {
+    for (int i = tid; i < E; i += NT) {
         const int t = upper_index(S.mo, cnt, i);
         const int li = i - S.mo[t], nl = S.ml[t];
         const int src = li < nl ? S.mb[t] + li : S.mb[t] + S.mnlF[t] + (li - nl);
@@ -266,7 +272,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     __syncthreads();
 
     // ---- tolerance: max(|D|, |z|) over the live and dead elements ------------
-    for (int b0 = 0; b0 < E; b0 += kLiveThreads) {
+    for (int b0 = 0; b0 < E; b0 += NT) {
         const int i = b0 + tid;
         int t = -1;
         double v = 0.0;
@@ -297,7 +303,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     if (S.bail) return;
 
     // ---- stable merge of each merge's two sorted live lists + z --------------
-    for (int i = tid; i < E; i += kLiveThreads) {
+    for (int i = tid; i < E; i += NT) {
         const int t = upper_index(S.mo, cnt, i);
         const int off = S.mo[t], nl = S.ml[t], Et = S.me[t];
         const int li = i - off;
@@ -324,10 +330,10 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     __syncthreads();
 
     // ---- small-z flags + NN compaction ---------------------------------------
-    for (int i = tid; i < E; i += kLiveThreads) S.flag[i] = fabs(S.Z[i]) > S.tol[upper_index(S.mo, cnt, i)];
+    for (int i = tid; i < E; i += NT) S.flag[i] = fabs(S.Z[i]) > S.tol[upper_index(S.mo, cnt, i)];
     __syncthreads();
-    const int NN = cta_scan_flags<kLiveThreads>(S.flag, E, S.nnPre, S.scan);
-    for (int i = tid; i < E; i += kLiveThreads)
+    const int NN = cta_scan_flags<NT>(S.flag, E, S.nnPre, S.scan);
+    for (int i = tid; i < E; i += NT)
         if (S.flag[i]) S.nnPos[S.nnPre[i]] = i;
     __syncthreads();
 
@@ -336,7 +342,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         double* pQ = lamIn;
         double* pS0 = bloIn;
         double* pS1 = bhiIn;
-        for (int q = tid; q < NN; q += kLiveThreads) {
+        for (int q = tid; q < NN; q += NT) {
             const int k = S.nnPos[q];
             const int t = upper_index(S.mo, cnt, k);
             const int qs = S.nnPre[S.mo[t]], qe = S.nnPre[S.mo[t + 1]];
@@ -379,7 +385,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
             }
         }
         __syncthreads();
-        for (int q = tid; q < NN; q += kLiveThreads) {
+        for (int q = tid; q < NN; q += NT) {
             if (S.surv[q]) continue;
             const int k = S.nnPos[q];
             double x0 = S.R0[k], x1 = S.R1[k];
@@ -392,10 +398,10 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     __syncthreads();
 
     // ---- survivor compaction: active (d, z^2) pairs, z, rows ------------------
-    const int T = cta_scan_flags<kLiveThreads>(S.surv, NN, S.survPre, S.scan);
+    const int T = cta_scan_flags<NT>(S.surv, NN, S.survPre, S.scan);
     double2* pairs = reinterpret_cast<double2*>(S.in);  // aliases lam/blo inputs (dead)
     double* zA = S.in + 2 * kLiveMax;                    // aliases the bhi input (dead)
-    for (int q = tid; q < NN; q += kLiveThreads) {
+    for (int q = tid; q < NN; q += NT) {
         if (!S.surv[q]) continue;
         const int g = S.survPre[q], k = S.nnPos[q];
         const double z = S.Z[k];
@@ -415,15 +421,38 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     }
     __syncthreads();
     int* qorder = S.nnPos;  // dead after the compaction
-    for (int g = tid; g < T; g += kLiveThreads) {
+    for (int g = tid; g < T; g += NT) {
         const int t = upper_index(S.kS, cnt, g);
         qorder[g == S.kS[t + 1] - 1 ? S.ne[t] : S.ne[cnt] + g - S.ne[t]] = g;
     }
     __syncthreads();
     LIVE_MARK(0);
 
-    // ---- secular roots: lane per root, CTA queue -----------------------------
-    {
+    // ---- secular roots ---------------------------------------------------------
+    if (SPLIT) {  // warp per root, 32-way split arithmetic (k_secular_warp), warp queue
+        unsigned long long ev = 0, tm = 0;
+        for (;;) {
+            int q = 0;
+            if (lane == 0) q = atomicAdd(&S.next, 1);
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (q >= T) break;
+            const int g = qorder[q];
+            const int t = upper_index(S.kS, cnt, g);
+            const int ks = S.kS[t], K = S.kS[t + 1] - ks;
+            int o;
+            double tu;
+            root_warp(pairs + ks, zA + ks, K, g - ks, S.rho[t], w.exact != 0, prm.patched != 0, w.status, o, tu,
+                      ev, tm);
+            if (lane == 0) {
+                S.org[g] = o;
+                S.tau[g] = tu;
+            }
+        }
+        if (lane == 0 && ev) {  // every lane counted its warp's evaluations: lane 0 reports
+            atomicAdd(&w.counters[8], ev);
+            atomicAdd(&w.counters[9], tm);
+        }
+    } else {  // lane per root, CTA queue
         double2* snap = reinterpret_cast<double2*>(S.Z) + tid;  // S.Z is dead after the compaction
         RootSM st;
         int g = -1, ks = 0;
@@ -483,13 +512,39 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     __syncthreads();
 
     double* sDorg = S.Z;  // d[origin] per root (S.Z is dead after the compaction)
-    for (int g = tid; g < T; g += kLiveThreads) sDorg[g] = pairs[S.kS[upper_index(S.kS, cnt, g)] + S.org[g]].x;
+    for (int g = tid; g < T; g += NT) sDorg[g] = pairs[S.kS[upper_index(S.kS, cnt, g)] + S.org[g]].x;
     __syncthreads();
     LIVE_MARK(1);
 
     // ---- Gu-Eisenstat refreshed weights (non-root merges, K > 1) -------------
-    if (prm.zhat && !isRoot) {
-        for (int g = tid; g < T; g += kLiveThreads) {
+    if (prm.zhat && !isRoot && SPLIT) {  // warp per pole: lane-strided products + butterfly (k_zhat_warp)
+        for (int g = wid; g < T; g += NT / 32) {
+            const int t = upper_index(S.kS, cnt, g);
+            const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
+            if (K == 1) continue;  // a lone pole keeps its z (the checker refreshes only K > 1)
+            const double di = pairs[g].x;
+            double prod = 1.0;
+            if (!w.exact && zhat_guard(PolesPairs{pairs + ks}, K, i)) {
+                for (int j = lane; j < K; j += 32) {
+                    const double del = (di - sDorg[ks + j]) - S.tau[ks + j];
+                    prod = prod * (j == i ? del : del * rcp_nr(di - pairs[ks + j].x));
+                }
+            } else {
+                for (int j = lane; j < K; j += 32) {
+                    const double del = (di - sDorg[ks + j]) - S.tau[ks + j];
+                    if (j == i) prod = prod * del;
+                    else prod = prod * (del * __drcp_rn(di - pairs[ks + j].x));
+                }
+            }
+            const double W = bfly_mul(prod);
+            if (lane == 0) {
+                const double mag = sqrt(fmax(0.0, -W));
+                zA[g] = zA[g] >= 0.0 ? mag : -mag;
+            }
+        }
+        __syncthreads();
+    } else if (prm.zhat && !isRoot) {
+        for (int g = tid; g < T; g += NT) {
             const int t = upper_index(S.kS, cnt, g);
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
             if (K == 1) continue;  // a lone pole keeps its z (the checker refreshes only K > 1)
@@ -518,7 +573,50 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     LIVE_MARK(2);
 
     // ---- roots: position in the parent's live order + boundary rows ----------
-    for (int g = tid; g < T; g += kLiveThreads) {
+    if (SPLIT) {  // warp per root: lane-strided sums + butterflies (k_rows_warp)
+        for (int g = wid; g < T; g += NT / 32) {
+            const int t = upper_index(S.kS, cnt, g);
+            const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
+            const int off = S.mo[t];
+            const double dorg = sDorg[g], tau = S.tau[g];
+            const double lam = dorg + tau;
+            int lo = 0, hi = K;  // #{dA <= lam}
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (!(lam < pairs[ks + mid].x)) lo = mid + 1; else hi = mid;
+            }
+            const int p = off + j + count_leq(S.D + off, S.me[t], lam) - lo;
+            if (lane == 0) S.oLam[p] = lam;
+            if (isRoot) continue;
+            double nn = 0.0, s0 = 0.0, s1 = 0.0;
+            if (!w.exact && eval_guard(SmemPairs{pairs + ks}, K, j, dorg, tau)) {
+                for (int i = lane; i < K; i += 32) {
+                    const double y = zA[ks + i] * rcp_nr((pairs[ks + i].x - dorg) - tau);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(S.r0A[ks + i], y, s0);
+                    s1 = __fma_rn(S.r1A[ks + i], y, s1);
+                }
+            } else {
+                bool zero = false;
+                for (int i = lane; i < K; i += 32) {
+                    const double del = (pairs[ks + i].x - dorg) - tau;
+                    zero |= (del == 0.0);
+                    const double y = zA[ks + i] * __drcp_rn(del);
+                    nn = __fma_rn(y, y, nn);
+                    s0 = __fma_rn(S.r0A[ks + i], y, s0);
+                    s1 = __fma_rn(S.r1A[ks + i], y, s1);
+                }
+                if (__any_sync(0xffffffffu, zero) && lane == 0) set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+            }
+            const double NNs = bfly_add(nn), S0 = bfly_add(s0), S1 = bfly_add(s1);
+            if (lane == 0) {
+                const double inv = 1.0 / sqrt(NNs);
+                S.oR0[p] = S0 * inv;
+                S.oR1[p] = S1 * inv;
+            }
+        }
+    } else
+    for (int g = tid; g < T; g += NT) {
         const int t = upper_index(S.kS, cnt, g);
         const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
         const int off = S.mo[t];
@@ -558,7 +656,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         S.oR1[p] = s1 * inv;
     }
     // deflated live elements: t + #{roots < D}
-    for (int k = tid; k < E; k += kLiveThreads) {
+    for (int k = tid; k < E; k += NT) {
         const int q = S.nnPre[k];
         if (S.flag[k] && S.surv[q]) continue;  // survivor: its column became a root
         const int t = upper_index(S.mo, cnt, k);
@@ -579,7 +677,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 
     // ---- parents' live lists: demote outputs with both rows <= tol / 2 --------
     if (isRoot) {  // the root's eigenvalues join the pool for the final sort
-        for (int c0 = 0; c0 < E; c0 += kLiveThreads) {
+        for (int c0 = 0; c0 < E; c0 += NT) {
             const int i = c0 + tid;
             pool_push(V, i < E, i < E ? S.oLam[i] : 0.0);
         }
@@ -589,7 +687,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
             const double theta = 0.5 * S.tol[t];
             int out = 0;
             double dl = 0.0, d0 = 0.0, d1 = 0.0;
-            for (int c0 = 0; c0 < Et; c0 += kLiveThreads) {
+            for (int c0 = 0; c0 < Et; c0 += NT) {
                 const int i = c0 + tid;
                 const bool valid = i < Et;
                 double v = 0.0, b0 = 0.0, b1 = 0.0;
@@ -603,7 +701,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
                     d1 = fmax(d1, fabs(b1));
                 }
                 int tot;
-                const int ex = block_exclusive_scan<kLiveThreads>(live ? 1 : 0, tot);
+                const int ex = block_exclusive_scan<NT>(live ? 1 : 0, tot);
                 if (live) {
                     const int p = base + out + ex;
                     w.lam[p] = v;
@@ -644,9 +742,12 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     }
 }
 
-// A CTA owns merges [blockIdx.x * G, +G) of the level and processes them in
-// batches of consecutive merges whose live inputs fit kLiveMax.
-__global__ void __launch_bounds__(kLiveThreads, 3)
+// A CTA owns merges [blockIdx.x * G, +G) and processes them in batches of
+// consecutive merges whose live inputs fit kLiveMax.  MODE 0: lane arithmetic
+// (256 threads), 1: split arithmetic, every merge > kSplitMinSize (one merge per
+// 1024-thread CTA: a warp per root / pole), 2: per merge (one merge per CTA).
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1)
 k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ traceOut, int G) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char live_raw[];
@@ -666,7 +767,12 @@ k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ t
         }
         __syncthreads();
         const int c = S.batch;
-        live_group(w, L, V, m, c, prm, traceOut, S);
+        if (MODE == 2) {
+            if (L.mSize[m] > kSplitMinSize) live_group<true, NT>(w, L, V, m, c, prm, traceOut, S);
+            else live_group<false, NT>(w, L, V, m, c, prm, traceOut, S);
+        } else {
+            live_group<MODE == 1, NT>(w, L, V, m, c, prm, traceOut, S);
+        }
         __syncthreads();
         m += c;
     }
@@ -817,11 +923,18 @@ void launch_live_init(cudaStream_t s, const Work& w, const LiveDev& V, const int
 
 void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
                        const SolveParams& prm, int* traceOut, int* launches, Prof* prof) {
-    // merges per CTA: a level of many merges packs up to kLiveGroup per CTA
-    // (a merge keeps K ~ 100 roots for 256 lanes), a few-merge level keeps one
-    const int per = std::max(1, std::min(kLiveGroup, L.M / (prm.sms * kLiveCtasPerSm)));
-    const int G = std::min(per, kLiveGroupMax);
-    launch_pdl(k_live_level, (L.M + G - 1) / G, kLiveThreads, sizeof(LiveSmem), s, w, L, V, prm, traceOut, G);
+    const size_t sm = sizeof(LiveSmem);
+    if (L.allSplit) {  // few large merges: one per CTA, a warp per root
+        launch_pdl(k_live_level<1, kLiveSplitThreads>, L.M, kLiveSplitThreads, sm, s, w, L, V, prm, traceOut, 1);
+    } else if (L.maxSize > kSplitMinSize) {  // both sides of the split rule (unbalanced tree)
+        launch_pdl(k_live_level<2, kLiveThreads>, L.M, kLiveThreads, sm, s, w, L, V, prm, traceOut, 1);
+    } else {
+        // merges per CTA: a level of many merges packs up to kLiveGroup per CTA
+        // (a merge keeps K ~ 100 roots for 256 lanes), a few-merge level keeps one
+        const int per = std::max(1, std::min(kLiveGroup, L.M / (prm.sms * kLiveCtasPerSm)));
+        const int G = std::min(per, kLiveGroupMax);
+        launch_pdl(k_live_level<0, kLiveThreads>, (L.M + G - 1) / G, kLiveThreads, sm, s, w, L, V, prm, traceOut, G);
+    }
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
@@ -841,7 +954,10 @@ int live_buckets(int n) { return n / 128 > 1 ? n / 128 : 1; }
 int live_max_elems() { return kLiveMax; }
 
 void init_live_attributes() {
-    cudaFuncSetAttribute(k_live_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LiveSmem));
+    const int sm = (int)sizeof(LiveSmem);
+    cudaFuncSetAttribute(k_live_level<0, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_level<1, kLiveSplitThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_level<2, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
 static_assert(sizeof(LiveSmem) <= 75 * 1024, "three live CTAs per SM");
