@@ -223,7 +223,9 @@ struct Handle {
     int subtree = 1;
     int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
     int live = 1;    // live-list top levels (BRGPU_OPT_LIVE)
-    int liveVeto = 0;  // order n whose last live-tier solve fell back (dense plans for it)
+    // live-tier fallback back-off: after a fallback at order liveVeto the next
+    // liveSkip solves of that order plan densely (8, doubling per repeated fallback)
+    int liveVeto = 0, liveSkip = 0, liveBackoff = 8;
     int strace = 0;  // secular-problem trace (brgpu_set_secular_trace): grid tier, dump per level
     double* strBuf = nullptr;  // per level 2n doubles (d, z) + rho per merge
     int64_t strCap = 0;
@@ -1221,7 +1223,12 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
     if (h->virt > 1) return solve_virtual(h, n, bstart, segs);
     Plan* p = h->plan.get();
     const bool sig = h->sig != nullptr;
-    const bool wantLive = !sig && h->live != 0 && !h->strace && h->subtree != 0 && h->liveVeto != n;
+    bool vetoed = false;
+    if (h->liveVeto == n && h->liveSkip > 0) {
+        vetoed = true;
+        --h->liveSkip;
+    }
+    const bool wantLive = !sig && h->live != 0 && !h->strace && h->subtree != 0 && !vetoed;
     if (!p || p->n != n || p->cutoff != h->leaf_cutoff || p->bstart != bstart || p->segs != segs ||
         p->sigma != sig || p->liveWanted != wantLive) {
         if (h->plan) free_plan(h->plan.get());
@@ -1347,9 +1354,12 @@ int finish_solve(Handle* h) {
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * kCounters, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
     if (lp && h->hsmall[2]) {  // the live tier could not prove this solve exact: redo it densely
+        h->liveBackoff = h->liveVeto == lp->n ? std::min(h->liveBackoff * 2, 1 << 16) : 8;
         h->liveVeto = lp->n;
+        h->liveSkip = h->liveBackoff + 1;  // + the retry itself
         return kRetryDense;
     }
+    if (lp && h->liveVeto == lp->n) h->liveBackoff = 8;  // the tier held at this order again
     if (h->virt <= 1) adapt_sparse(h, h->plan.get());
     {
         // both pairs are recorded on every path; a failure here must not leave a
@@ -1436,7 +1446,7 @@ int solve_device(Handle* h, int64_t n64, const double* d, const double* e, doubl
     else if (w_out != h->w.lam)
         CUDA_TRY(h, cudaMemcpyAsync(w_out, h->w.lam, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     r = finish_solve(h);
-    // the live tier fell back (liveVeto = n: the next plan is dense); inputs
+    // the live tier fell back (liveSkip: the next plans of this order are dense); inputs
     // staged in the workspace (brgpu_eigvals) are re-staged by the caller
     if (r == kRetryDense && d != h->w.D && e != h->w.Z) return solve_device(h, n64, d, e, w_out, w_host);
     return r;
@@ -1568,7 +1578,7 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
             return BRGPU_OK;
         case BRGPU_OPT_ROOT_SPLIT: set_plan_opt(h, h->root_split, v != 0); return BRGPU_OK;
         case BRGPU_OPT_SPARSE: set_plan_opt(h, h->sparse, v != 0); return BRGPU_OK;
-        case BRGPU_OPT_LIVE: set_plan_opt(h, h->live, v != 0); h->liveVeto = 0; return BRGPU_OK;
+        case BRGPU_OPT_LIVE: set_plan_opt(h, h->live, v != 0); h->liveVeto = h->liveSkip = 0; return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");

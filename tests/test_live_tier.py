@@ -30,30 +30,39 @@ def _live_ran(s, d, e) -> bool:
     return prof.get("live_level", (0.0, 0))[1] > 0
 
 
+@pytest.fixture(scope="module")
+def live_solver():
+    # its own handle: a shared one may be backing off the tier at an order where an
+    # earlier test's input fell back
+    s = br.Solver(0)
+    yield s
+    s.close()
+
+
 @pytest.mark.parametrize("fam,n", [("sym-uniform", 1 << 16), ("normal", 40000), ("uniform", 65537),
                                    ("sym-uniform", 131072)])
-def test_live_bitwise_vs_checker(solver, fam, n):
+def test_live_bitwise_vs_checker(live_solver, fam, n):
     d, e = G.generate(fam, n)
     ref = O.eigvals(d, e).w
     for _ in range(2):  # the second solve replays the captured graph
-        w = solver.eigvals(d, e)
+        w = live_solver.eigvals(d, e)
         assert np.array_equal(w.view(np.int64), ref.view(np.int64)), f"max diff {np.max(np.abs(w - ref)):.3e}"
-    assert _live_ran(solver, d, e)
+    assert _live_ran(live_solver, d, e)
 
 
 @pytest.mark.parametrize("fam,n", [("sym-uniform", 1 << 20), ("sym-uniform", 100003), ("normal", 300001),
                                    ("uniform", 1 << 18)])
-def test_live_matches_dense(solver, dense_solver, fam, n):
+def test_live_matches_dense(live_solver, dense_solver, fam, n):
     d, e = G.generate(fam, n)
-    solver.set_trace(True)
+    live_solver.set_trace(True)
     dense_solver.set_trace(True)
     try:
-        w1 = solver.eigvals(d, e)
-        t1 = solver.trace()
+        w1 = live_solver.eigvals(d, e)
+        t1 = live_solver.trace()
         w0 = dense_solver.eigvals(d, e)
         t0 = dense_solver.trace()
     finally:
-        solver.set_trace(False)
+        live_solver.set_trace(False)
         dense_solver.set_trace(False)
     assert np.array_equal(w1.view(np.int64), w0.view(np.int64))
     assert t1 == t0
@@ -68,18 +77,18 @@ def test_live_fallback_is_exact(fam, n, dense_solver):
     s = br.Solver(0)
     try:
         w_first = s.eigvals(d, e)  # host-buffer path: the input is re-staged for the retry
-        w_again = s.eigvals(d, e)
+        w_again = [s.eigvals(d, e) for _ in range(12)]  # dense back-off, then the tier is tried again
     finally:
         s.close()
     w0 = dense_solver.eigvals(d, e)
-    assert np.array_equal(w_first, w0) and np.array_equal(w_again, w0)
+    assert np.array_equal(w_first, w0) and all(np.array_equal(w, w0) for w in w_again)
 
 
-def test_live_device_path_and_option(solver):
+def test_live_device_path_and_option(live_solver):
     import torch
     d, e = G.generate("sym-uniform", 1 << 17)
     td, te = torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda")
-    w = solver.eigvals_device(td, te).cpu().numpy()
+    w = live_solver.eigvals_device(td, te).cpu().numpy()
     assert np.array_equal(w, O.eigvals(d, e).w)
     s = br.Solver(0, br.BrOptions(live=False))
     try:
@@ -89,10 +98,10 @@ def test_live_device_path_and_option(solver):
         s.close()
 
 
-def test_live_scaled_and_shifted(solver):
+def test_live_scaled_and_shifted(live_solver):
     # block scaling (|T| >> 1) and a shifted spectrum: the final sort sees the
     # scaled values (the rescale follows it)
     d, e = G.generate("sym-uniform", 1 << 16)
     for sc, sh in ((2.0 ** 40, 0.0), (1.0, 1e3), (2.0 ** -30, -5.0)):
         dd, ee = d * sc + sh, e * sc
-        assert np.array_equal(solver.eigvals(dd, ee), O.eigvals(dd, ee).w)
+        assert np.array_equal(live_solver.eigvals(dd, ee), O.eigvals(dd, ee).w)
