@@ -558,12 +558,22 @@ __global__ void __launch_bounds__(256) k_segment_walk(Work w, LevelDev L, int n,
             double dprev_nn = dp;
             int nmem = 0;
             bool done = false;
+            // two-stage prefetch: the next chunk's data and the chunk after's
+            // positions are in flight while this chunk replays (a long segment is
+            // then bound by the replay, not by dependent L2 round trips); loads
+            // ahead are safe: the walk only writes the survivors' Z / R0 / R1,
+            // which precede every entry still to come
+            int kc = hq + 1 + lane < hqe ? w.nnPos[hq + 1 + lane] : 0;
+            double d2 = 0.0, z2 = 0.0, x0 = 0.0, x1 = 0.0;
+            if (hq + 1 + lane < hqe) { d2 = w.D[kc]; z2 = w.Z[kc]; x0 = w.R0[kc]; x1 = w.R1[kc]; }
+            int kn = hq + 33 + lane < hqe ? w.nnPos[hq + 33 + lane] : 0;
             for (int cb = hq + 1; !done && cb < hqe; cb += 32) {
                 const int q2 = cb + lane;
-                const bool in = q2 < hqe;
-                const int k2 = in ? w.nnPos[q2] : 0;
-                double d2 = 0.0, z2 = 0.0, x0 = 0.0, x1 = 0.0;
-                if (in) { d2 = w.D[k2]; z2 = w.Z[k2]; x0 = w.R0[k2]; x1 = w.R1[k2]; }
+                const int k2 = kc;
+                const bool nin = cb + 32 + lane < hqe;
+                double nd = 0.0, nz = 0.0, nx0 = 0.0, nx1 = 0.0;
+                if (nin) { nd = w.D[kn]; nz = w.Z[kn]; nx0 = w.R0[kn]; nx1 = w.R1[kn]; }
+                const int knn = cb + 64 + lane < hqe ? w.nnPos[cb + 64 + lane] : 0;
                 const int cnt = min(32, hqe - cb);
                 int role = -1;  // this lane's entry: 0 member (prefix below), 1 group head
                 double mQ = 0.0, mS0 = 0.0, mS1 = 0.0;
@@ -597,6 +607,8 @@ __global__ void __launch_bounds__(256) k_segment_walk(Work w, LevelDev L, int n,
                 } else if (role == 1) {
                     w.survFlag[q2] = 1;
                 }
+                kc = kn; d2 = nd; z2 = nz; x0 = nx0; x1 = nx1;
+                kn = knn;
             }
             if (nmem && lane == 0) walk_retire(w, prev, Q, S0, S1);
         }
