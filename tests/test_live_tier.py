@@ -105,3 +105,31 @@ def test_live_scaled_and_shifted(live_solver):
     for sc, sh in ((2.0 ** 40, 0.0), (1.0, 1e3), (2.0 ** -30, -5.0)):
         dd, ee = d * sc + sh, e * sc
         assert np.array_equal(live_solver.eigvals(dd, ee), O.eigvals(dd, ee).w)
+
+
+def _special(kind, n, rng):
+    if kind == "graded":
+        return np.exp(-np.linspace(0, 30, n)) * rng.uniform(-1, 1, n), rng.uniform(-1, 1, n - 1) * 1e-3
+    if kind == "tiny-e":
+        return rng.uniform(-1, 1, n), rng.uniform(-1, 1, n - 1) * 1e-9
+    if kind == "repeated":
+        return np.round(rng.uniform(-1, 1, n), 2), rng.uniform(-1, 1, n - 1) * 0.3
+    if kind == "spikes":
+        d = rng.uniform(-1, 1, n)
+        d[::97] *= 1e6
+        return d, rng.uniform(-1, 1, n - 1)
+    return np.ones(n), rng.uniform(0.5, 1, n - 1)  # "ones": nothing deflates (fallback)
+
+
+@pytest.mark.parametrize("kind", ["graded", "tiny-e", "repeated", "spikes", "ones"])
+@pytest.mark.parametrize("n", [65536, 100001])
+def test_live_special_inputs_vs_checker(kind, n):
+    # graded / tiny-coupling / repeated / spiked / undeflatable inputs: whether the
+    # tier holds or falls back, the result is the checker's bit for bit
+    d, e = _special(kind, n, np.random.default_rng(11))
+    s = br.Solver(0)
+    try:
+        w = s.eigvals(d, e)
+    finally:
+        s.close()
+    assert np.array_equal(w.view(np.int64), O.eigvals(d, e).w.view(np.int64))
