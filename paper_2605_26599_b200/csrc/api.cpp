@@ -101,6 +101,14 @@ constexpr int kSpMinSpan = 16;        // smallest k_sp_solve group key span (gro
 #endif
 constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
 constexpr int kFuseMaxMergesHost = 128;
+// A fused level with fewer merges than this many per SM x SMs gives every merge
+// its own CTA (one merge's roots per 256 lanes instead of a group's) and runs as
+// its own launch: small solves are bound by the per-level latency of a CTA's
+// root queue (n = 4096: 8 CTAs for levels 1-5 as one run)
+#ifndef BRGPU_FEW_MERGES_PER_SM
+#define BRGPU_FEW_MERGES_PER_SM 1
+#endif
+constexpr int kFewMergesPerSm = BRGPU_FEW_MERGES_PER_SM;
 
 void init_kernel_attributes();
 void launch_sigma_leaves(cudaStream_t s, const SigmaDev& sg, int maxm, const int* taskOf, const int* tOff,
@@ -387,9 +395,10 @@ void add_levels(Plan* p, std::vector<NodeRec> nodes, bool fuse, std::vector<Leve
         L.G = 0;
         if (L.fused) {
             int q = 0;
+            const bool few = L.M < kFewMergesPerSm * p->sms;
             while (q < L.M) {
                 int c = 1, tot = p->mSize[L.m0 + q];
-                while (q + c < L.M && c < kFuseMaxMergesHost &&
+                while (!few && q + c < L.M && c < kFuseMaxMergesHost &&
                        p->mOff[L.m0 + q + c] == p->mOff[L.m0 + q + c - 1] + p->mSize[L.m0 + q + c - 1] &&
                        tot + p->mSize[L.m0 + q + c] <= L.cap) {
                     tot += p->mSize[L.m0 + q + c];
@@ -423,7 +432,8 @@ void plan_fused_runs(Plan* p) {
     while (i < lv.size()) {
         size_t j = i;
         while (j < lv.size() && lv[j].fused && lv[j].cap == kFuseSmallElems &&
-               (j == i || lv[j].level == lv[j - 1].level + 1) && j - i < (size_t)kMaxFusedRun)
+               (j == i || lv[j].level == lv[j - 1].level + 1) && j - i < (size_t)kMaxFusedRun &&
+               lv[j].M >= kFewMergesPerSm * p->sms)  // few-merge levels launch on their own
             ++j;
         if (j - i < 2) { i = std::max(j, i + 1); continue; }
         const LevelHost& top = lv[j - 1];

@@ -44,7 +44,10 @@
 namespace brgpu {
 
 constexpr int kLiveMax = 512;      // live elements of one merge (both children)
-constexpr int kLiveThreads = 256;
+#ifndef BRGPU_LIVE_THREADS
+#define BRGPU_LIVE_THREADS 256
+#endif
+constexpr int kLiveThreads = BRGPU_LIVE_THREADS;
 constexpr int kLiveInitThreads = 256;
 constexpr int kBucketCap = 4096;   // elements of one final-sort bucket (shared memory)
 constexpr int kBucketThreads = 256;
@@ -747,7 +750,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 // (256 threads), 1: split arithmetic, every merge > kSplitMinSize (one merge per
 // 1024-thread CTA: a warp per root / pole), 2: per merge (one merge per CTA).
 template <int MODE, int NT>
-__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1)
+__global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1)
 k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ traceOut, int G) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char live_raw[];
