@@ -81,6 +81,7 @@ void init_live_attributes();
 constexpr int kLiveMinSize = BRGPU_LIVE_MIN_SIZE;
 constexpr int kLiveMinN = 1 << 15;
 constexpr int kRetryDense = 1000;  // internal: the live tier fell back, redo the solve densely
+constexpr int kLiveBackoff0 = 64;  // dense solves of an order after its first live-tier fallback
 // work counters (Work::counters): [0,1] grid-tier evaluations / pole terms, [2,3]
 // fused tier, [4..7] phase cycles of profiling builds, [8,9] live tier
 constexpr int kCounters = 12;
@@ -232,8 +233,9 @@ struct Handle {
     int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
     int live = 1;    // live-list top levels (BRGPU_OPT_LIVE)
     // live-tier fallback back-off: after a fallback at order liveVeto the next
-    // liveSkip solves of that order plan densely (8, doubling per repeated fallback)
-    int liveVeto = 0, liveSkip = 0, liveBackoff = 8;
+    // liveSkip solves of that order plan densely (64, doubling per repeated fallback:
+    // a failed attempt costs ~40% of a solve, so inputs that never hold pay < 1%)
+    int liveVeto = 0, liveSkip = 0, liveBackoff = kLiveBackoff0;
     int strace = 0;  // secular-problem trace (brgpu_set_secular_trace): grid tier, dump per level
     double* strBuf = nullptr;  // per level 2n doubles (d, z) + rho per merge
     int64_t strCap = 0;
@@ -1364,12 +1366,12 @@ int finish_solve(Handle* h) {
     CUDA_TRY(h, cudaMemcpyAsync(h->hcnt, h->w.counters, sizeof(unsigned long long) * kCounters, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(h, cudaStreamSynchronize(s));
     if (lp && h->hsmall[2]) {  // the live tier could not prove this solve exact: redo it densely
-        h->liveBackoff = h->liveVeto == lp->n ? std::min(h->liveBackoff * 2, 1 << 16) : 8;
+        h->liveBackoff = h->liveVeto == lp->n ? std::min(h->liveBackoff * 2, 1 << 16) : kLiveBackoff0;
         h->liveVeto = lp->n;
         h->liveSkip = h->liveBackoff + 1;  // + the retry itself
         return kRetryDense;
     }
-    if (lp && h->liveVeto == lp->n) h->liveBackoff = 8;  // the tier held at this order again
+    if (lp && h->liveVeto == lp->n) h->liveBackoff = kLiveBackoff0;  // the tier held at this order again
     if (h->virt <= 1) adapt_sparse(h, h->plan.get());
     {
         // both pairs are recorded on every path; a failure here must not leave a
