@@ -70,6 +70,9 @@ void launch_live_init(cudaStream_t s, const Work& w, const LiveDev& V, const int
 void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
                        const SolveParams& prm, int* traceOut, int* launches, Prof* prof);
 void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int sms, int* launches, Prof* prof);
+void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
+                     int* launches, Prof* prof);
+int live_top_capacity(int sms);
 int live_buckets(int n);
 void init_live_attributes();
 // Live-list tier (live.cu): single-block solves of at least kLiveMinN elements
@@ -214,6 +217,9 @@ struct Plan {
     int* d_liveCtl = nullptr;
     unsigned long long* d_liveKeys = nullptr;
     int liveNb = 0;
+    int liveTop = -1;        // first level of the dataflow top run (k_live_top), -1: none
+    int liveTopMerges = 0;
+    int* d_liveDone = nullptr;
     cudaGraphExec_t graph = nullptr;
     bool graph_trace = false;
     uint64_t graph_gen = 0;
@@ -569,6 +575,32 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
             std::sort(front.begin(), front.end());
             for (auto& f : front) { p->liveFront.push_back(f.first); p->liveFront.push_back(f.second); }
             p->liveNb = live_buckets(n);
+            // dataflow top run: the longest tail of split-arithmetic levels that form
+            // a complete binary tree (merge m of level l = merges 2m, 2m+1 of l - 1)
+            // whose merges are all co-resident
+            const int cap = live_top_capacity(sms);
+            size_t t = p->levels.size();
+            int merges = 0;
+            while (t > li && p->levels.size() - t < (size_t)kMaxLiveTop) {
+                const LevelHost& lh = p->levels[t - 1];
+                if (lh.minSize <= kSplitMinSizeHost || merges + lh.M > cap) break;
+                if (t < p->levels.size()) {  // lh must be the complete child level of levels[t]
+                    const LevelHost& up = p->levels[t];
+                    bool ok = lh.M == 2 * up.M;
+                    for (int q = 0; ok && q < up.M; ++q) {
+                        const size_t a = (size_t)(up.m0 + q), c0 = (size_t)(lh.m0 + 2 * q), c1 = c0 + 1;
+                        ok = p->mOff[a] == p->mOff[c0] && p->mNL[a] == p->mSize[c0] &&
+                             p->mOff[c1] == p->mOff[a] + p->mNL[a] && p->mSize[c1] == p->mSize[a] - p->mNL[a];
+                    }
+                    if (!ok) break;
+                }
+                merges += lh.M;
+                --t;
+            }
+            if (p->levels.size() - t >= 2) {
+                p->liveTop = (int)t;
+                p->liveTopMerges = merges;
+            }
         }
     }
     // control words per level; phase-1 grid levels may run the sparse pipeline
@@ -656,6 +688,7 @@ int upload_plan(Handle* h, Plan* p) {
     const size_t oFront = put(p->liveFront);  // int2 pairs
     const size_t oLiveCtl = put(std::vector<int>(p->liveLev >= 0 ? 4 : 0, 0));
     const size_t oLiveKeys = put(std::vector<int>(p->liveLev >= 0 ? 4 : 0, 0));  // 2 u64 (16-byte aligned offsets)
+    const size_t oLiveDone = put(std::vector<int>((size_t)p->liveTopMerges, 0));
     if (anySp) CUDA_TRY(h, cudaMallocHost(&p->h_ctl, sizeof(int) * (size_t)p->nctl));
     p->devInts = buf.size();
     CUDA_TRY(h, cudaMalloc(&p->dev, sizeof(int) * std::max<size_t>(buf.size(), 1)));
@@ -675,6 +708,7 @@ int upload_plan(Handle* h, Plan* p) {
     p->d_liveFront = reinterpret_cast<int2*>(p->dev + oFront);
     p->d_liveCtl = p->dev + oLiveCtl;
     p->d_liveKeys = reinterpret_cast<unsigned long long*>(p->dev + oLiveKeys);
+    p->d_liveDone = p->dev + oLiveDone;
     return BRGPU_OK;
 }
 
@@ -916,6 +950,21 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
             if ((int)li == p->liveLev)
                 launch_live_init(s, h->w, V, p->d_liveFront, (int)p->liveFront.size() / 2, prm.tol_scale,
                                  launches, prof);
+            if (phase1 && (int)li == p->liveTop) {  // the rest of the tree as one dataflow launch
+                LiveRun R{};
+                R.nlev = (int)(levels.size() - li);
+                R.first[0] = 0;
+                for (int l = 0; l < R.nlev; ++l) {
+                    const LevelHost& ll = levels[li + (size_t)l];
+                    R.L[l] = level_dev(h, p, ll);
+                    R.trace[l] = h->trace ? h->traceBuf + 2 * ll.m0 : nullptr;
+                    R.first[l + 1] = R.first[l] + ll.M;
+                }
+                R.done = p->d_liveDone;
+                launch_live_top(s, h->w, R, V, prm, launches, prof);
+                launch_live_sort(s, V, n, h->w.lam, h->sms, launches, prof);
+                break;
+            }
             launch_level_live(s, h->w, L, V, prm, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
             if (li + 1 == levels.size()) launch_live_sort(s, V, n, h->w.lam, h->sms, launches, prof);
             continue;
@@ -957,6 +1006,7 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     const int nblk = (int)p->bstart.size() - 1;
     if (p->anySp) cudaMemsetAsync(p->d_ctl, 0, sizeof(int) * (size_t)p->nctl, s);  // level words (barrier counters)
     if (p->liveLev >= 0) cudaMemsetAsync(p->d_liveCtl, 0, sizeof(int) * 8, s);   // live words + key words
+    if (p->liveTopMerges) cudaMemsetAsync(p->d_liveDone, 0, sizeof(int) * (size_t)p->liveTopMerges, s);
     launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
                    p->d_cut, launches, prof);
     launch_leaves(s, (int)p->tOff.size(), p->maxLeaf, p->d_tOff, p->d_tSize, p->d_tFlags, h->w,

@@ -121,6 +121,18 @@ struct LiveDev {
     int nb;          // buckets of the final sort
 };
 
+// The top levels of the live tier as one dataflow launch (k_live_top): CTA b
+// solves merge b - first[l] of level l once its two children (merges of level
+// l - 1, or nodes completed before the launch) have set their done words.
+constexpr int kMaxLiveTop = 16;
+struct LiveRun {
+    LevelDev L[kMaxLiveTop];
+    int* trace[kMaxLiveTop];
+    int first[kMaxLiveTop + 1];  // CTA offset of each level
+    int nlev;
+    int* done;                   // one word per merge of the run (zeroed per solve)
+};
+
 // A run of consecutive fused levels launched as one kernel (k_levels_fused).
 constexpr int kMaxFusedRun = 8;
 struct FusedRun {

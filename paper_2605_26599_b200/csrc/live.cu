@@ -781,6 +781,33 @@ k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ t
     }
 }
 
+// The few-merge top levels as one launch: merges start when their children are
+// done instead of at level boundaries, so the critical path is the slowest chain
+// of merges rather than the sum of each level's slowest merge (one merge per
+// CTA, split arithmetic; the children of merge m of level l are merges 2m and
+// 2m + 1 of level l - 1 -- api.cpp checks the run is that complete binary
+// tree and that every CTA of the run is co-resident).
+__global__ void __launch_bounds__(kLiveSplitThreads, 1) k_live_top(Work w, LiveRun R, LiveDev V, SolveParams prm) {
+    pdl_entry();
+    extern __shared__ __align__(16) unsigned char live_raw[];
+    LiveSmem& S = *reinterpret_cast<LiveSmem*>(live_raw);
+    const int b = blockIdx.x;
+    const int l = upper_index(R.first, R.nlev, b);
+    const int m = b - R.first[l];
+    if (l > 0 && threadIdx.x == 0) {
+        const volatile int* c = R.done + R.first[l - 1] + 2 * m;
+        while (c[0] == 0 || c[1] == 0) __nanosleep(200);
+        __threadfence();
+    }
+    __syncthreads();
+    live_group<true, kLiveSplitThreads>(w, R.L[l], V, m, 1, prm, R.trace[l], S);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(R.done + b, 1);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Final order: bucket sort of the pool (n values).  Buckets split the value
 // range uniformly (a monotone bucket function, so concatenated buckets are in
@@ -942,6 +969,20 @@ void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const L
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
 
+void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
+                     int* launches, Prof* prof) {
+    launch_pdl(k_live_top, R.first[R.nlev], kLiveSplitThreads, sizeof(LiveSmem), s, w, R, V, prm);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
+}
+
+// co-resident CTAs of k_live_top (the run's merges must all fit at once)
+int live_top_capacity(int sms) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_live_top, kLiveSplitThreads, sizeof(LiveSmem));
+    return per * sms;
+}
+
 void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int sms, int* launches, Prof* prof) {
     const int g = sms * 4;
     launch_pdl(k_live_bounds, g, 256, 0, s, V, n);
@@ -961,6 +1002,7 @@ void init_live_attributes() {
     cudaFuncSetAttribute(k_live_level<0, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<1, kLiveSplitThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<2, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_top, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
 static_assert(sizeof(LiveSmem) <= 75 * 1024, "three live CTAs per SM");
