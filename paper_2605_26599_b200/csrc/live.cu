@@ -203,6 +203,7 @@ template <bool SPLIT, int NT>
 __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, const LiveDev& V, const int m0,
                                            const int cnt, const SolveParams& prm, int* __restrict__ traceOut,
                                            LiveSmem& S) {
+    static_assert(SPLIT || NT <= kLiveMax / 2, "lane mode: one double2 snapshot slot per thread in S.Z");
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
 #ifdef BRGPU_LIVE_PROF
