@@ -771,7 +771,7 @@ k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ t
         }
         __syncthreads();
         const int c = S.batch;
-        if (MODE == 2) {
+        if constexpr (MODE == 2) {
             if (L.mSize[m] > kSplitMinSize) live_group<true, NT>(w, L, V, m, c, prm, traceOut, S);
             else live_group<false, NT>(w, L, V, m, c, prm, traceOut, S);
         } else {
