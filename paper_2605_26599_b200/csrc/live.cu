@@ -996,7 +996,6 @@ void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int 
 }
 
 int live_buckets(int n) { return n / 128 > 1 ? n / 128 : 1; }
-int live_max_elems() { return kLiveMax; }
 
 void init_live_attributes() {
     const int sm = (int)sizeof(LiveSmem);
