@@ -116,9 +116,14 @@ struct LiveDev {
     double* tmp;     // bucket-sort scatter buffer (n)
     int* bcount;     // bucket counts (nb), bucket starts (nb + 1)
     int* bcur;       // bucket cursors (nb)
-    int* ctl;        // [0] pool fill, [1] fallback (redo the solve on the dense tiers)
+    int* ctl;        // [0] pool fill (one block), [1] fallback (redo the solve on the dense tiers)
     unsigned long long* keys;  // [0] ~min key, [1] max key of the pool (order-preserving)
     int nb;          // buckets of the final sort
+    // blocks (irreducible blocks / batch matrices): block b's pool is
+    // pool[bstart[b] ..), filled through bctr[b] (one block: bctr = ctl)
+    const int* bstart;
+    int nblk;
+    int* bctr;
 };
 
 // The top levels of the live tier as one dataflow launch (k_live_top): CTA b

@@ -87,6 +87,7 @@ struct LiveSmem {
     int me[kLiveGroup];        // live inputs
     int ml[kLiveGroup];        // ... of the left child
     int mb[kLiveGroup];        // first position of the merge
+    int mblk[kLiveGroup];      // its block (pool)
     int mnlF[kLiveGroup];      // left child's size
     int kS[kLiveGroup + 1];    // active ranges
     int ne[kLiveGroup + 1];    // merges with K > 0 before t (root queue order)
@@ -107,14 +108,24 @@ __device__ __forceinline__ double bitsd(unsigned long long b) { return __longlon
 
 __device__ __forceinline__ void live_fail(const LiveDev& V) { atomicExch(&V.ctl[1], 1); }
 
-// warp-aggregated append of v to the pool
-__device__ __forceinline__ void pool_push(const LiveDev& V, bool push, double v) {
+// block of position p (one block: 0)
+__device__ __forceinline__ int live_block(const LiveDev& V, int p) {
+    int lo = 0, hi = V.nblk;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (V.bstart[mid] <= p) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// warp-aggregated append of v to block blk's pool (blk uniform per warp)
+__device__ __forceinline__ void pool_push(const LiveDev& V, int blk, bool push, double v) {
     const unsigned m = __ballot_sync(0xffffffffu, push);
     if (!m) return;
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(m) - 1;
     int base = 0;
-    if (lane == leader) base = atomicAdd(&V.ctl[0], __popc(m));
+    if (lane == leader) base = V.bstart[blk] + atomicAdd(&V.bctr[blk], __popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (push) V.pool[base + __popc(m & ((1u << lane) - 1u))] = v;
 }
@@ -148,6 +159,7 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
         V.bcount[i] = 0;
     const int2 f = front[blockIdx.x];
     const int off = f.x, size = f.y;
+    const int blk = live_block(V, off);
     double mx = 0.0;
     for (int i = threadIdx.x; i < size; i += kLiveInitThreads) mx = fmax(mx, fabs(w.lam[off + i]));
     mx = block_max<kLiveInitThreads>(mx, s_red);
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
         }
         const bool live = valid && fmax(fabs(b0), fabs(b1)) > theta;
         const bool dead = valid && !live;
-        pool_push(V, dead, v);
+        pool_push(V, blk, dead, v);
         if (dead) {
             dl = fmax(dl, fabs(v));
             d0 = fmax(d0, fabs(b0));
@@ -228,6 +240,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         const int base = L.mOff[m], nlF = L.mNL[m];
         const int cl = V.cnt[base], cr = V.cnt[base + nlF];
         S.mb[tid] = base;
+        S.mblk[tid] = live_block(V, base);
         S.mnlF[tid] = nlF;
         S.ml[tid] = cl;
         S.me[tid] = cl + cr;
@@ -680,11 +693,12 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     __syncthreads();
 
     // ---- parents' live lists: demote outputs with both rows <= tol / 2 --------
-    if (isRoot) {  // the root's eigenvalues join the pool for the final sort
-        for (int c0 = 0; c0 < E; c0 += NT) {
-            const int i = c0 + tid;
-            pool_push(V, i < E, i < E ? S.oLam[i] : 0.0);
-        }
+    if (isRoot) {  // the roots' eigenvalues join their blocks' pools for the final sort
+        for (int t = 0; t < cnt; ++t)
+            for (int c0 = 0; c0 < S.me[t]; c0 += NT) {
+                const int i = c0 + tid;
+                pool_push(V, S.mblk[t], i < S.me[t], i < S.me[t] ? S.oLam[S.mo[t] + i] : 0.0);
+            }
     } else {
         for (int t = 0; t < cnt; ++t) {
             const int off = S.mo[t], Et = S.me[t], base = S.mb[t];
@@ -698,7 +712,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
                 if (valid) { v = S.oLam[off + i]; b0 = S.oR0[off + i]; b1 = S.oR1[off + i]; }
                 const bool live = valid && fmax(fabs(b0), fabs(b1)) > theta;
                 const bool dead = valid && !live;
-                pool_push(V, dead, v);
+                pool_push(V, S.mblk[t], dead, v);
                 if (dead) {
                     dl = fmax(dl, fabs(v));
                     d0 = fmax(d0, fabs(b0));
@@ -942,6 +956,43 @@ __global__ void __launch_bounds__(kBucketThreads) k_live_bucket(LiveDev V, doubl
     }
 }
 
+// Several blocks (a batch): every live block (<= kBucketCap elements) is sorted
+// from its own pool by one CTA -- a bitonic network over order-preserving 64-bit
+// keys in shared memory (padded to a power of two with +inf); a pool that did
+// not fill its block is a fallback.
+__global__ void __launch_bounds__(kBucketThreads) k_live_blocksort(LiveDev V, const int* __restrict__ blocks,
+                                                                   double* __restrict__ out) {
+    pdl_entry();
+    if (V.ctl[1]) return;
+    __shared__ unsigned long long s_k[kBucketCap];
+    const int b = blocks[blockIdx.x];
+    const int start = V.bstart[b], cnt = V.bstart[b + 1] - start;
+    if (V.bctr[b] != cnt) {
+        if (threadIdx.x == 0) live_fail(V);
+        return;
+    }
+    int P = 1;
+    while (P < cnt) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += kBucketThreads) s_k[i] = i < cnt ? okey(V.pool[start + i]) : ~0ULL;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < P / 2; t += kBucketThreads) {
+                const int i = 2 * t - (t & (j - 1));  // lower index of the pair (i, i + j)
+                const int q = i + j;
+                const bool up = (i & k) == 0;
+                const unsigned long long a = s_k[i], c = s_k[q];
+                if ((a > c) == up) {
+                    s_k[i] = c;
+                    s_k[q] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < cnt; i += kBucketThreads) out[start + i] = okey_val(s_k[i]);
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
@@ -996,6 +1047,14 @@ void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int 
 }
 
 int live_buckets(int n) { return n / 128 > 1 ? n / 128 : 1; }
+int live_block_cap() { return kBucketCap; }
+
+void launch_live_blocksort(cudaStream_t s, const LiveDev& V, const int* blocks, int nlive, double* out,
+                           int* launches, Prof* prof) {
+    launch_pdl(k_live_blocksort, nlive, kBucketThreads, 0, s, V, blocks, out);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE_SORT);
+}
 
 void init_live_attributes() {
     const int sm = (int)sizeof(LiveSmem);

@@ -133,3 +133,41 @@ def test_live_special_inputs_vs_checker(kind, n):
     finally:
         s.close()
     assert np.array_equal(w.view(np.int64), O.eigvals(d, e).w.view(np.int64))
+
+
+def test_live_batch_blocks_vs_checker():
+    # a batch of 64 matrices of 4096: every block's three top levels are live and each
+    # block is sorted by its own CTA at the end
+    import torch
+    rng = np.random.default_rng(3)
+    batch, n = 64, 4096
+    d = rng.uniform(-1, 1, (batch, n))
+    e = rng.uniform(-1, 1, (batch, n - 1))
+    s = br.Solver(0)
+    try:
+        w = s.eigvals_batched(d, e)
+        prof = s.profile_kernels(torch.tensor(d, device="cuda"), torch.tensor(e, device="cuda"), batch)
+    finally:
+        s.close()
+    ref = O.eigvals_batched(d.reshape(-1), e.reshape(-1), batch, n)
+    assert np.array_equal(np.asarray(w).reshape(-1).view(np.int64), np.asarray(ref).reshape(-1).view(np.int64))
+    assert prof.get("live_level", (0.0, 0))[1] > 0
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_live_natural_blocks_vs_checker(big):
+    # natural splits (zero couplings) into blocks of <= 4096, or with one block too large
+    # for the per-block sort (the tier then stays off): the checker's result either way
+    rng = np.random.default_rng(4)
+    n = 1 << 17
+    d, e = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n - 1)
+    cuts = np.arange(4096, n, 4096) - 1
+    if big:
+        cuts = cuts[cuts > 3 * 4096]
+    e[cuts] = 0.0
+    s = br.Solver(0)
+    try:
+        w = s.eigvals(d, e)
+    finally:
+        s.close()
+    assert np.array_equal(w.view(np.int64), O.eigvals(d, e).w.view(np.int64))
