@@ -13,6 +13,6 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 $NCU --metrics $M -c 600 --csv --log-file $O/launches_c5.csv python tools/ncu_solve.py --reps 2 > $O/launches_c5.log 2>&1
 F="$NCU --set full --import-source on"
 $F -k regex:"k_live_level" -s 0 -c 1 -o $O/live_first python tools/ncu_solve.py --reps 1 > $O/live1.log 2>&1
-$F -k regex:"k_live_level" -s 6 -c 1 -o $O/live_top python tools/ncu_solve.py --reps 1 > $O/live2.log 2>&1
+$F -k regex:"k_live_top" -c 1 -o $O/live_top python tools/ncu_solve.py --reps 1 > $O/live2.log 2>&1
 $F -k regex:"k_live_init|k_live_bucket|k_live_scatter" -c 3 -o $O/live_aux python tools/ncu_solve.py --reps 1 > $O/live3.log 2>&1
 ls -la $O
