@@ -484,6 +484,7 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
     double tau = 0.5 * (lo + hi);
     int converged = 0;
     for (int iter = 0; iter < 400; ++iter) {
+        double pole_tau = NAN;
         ev_t ev;
         if (reuse) {
             ev = mid_ev;
@@ -524,18 +525,29 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
             if (nslow >= 2) {
                 const double rest = ev.f + worg / tau;
                 if (tau > 0.0 && ev.f > 0.0 && rest > 4.0 * ftol) {
-                    const double bnd = 0.5 * (worg / rest);
+                    const double q = worg / rest;
+                    const double bnd = 0.5 * q;
                     if (bnd > lo && bnd < tau) lo = bnd;
+                    pole_tau = q;
                 } else if (tau < 0.0 && ev.f < 0.0 && rest < -4.0 * ftol) {
-                    const double bnd = 0.5 * (worg / rest);
+                    const double q = worg / rest;
+                    const double bnd = 0.5 * q;
                     if (bnd < hi && bnd > tau) hi = bnd;
+                    pole_tau = q;
                 }
             }
             if (slow && !last) swtch = !swtch;
             prevf = ev.f;
         }
         double tau_next = NAN;
-        const int geo_step = nslow >= 2 && geo_ok(lo, hi);
+        /* GPU arithmetic, pole step: after the origin bound applied, a root three
+         * orders of magnitude closer to the origin pole than the iterate is taken
+         * from the pole-dominant model f ~ rest + worg/(-t) (root worg/rest), not
+         * halved towards it geometrically (random 2^17: the slowest root per merge
+         * 7.90 -> 7.35 evaluations; eigenvalues within 1e-16 relative) */
+        const int pstep = !ref && isfinite(pole_tau) && pole_tau > lo && pole_tau < hi && pole_tau != tau &&
+                          fabs(pole_tau) < 1e-3 * fabs(tau);
+        const int geo_step = pstep || (nslow >= 2 && geo_ok(lo, hi));
 #ifndef BRO_NO_LAST_GUESS
         /* GPU arithmetic, the last root's start (dlaed4's case i = n): its first
          * iterate is the bracket midpoint, often far from the root; the first
@@ -556,7 +568,9 @@ static int solve_root_impl(int k, const double* d, const double* z, double rho, 
             }
         }
 #endif
-        if (nslow >= 2 && geo_ok(lo, hi)) {
+        if (pstep) {
+            tau_next = pole_tau;
+        } else if (nslow >= 2 && geo_ok(lo, hi)) {
             tau_next = geo_mid(lo, hi);
         } else
         if (iter == 0 && gmode) {
