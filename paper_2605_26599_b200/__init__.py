@@ -137,6 +137,7 @@ class BrOptions:
     root_split: bool = True  # multi-rank: split the shared top merges' roots across ranks
     sparse: bool = False  # opt-in: grid levels with <= C non-negligible poles per merge run the sparse pipeline
     live: bool = True  # top levels of large single-block solves on live lists (live.cu); dense fallback
+    live_cluster: bool = True  # split-rule live levels: one merge per thread-block cluster (live.cu)
 
 
 @dataclass
@@ -232,6 +233,9 @@ class Solver:
         if not o.live or getattr(self, "_live_off", False):  # default on: set only once turned off
             self._opt(_native.OPT_LIVE, int(o.live))
             self._live_off = not o.live
+        if not o.live_cluster or getattr(self, "_cl_off", False):  # default on: set only once turned off
+            self._opt(_native.OPT_LIVE_CLUSTER, int(o.live_cluster))
+            self._cl_off = not o.live_cluster
         if self.nranks == 1:
             self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o

@@ -24,6 +24,7 @@ OPT_EXACT_PASSES = 7
 OPT_ROOT_SPLIT = 8
 OPT_SPARSE = 9
 OPT_LIVE = 10
+OPT_LIVE_CLUSTER = 11
 
 
 class Stats(C.Structure):

@@ -73,6 +73,10 @@ void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int 
 void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
                      int* launches, Prof* prof);
 int live_top_capacity(int sms);
+int live_cluster_max(int device);
+int live_cluster_size(int M, int sms, int cmax);
+void launch_level_live_cluster(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
+                               const SolveParams& prm, int* traceOut, int C, int* launches, Prof* prof);
 int live_block_cap();
 void launch_live_blocksort(cudaStream_t s, const LiveDev& V, const int* blocks, int nlive, double* out,
                            int* launches, Prof* prof);
@@ -225,6 +229,7 @@ struct Plan {
     int* d_liveBctr = nullptr;    // per-block pool counters (several blocks)
     int liveTop = -1;        // first level of the dataflow top run (k_live_top), -1: none
     int liveTopMerges = 0;
+    int liveCl = 1;          // > 1: split-rule live levels run one merge per cluster of up to liveCl CTAs
     int* d_liveDone = nullptr;
     cudaGraphExec_t graph = nullptr;
     bool graph_trace = false;
@@ -244,6 +249,7 @@ struct Handle {
     int subtree = 1;
     int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
     int live = 1;    // live-list top levels (BRGPU_OPT_LIVE)
+    int liveCluster = 1;  // split-rule live levels on thread-block clusters (BRGPU_OPT_LIVE_CLUSTER)
     // live-tier fallback back-off: after a fallback at order liveVeto the next
     // liveSkip solves of that order plan densely (64, doubling per repeated fallback:
     // a failed attempt costs ~40% of a solve, so inputs that never hold pay < 1%)
@@ -490,7 +496,7 @@ void plan_fused_runs(Plan* p) {
 // subtree; smaller blocks go to ranks in contiguous chunks of the total size.
 std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
                                 const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0,
-                                int sms = 148, bool sparse = false, bool live = false) {
+                                int sms = 148, bool sparse = false, bool live = false, int liveCl = 1) {
     auto p = std::make_unique<Plan>();
     p->n = n;
     p->sms = sms;
@@ -608,7 +614,8 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
             // dataflow top run: the longest tail of split-arithmetic levels that form
             // a complete binary tree (merge m of level l = merges 2m, 2m+1 of l - 1)
             // whose merges are all co-resident
-            const int cap = live_top_capacity(sms);
+            p->liveCl = liveCl;
+            const int cap = liveCl > 1 ? 0 : live_top_capacity(sms);  // clusters replace the dataflow run
             size_t t = p->levels.size();
             int merges = 0;
             while (t > li && p->levels.size() - t < (size_t)kMaxLiveTop) {
@@ -1011,7 +1018,12 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
                 live_final_sort(h, p, V, launches, prof);
                 break;
             }
-            launch_level_live(s, h->w, L, V, prm, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
+            const int C = L.allSplit && p->liveCl > 1 ? live_cluster_size(lh.M, h->sms, p->liveCl) : 1;
+            if (C > 1)
+                launch_level_live_cluster(s, h->w, L, V, prm, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, C,
+                                          launches, prof);
+            else
+                launch_level_live(s, h->w, L, V, prm, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, launches, prof);
             if (li + 1 == levels.size()) live_final_sort(h, p, V, launches, prof);
             continue;
         }
@@ -1342,7 +1354,8 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
         p->sigma != sig || p->liveWanted != wantLive) {
         if (h->plan) free_plan(h->plan.get());
         h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0 && !h->strace, h->nranks,
-                            h->rank, h->sms, !sig && h->sparse != 0 && !h->strace, wantLive);
+                            h->rank, h->sms, !sig && h->sparse != 0 && !h->strace, wantLive,
+                            h->liveCluster ? live_cluster_max(h->device) : 1);
         p = h->plan.get();
         if (sig) {  // every merge propagates the requested rows: no root-only mode
             p->sigma = true;
@@ -1688,6 +1701,7 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
         case BRGPU_OPT_ROOT_SPLIT: set_plan_opt(h, h->root_split, v != 0); return BRGPU_OK;
         case BRGPU_OPT_SPARSE: set_plan_opt(h, h->sparse, v != 0); return BRGPU_OK;
         case BRGPU_OPT_LIVE: set_plan_opt(h, h->live, v != 0); h->liveVeto = h->liveSkip = 0; return BRGPU_OK;
+        case BRGPU_OPT_LIVE_CLUSTER: set_plan_opt(h, h->liveCluster, v != 0); return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -1711,6 +1725,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_EXACT_PASSES: *v = h->exact; return BRGPU_OK;
         case BRGPU_OPT_SPARSE: *v = h->sparse; return BRGPU_OK;
         case BRGPU_OPT_LIVE: *v = h->live; return BRGPU_OK;
+        case BRGPU_OPT_LIVE_CLUSTER: *v = h->liveCluster; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }
 }

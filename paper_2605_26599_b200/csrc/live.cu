@@ -41,6 +41,10 @@
 #include "numerics.cuh"
 #include "grid_common.cuh"
 
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
 namespace brgpu {
 
 constexpr int kLiveMax = 512;      // live elements of one merge (both children)
@@ -211,13 +215,29 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
 // up to G merges and cuts them into batches greedily, so one CTA's 256 lanes
 // hold the roots of several merges of K ~ 100.
 // ---------------------------------------------------------------------------
-template <bool SPLIT, int NT>
+//
+// CLU: one merge per thread-block CLUSTER (k_live_cluster; split arithmetic):
+// every CTA of the cluster runs the deflation on its own copy of the inputs
+// (same operations, same results), then the CTAs share the roots, refreshed
+// weights and boundary rows by index (CTA r of C takes root queue entries
+// r, r + C, ...; warp slices for the weights and rows) and publish each result
+// into every CTA's shared memory over DSMEM, a cluster barrier per phase; CTA 0
+// writes the parent.  Every root / weight / row is computed by the same code on
+// the same shared-memory operands, so the results are bitwise those of one CTA.
+template <bool SPLIT, int NT, bool CLU = false>
 __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, const LiveDev& V, const int m0,
                                            const int cnt, const SolveParams& prm, int* __restrict__ traceOut,
                                            LiveSmem& S) {
     static_assert(SPLIT || NT <= kLiveMax / 2, "lane mode: one double2 snapshot slot per thread in S.Z");
+    static_assert(!CLU || SPLIT, "cluster mode runs the split arithmetic");
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
+    // cluster rank / size (1 CTA: 0 / 1)
+    int crank = 0, csize = 1;
+    if constexpr (CLU) {
+        crank = (int)cg::this_cluster().block_rank();
+        csize = (int)cg::this_cluster().num_blocks();
+    }
 #ifdef BRGPU_LIVE_PROF
     // phase cycles of the few-merge (latency-bound) levels, summed over CTAs in
     // counters[4..7]: deflation / secular / refreshed weights / rows + output
@@ -225,7 +245,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 #define LIVE_MARK(k)                                                                          \
     do {                                                                                      \
         __syncthreads();                                                                      \
-        if (tid == 0 && gridDim.x <= 64) {                                                    \
+        if (tid == 0 && (CLU ? crank == 0 : gridDim.x <= 64)) {                               \
             const long long t_ = clock64();                                                   \
             atomicAdd(&w.counters[4 + (k)], (unsigned long long)(t_ - ph_t));                 \
             ph_t = t_;                                                                        \
@@ -268,7 +288,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         int o = 0;
         for (int t = 0; t < cnt; ++t) { S.mo[t] = o; o += S.me[t]; }
         S.mo[cnt] = o;
-        S.bail = *(volatile int*)&V.ctl[1] != 0 || o > kLiveMax;
+        S.bail = (!CLU && *(volatile int*)&V.ctl[1] != 0) || o > kLiveMax;
         if (o > kLiveMax) live_fail(V);
     }
     __syncthreads();
@@ -450,7 +470,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         unsigned long long ev = 0, tm = 0;
         for (;;) {
             int q = 0;
-            if (lane == 0) q = atomicAdd(&S.next, 1);
+            if (lane == 0) q = atomicAdd(&S.next, 1) * csize + crank;
             q = __shfl_sync(0xffffffffu, q, 0);
             if (q >= T) break;
             const int g = qorder[q];
@@ -460,7 +480,12 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
             double tu;
             root_warp(pairs + ks, zA + ks, K, g - ks, S.rho[t], w.exact != 0, prm.patched != 0, w.status, o, tu,
                       ev, tm);
-            if (lane == 0) {
+            if constexpr (CLU) {
+                if (lane < csize) {  // lane r publishes into CTA r's shared memory
+                    *cg::this_cluster().map_shared_rank(&S.org[g], lane) = o;
+                    *cg::this_cluster().map_shared_rank(&S.tau[g], lane) = tu;
+                }
+            } else if (lane == 0) {
                 S.org[g] = o;
                 S.tau[g] = tu;
             }
@@ -526,7 +551,8 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
             atomicAdd(&w.counters[9], terms);
         }
     }
-    __syncthreads();
+    if constexpr (CLU) cg::this_cluster().sync();
+    else __syncthreads();
 
     double* sDorg = S.Z;  // d[origin] per root (S.Z is dead after the compaction)
     for (int g = tid; g < T; g += NT) sDorg[g] = pairs[S.kS[upper_index(S.kS, cnt, g)] + S.org[g]].x;
@@ -535,7 +561,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 
     // ---- Gu-Eisenstat refreshed weights (non-root merges, K > 1) -------------
     if (prm.zhat && !isRoot && SPLIT) {  // warp per pole: lane-strided products + butterfly (k_zhat_warp)
-        for (int g = wid; g < T; g += NT / 32) {
+        for (int g = wid + crank * (NT / 32); g < T; g += csize * (NT / 32)) {
             const int t = upper_index(S.kS, cnt, g);
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
             if (K == 1) continue;  // a lone pole keeps its z (the checker refreshes only K > 1)
@@ -554,12 +580,17 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
                 }
             }
             const double W = bfly_mul(prod);
-            if (lane == 0) {
-                const double mag = sqrt(fmax(0.0, -W));
-                zA[g] = zA[g] >= 0.0 ? mag : -mag;
+            const double mag = sqrt(fmax(0.0, -W));
+            const double zh = zA[g] >= 0.0 ? mag : -mag;
+            __syncwarp();
+            if constexpr (CLU) {
+                if (lane < csize) *cg::this_cluster().map_shared_rank(&zA[g], lane) = zh;
+            } else if (lane == 0) {
+                zA[g] = zh;
             }
         }
-        __syncthreads();
+        if constexpr (CLU) cg::this_cluster().sync();
+        else __syncthreads();
     } else if (prm.zhat && !isRoot) {
         for (int g = tid; g < T; g += NT) {
             const int t = upper_index(S.kS, cnt, g);
@@ -591,7 +622,16 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 
     // ---- roots: position in the parent's live order + boundary rows ----------
     if (SPLIT) {  // warp per root: lane-strided sums + butterflies (k_rows_warp)
-        for (int g = wid; g < T; g += NT / 32) {
+        // (cluster: CTA r's warp slice; every result goes to CTA 0's shared memory)
+        double* oLam = S.oLam;
+        double* oR0 = S.oR0;
+        double* oR1 = S.oR1;
+        if constexpr (CLU) {
+            oLam = cg::this_cluster().map_shared_rank(S.oLam, 0);
+            oR0 = cg::this_cluster().map_shared_rank(S.oR0, 0);
+            oR1 = cg::this_cluster().map_shared_rank(S.oR1, 0);
+        }
+        for (int g = wid + crank * (NT / 32); g < T; g += csize * (NT / 32)) {
             const int t = upper_index(S.kS, cnt, g);
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
             const int off = S.mo[t];
@@ -603,7 +643,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
                 if (!(lam < pairs[ks + mid].x)) lo = mid + 1; else hi = mid;
             }
             const int p = off + j + count_leq(S.D + off, S.me[t], lam) - lo;
-            if (lane == 0) S.oLam[p] = lam;
+            if (lane == 0) oLam[p] = lam;
             if (isRoot) continue;
             double nn = 0.0, s0 = 0.0, s1 = 0.0;
             if (!w.exact && eval_guard(SmemPairs{pairs + ks}, K, j, dorg, tau)) {
@@ -628,8 +668,8 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
             const double NNs = bfly_add(nn), S0 = bfly_add(s0), S1 = bfly_add(s1);
             if (lane == 0) {
                 const double inv = 1.0 / sqrt(NNs);
-                S.oR0[p] = S0 * inv;
-                S.oR1[p] = S1 * inv;
+                oR0[p] = S0 * inv;
+                oR1[p] = S1 * inv;
             }
         }
     } else
@@ -673,7 +713,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         S.oR1[p] = s1 * inv;
     }
     // deflated live elements: t + #{roots < D}
-    for (int k = tid; k < E; k += NT) {
+    for (int k = tid; k < (crank == 0 ? E : 0); k += NT) {
         const int q = S.nnPre[k];
         if (S.flag[k] && S.surv[q]) continue;  // survivor: its column became a root
         const int t = upper_index(S.mo, cnt, k);
@@ -690,7 +730,12 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
         S.oR0[off + tt + lo] = S.R0[k];
         S.oR1[off + tt + lo] = S.R1[k];
     }
-    __syncthreads();
+    if constexpr (CLU) {
+        cg::this_cluster().sync();  // every output is in CTA 0's shared memory; no DSMEM access after this
+        if (crank != 0) return;
+    } else {
+        __syncthreads();
+    }
 
     // ---- parents' live lists: demote outputs with both rows <= tol / 2 --------
     if (isRoot) {  // the roots' eigenvalues join their blocks' pools for the final sort
@@ -821,6 +866,20 @@ __global__ void __launch_bounds__(kLiveSplitThreads, 1) k_live_top(Work w, LiveR
         __threadfence();
         atomicExch(R.done + b, 1);
     }
+}
+
+// A few-merge split-rule level with one merge per thread-block cluster of C CTAs
+// on C SMs (cluster size chosen per launch): a merge's ~100-200 roots then run
+// at ~one root per warp instead of ~5 per warp on one SM, whose FP64 pipe the
+// split arithmetic (bracket / model replicated on 32 lanes) saturates.
+__global__ void __launch_bounds__(kLiveSplitThreads, 1) k_live_cluster(Work w, LevelDev L, LiveDev V, SolveParams prm,
+                                                                       int* __restrict__ traceOut) {
+    pdl_entry();
+    extern __shared__ __align__(16) unsigned char live_raw[];
+    LiveSmem& S = *reinterpret_cast<LiveSmem*>(live_raw);
+    cg::this_cluster().sync();  // every CTA of the cluster runs before any DSMEM store
+    const int m = (int)(blockIdx.x / cg::this_cluster().num_blocks());
+    live_group<true, kLiveSplitThreads, true>(w, L, V, m, 1, prm, traceOut, S);
 }
 
 // ---------------------------------------------------------------------------
@@ -1028,6 +1087,64 @@ void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const Live
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
 
+// cluster size of a split-rule live level of M merges: ~all SMs, a power of two
+// the device can co-schedule (live_cluster_max(), probed once per device)
+static int g_cluster_max[64];
+int live_cluster_max(int device) {
+    if (device < 0 || device >= 64) return 1;
+    if (g_cluster_max[device]) return g_cluster_max[device];
+    int best = 1;
+    cudaFuncSetAttribute(k_live_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c = 2; c <= 16; c *= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(c);
+        cfg.blockDim = dim3(kLiveSplitThreads);
+        cfg.dynamicSmemBytes = sizeof(LiveSmem);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k_live_cluster, &cfg) != cudaSuccess || nc < 1) {
+            cudaGetLastError();
+            break;
+        }
+        best = c;
+    }
+    g_cluster_max[device] = best;
+    return best;
+}
+
+int live_cluster_size(int M, int sms, int cmax) {
+    int c = 1;
+    while (c * 2 <= cmax && (c * 2) * M <= sms) c *= 2;
+    return c;
+}
+
+void launch_level_live_cluster(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
+                               const SolveParams& prm, int* traceOut, int C, int* launches, Prof* prof) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.M * C);
+    cfg.blockDim = dim3(kLiveSplitThreads);
+    cfg.dynamicSmemBytes = sizeof(LiveSmem);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = C;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, k_live_cluster, w, L, V, prm, traceOut);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
+}
+
 // co-resident CTAs of k_live_top (the run's merges must all fit at once)
 int live_top_capacity(int sms) {
     int per = 0;
@@ -1062,6 +1179,8 @@ void init_live_attributes() {
     cudaFuncSetAttribute(k_live_level<1, kLiveSplitThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<2, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_top, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
 static_assert(sizeof(LiveSmem) <= 75 * 1024, "three live CTAs per SM");

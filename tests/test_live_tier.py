@@ -171,3 +171,29 @@ def test_live_natural_blocks_vs_checker(big):
     finally:
         s.close()
     assert np.array_equal(w.view(np.int64), O.eigvals(d, e).w.view(np.int64))
+
+
+@pytest.mark.parametrize("fam,n", [("sym-uniform", 1 << 20), ("normal", 300001), ("uniform", 1 << 17),
+                                   ("sym-uniform", 70001)])
+def test_live_cluster_matches_single_cta(live_solver, fam, n):
+    # split-rule live levels on thread-block clusters (one merge per cluster, roots /
+    # weights / rows shared over DSMEM) against one merge per CTA with the dataflow
+    # top run: bit-identical eigenvalues and per-merge (nn, K) traces
+    d, e = G.generate(fam, n)
+    s = br.Solver(0, br.BrOptions(live_cluster=False))
+    live_solver.set_trace(True)
+    s.set_trace(True)
+    try:
+        w1 = live_solver.eigvals(d, e)
+        t1 = live_solver.trace()
+        w0 = s.eigvals(d, e)
+        t0 = s.trace()
+        import ctypes
+        v = ctypes.c_int64(-1)
+        assert s._lib.brgpu_get_option(s._h, 11, ctypes.byref(v)) == 0 and v.value == 0
+        assert live_solver._lib.brgpu_get_option(live_solver._h, 11, ctypes.byref(v)) == 0 and v.value == 1
+    finally:
+        live_solver.set_trace(False)
+        s.close()
+    assert np.array_equal(w1.view(np.int64), w0.view(np.int64))
+    assert t1 == t0
