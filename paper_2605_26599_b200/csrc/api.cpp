@@ -74,7 +74,7 @@ void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const Live
                      int* launches, Prof* prof);
 int live_top_capacity(int sms);
 int live_cluster_max(int device);
-int live_cluster_size(int M, int sms, int cmax);
+int live_cluster_size(int device, int M, int cmax);
 void launch_level_live_cluster(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
                                const SolveParams& prm, int* traceOut, int C, int* launches, Prof* prof);
 int live_block_cap();
@@ -1018,7 +1018,7 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
                 live_final_sort(h, p, V, launches, prof);
                 break;
             }
-            const int C = L.allSplit && p->liveCl > 1 ? live_cluster_size(lh.M, h->sms, p->liveCl) : 1;
+            const int C = L.allSplit && p->liveCl > 1 ? live_cluster_size(h->device, lh.M, p->liveCl) : 1;
             if (C > 1)
                 launch_level_live_cluster(s, h->w, L, V, prm, h->trace ? h->traceBuf + 2 * lh.m0 : nullptr, C,
                                           launches, prof);

@@ -224,12 +224,15 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
 // into every CTA's shared memory over DSMEM, a cluster barrier per phase; CTA 0
 // writes the parent.  Every root / weight / row is computed by the same code on
 // the same shared-memory operands, so the results are bitwise those of one CTA.
-template <bool SPLIT, int NT, bool CLU = false>
+// LPR < 32: the split arithmetic on groups of LPR lanes (LaneGroup, numerics.cuh;
+// bitwise the warp-per-root form), 32 / LPR roots / poles per warp.
+template <bool SPLIT, int NT, bool CLU = false, int LPR = 32>
 __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, const LiveDev& V, const int m0,
                                            const int cnt, const SolveParams& prm, int* __restrict__ traceOut,
                                            LiveSmem& S) {
     static_assert(SPLIT || NT <= kLiveMax / 2, "lane mode: one double2 snapshot slot per thread in S.Z");
     static_assert(!CLU || SPLIT, "cluster mode runs the split arithmetic");
+    static_assert(LPR == 32 || SPLIT, "lane groups run the split arithmetic");
     const int tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     // cluster rank / size (1 CTA: 0 / 1)
@@ -466,7 +469,72 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     LIVE_MARK(0);
 
     // ---- secular roots ---------------------------------------------------------
-    if (SPLIT) {  // warp per root, 32-way split arithmetic (k_secular_warp), warp queue
+    if (SPLIT && LPR < 32) {  // a lane group per root, group queue
+        const LaneGroup<LPR> G;
+        RootSM st;
+        int g = -1, ks = 0;
+        bool exhausted = false;
+        unsigned long long ev = 0, tm = 0;
+        for (;;) {
+            while (g < 0 && !exhausted) {
+                int q = 0;
+                if (G.gl == 0) q = atomicAdd(&S.next, 1) * csize + crank;
+                q = __shfl_sync(G.mask, q, G.base);
+                if (q >= T) { exhausted = true; break; }
+                g = qorder[q];
+                const int t = upper_index(S.kS, cnt, g);
+                ks = S.kS[t];
+                const int K = S.kS[t + 1] - ks, j = g - ks;
+                const double2* P = pairs + ks;
+                const double zsq = (j == K - 1 && K > 1) ? grp_zsq(G, P, K) : 0.0;
+                rs_begin_zsq(st, K, j, S.rho[t], PolesPairs{P}, zA[ks], zsq, P[K - 1].y);
+                if (st.phase == kRsDone) {
+                    if constexpr (CLU) {
+                        for (int rr = G.gl; rr < csize; rr += LPR) {
+                            *cg::this_cluster().map_shared_rank(&S.org[g], rr) = st.org;
+                            *cg::this_cluster().map_shared_rank(&S.tau[g], rr) = st.tau;
+                        }
+                    } else if (G.gl == 0) {
+                        S.org[g] = st.org;
+                        S.tau[g] = st.tau;
+                    }
+                    g = -1;
+                }
+            }
+            if (!__any_sync(0xffffffffu, g >= 0)) break;
+            if (g >= 0) {
+                const double2* P = pairs + ks;
+                const Ev e = grp_eval(G, P, st, w.exact != 0);
+                if (G.gl == 0) {
+                    ++ev;
+                    tm += (unsigned long long)st.K;
+                }
+                rs_consume(st, e, PolesPairs{P}, Z2Pairs{P}, prm.patched != 0);
+                if (st.phase == kRsDone || st.phase == kRsFail) {
+                    if (st.phase == kRsFail && G.gl == 0) set_status(w.status, BRGPU_ERR_NO_CONVERGENCE);
+                    if constexpr (CLU) {
+                        for (int rr = G.gl; rr < csize; rr += LPR) {
+                            *cg::this_cluster().map_shared_rank(&S.org[g], rr) = st.org;
+                            *cg::this_cluster().map_shared_rank(&S.tau[g], rr) = st.tau;
+                        }
+                    } else if (G.gl == 0) {
+                        S.org[g] = st.org;
+                        S.tau[g] = st.tau;
+                    }
+                    g = -1;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ev += __shfl_xor_sync(0xffffffffu, ev, o);
+            tm += __shfl_xor_sync(0xffffffffu, tm, o);
+        }
+        if (lane == 0 && ev) {
+            atomicAdd(&w.counters[8], ev);
+            atomicAdd(&w.counters[9], tm);
+        }
+    } else if (SPLIT) {  // warp per root, 32-way split arithmetic (k_secular_warp), warp queue
         unsigned long long ev = 0, tm = 0;
         for (;;) {
             int q = 0;
@@ -560,7 +628,26 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     LIVE_MARK(1);
 
     // ---- Gu-Eisenstat refreshed weights (non-root merges, K > 1) -------------
-    if (prm.zhat && !isRoot && SPLIT) {  // warp per pole: lane-strided products + butterfly (k_zhat_warp)
+    if (prm.zhat && !isRoot && SPLIT && LPR < 32) {  // a lane group per pole
+        const LaneGroup<LPR> G;
+        constexpr int GPW = 32 / LPR;  // groups per warp
+        for (int g = (crank * (NT / 32) + wid) * GPW + lane / LPR; g < T; g += csize * (NT / LPR)) {
+            const int t = upper_index(S.kS, cnt, g);
+            const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
+            if (K == 1) continue;  // a lone pole keeps its z (the checker refreshes only K > 1)
+            const double W = grp_zhat_prod(G, pairs + ks, sDorg + ks, S.tau + ks, K, i, w.exact != 0);
+            const double mag = sqrt(fmax(0.0, -W));
+            const double zh = zA[g] >= 0.0 ? mag : -mag;
+            __syncwarp(G.mask);
+            if constexpr (CLU) {
+                for (int rr = G.gl; rr < csize; rr += LPR) *cg::this_cluster().map_shared_rank(&zA[g], rr) = zh;
+            } else if (G.gl == 0) {
+                zA[g] = zh;
+            }
+        }
+        if constexpr (CLU) cg::this_cluster().sync();
+        else __syncthreads();
+    } else if (prm.zhat && !isRoot && SPLIT) {  // warp per pole: lane-strided products + butterfly (k_zhat_warp)
         for (int g = wid + crank * (NT / 32); g < T; g += csize * (NT / 32)) {
             const int t = upper_index(S.kS, cnt, g);
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, i = g - ks;
@@ -631,7 +718,8 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
             oR0 = cg::this_cluster().map_shared_rank(S.oR0, 0);
             oR1 = cg::this_cluster().map_shared_rank(S.oR1, 0);
         }
-        for (int g = wid + crank * (NT / 32); g < T; g += csize * (NT / 32)) {
+        const LaneGroup<LPR> G;
+        for (int g = (crank * (NT / 32) + wid) * (32 / LPR) + lane / LPR; g < T; g += csize * (NT / LPR)) {
             const int t = upper_index(S.kS, cnt, g);
             const int ks = S.kS[t], K = S.kS[t + 1] - ks, j = g - ks;
             const int off = S.mo[t];
@@ -643,8 +731,20 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
                 if (!(lam < pairs[ks + mid].x)) lo = mid + 1; else hi = mid;
             }
             const int p = off + j + count_leq(S.D + off, S.me[t], lam) - lo;
-            if (lane == 0) oLam[p] = lam;
+            if (G.gl == 0) oLam[p] = lam;
             if (isRoot) continue;
+            if constexpr (LPR < 32) {
+                double NNs, S0, S1;
+                if (!grp_rows(G, pairs + ks, zA + ks, S.r0A + ks, S.r1A + ks, K, j, dorg, tau, w.exact != 0, NNs, S0,
+                              S1) && G.gl == 0)
+                    set_status(w.status, BRGPU_ERR_ZERO_DENOMINATOR);
+                if (G.gl == 0) {
+                    const double inv = 1.0 / sqrt(NNs);
+                    oR0[p] = S0 * inv;
+                    oR1[p] = S1 * inv;
+                }
+                continue;
+            }
             double nn = 0.0, s0 = 0.0, s1 = 0.0;
             if (!w.exact && eval_guard(SmemPairs{pairs + ks}, K, j, dorg, tau)) {
                 for (int i = lane; i < K; i += 32) {
@@ -805,10 +905,22 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
     }
 }
 
+// Split-rule levels: NT threads per cluster CTA, LPR lanes per root / pole / row
+// (LaneGroup; 16 measured best against 8, 32 and 4 at C5).
+#ifndef BRGPU_CLUSTER_THREADS
+#define BRGPU_CLUSTER_THREADS 512
+#endif
+#ifndef BRGPU_CLUSTER_LPR
+#define BRGPU_CLUSTER_LPR 16
+#endif
+constexpr int kClThreads = BRGPU_CLUSTER_THREADS;
+constexpr int kClLpr = BRGPU_CLUSTER_LPR;
+
 // A CTA owns merges [blockIdx.x * G, +G) and processes them in batches of
 // consecutive merges whose live inputs fit kLiveMax.  MODE 0: lane arithmetic
 // (256 threads), 1: split arithmetic, every merge > kSplitMinSize (one merge per
-// 1024-thread CTA: a warp per root / pole), 2: per merge (one merge per CTA).
+// 1024-thread CTA: a warp per root / pole), 2: per merge (one merge per CTA),
+// 3: split arithmetic on lane groups (many-merge split-rule levels, G merges per CTA).
 template <int MODE, int NT>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 3 : 1)
 k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ traceOut, int G) {
@@ -833,6 +945,8 @@ k_live_level(Work w, LevelDev L, LiveDev V, SolveParams prm, int* __restrict__ t
         if constexpr (MODE == 2) {
             if (L.mSize[m] > kSplitMinSize) live_group<true, NT>(w, L, V, m, c, prm, traceOut, S);
             else live_group<false, NT>(w, L, V, m, c, prm, traceOut, S);
+        } else if constexpr (MODE == 3) {
+            live_group<true, NT, false, kClLpr>(w, L, V, m, c, prm, traceOut, S);
         } else {
             live_group<MODE == 1, NT>(w, L, V, m, c, prm, traceOut, S);
         }
@@ -872,14 +986,15 @@ __global__ void __launch_bounds__(kLiveSplitThreads, 1) k_live_top(Work w, LiveR
 // on C SMs (cluster size chosen per launch): a merge's ~100-200 roots then run
 // at ~one root per warp instead of ~5 per warp on one SM, whose FP64 pipe the
 // split arithmetic (bracket / model replicated on 32 lanes) saturates.
-__global__ void __launch_bounds__(kLiveSplitThreads, 1) k_live_cluster(Work w, LevelDev L, LiveDev V, SolveParams prm,
-                                                                       int* __restrict__ traceOut) {
+template <int NT, int LPR>
+__global__ void __launch_bounds__(NT, 1) k_live_cluster(Work w, LevelDev L, LiveDev V, SolveParams prm,
+                                                        int* __restrict__ traceOut) {
     pdl_entry();
     extern __shared__ __align__(16) unsigned char live_raw[];
     LiveSmem& S = *reinterpret_cast<LiveSmem*>(live_raw);
     cg::this_cluster().sync();  // every CTA of the cluster runs before any DSMEM store
     const int m = (int)(blockIdx.x / cg::this_cluster().num_blocks());
-    live_group<true, kLiveSplitThreads, true>(w, L, V, m, 1, prm, traceOut, S);
+    live_group<true, NT, true, LPR>(w, L, V, m, 1, prm, traceOut, S);
 }
 
 // ---------------------------------------------------------------------------
@@ -1065,7 +1180,11 @@ void launch_live_init(cudaStream_t s, const Work& w, const LiveDev& V, const int
 void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
                        const SolveParams& prm, int* traceOut, int* launches, Prof* prof) {
     const size_t sm = sizeof(LiveSmem);
-    if (L.allSplit) {  // few large merges: one per CTA, a warp per root
+    if (L.allSplit && L.M > prm.sms) {  // many split-rule merges: lane groups, G merges per CTA
+        const int per = std::max(1, std::min(kLiveGroup, L.M / (prm.sms * kLiveCtasPerSm)));
+        const int G = std::min(per, kLiveGroupMax);
+        launch_pdl(k_live_level<3, kLiveThreads>, (L.M + G - 1) / G, kLiveThreads, sm, s, w, L, V, prm, traceOut, G);
+    } else if (L.allSplit) {  // few large merges: one per CTA, a warp per root
         launch_pdl(k_live_level<1, kLiveSplitThreads>, L.M, kLiveSplitThreads, sm, s, w, L, V, prm, traceOut, 1);
     } else if (L.maxSize > kSplitMinSize) {  // both sides of the split rule (unbalanced tree)
         launch_pdl(k_live_level<2, kLiveThreads>, L.M, kLiveThreads, sm, s, w, L, V, prm, traceOut, 1);
@@ -1087,40 +1206,50 @@ void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const Live
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
 
-// cluster size of a split-rule live level of M merges: ~all SMs, a power of two
-// the device can co-schedule (live_cluster_max(), probed once per device)
-static int g_cluster_max[64];
+// cluster size of a split-rule live level of M merges: the largest power of two
+// c <= 16 for which all M clusters are co-resident (cudaOccupancyMaxActiveClusters:
+// a cluster must fit one GPC, so 16 clusters of 8 need not fit 148 SMs) -- a
+// second wave would double the level's time.  Probed once per device.
+static int g_cluster_active[64][5];  // [device][log2 c]: co-resident clusters of c CTAs (0: unprobed)
+static bool g_cluster_probed[64];
 int live_cluster_max(int device) {
     if (device < 0 || device >= 64) return 1;
-    if (g_cluster_max[device]) return g_cluster_max[device];
-    int best = 1;
-    cudaFuncSetAttribute(k_live_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int c = 2; c <= 16; c *= 2) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(c);
-        cfg.blockDim = dim3(kLiveSplitThreads);
-        cfg.dynamicSmemBytes = sizeof(LiveSmem);
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = c;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, k_live_cluster, &cfg) != cudaSuccess || nc < 1) {
-            cudaGetLastError();
-            break;
+    if (!g_cluster_probed[device]) {
+        cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(LiveSmem));
+        for (int l = 1; l <= 4; ++l) {
+            const int c = 1 << l;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(c);
+            cfg.blockDim = dim3(kClThreads);
+            cfg.dynamicSmemBytes = sizeof(LiveSmem);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = c;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, k_live_cluster<kClThreads, kClLpr>, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                nc = 0;
+            }
+            g_cluster_active[device][l] = nc;
         }
-        best = c;
+        g_cluster_probed[device] = true;
     }
-    g_cluster_max[device] = best;
+    int best = 1;
+    for (int l = 1; l <= 4; ++l)
+        if (g_cluster_active[device][l] > 0) best = 1 << l;
     return best;
 }
 
-int live_cluster_size(int M, int sms, int cmax) {
+int live_cluster_size(int device, int M, int cmax) {
     int c = 1;
-    while (c * 2 <= cmax && (c * 2) * M <= sms) c *= 2;
+    for (int l = 1; l <= 4 && (1 << l) <= cmax; ++l)
+        if (device >= 0 && device < 64 && M <= g_cluster_active[device][l]) c = 1 << l;
     return c;
 }
 
@@ -1128,7 +1257,7 @@ void launch_level_live_cluster(cudaStream_t s, const Work& w, const LevelDev& L,
                                const SolveParams& prm, int* traceOut, int C, int* launches, Prof* prof) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(L.M * C);
-    cfg.blockDim = dim3(kLiveSplitThreads);
+    cfg.blockDim = dim3(kClThreads);
     cfg.dynamicSmemBytes = sizeof(LiveSmem);
     cfg.stream = s;
     cudaLaunchAttribute at[2];
@@ -1140,7 +1269,7 @@ void launch_level_live_cluster(cudaStream_t s, const Work& w, const LevelDev& L,
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, k_live_cluster, w, L, V, prm, traceOut);
+    cudaLaunchKernelEx(&cfg, k_live_cluster<kClThreads, kClLpr>, w, L, V, prm, traceOut);
     *launches += 1;
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
@@ -1178,9 +1307,10 @@ void init_live_attributes() {
     cudaFuncSetAttribute(k_live_level<0, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<1, kLiveSplitThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<2, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_level<3, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_top, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_live_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_live_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
 static_assert(sizeof(LiveSmem) <= 75 * 1024, "three live CTAs per SM");
