@@ -197,3 +197,15 @@ def test_live_cluster_matches_single_cta(live_solver, fam, n):
         s.close()
     assert np.array_equal(w1.view(np.int64), w0.view(np.int64))
     assert t1 == t0
+
+
+def test_live_many_split_merges_vs_checker(live_solver):
+    # n ~ 3M: the first split-rule live level has ~180 merges (> SMs), which run
+    # on lane groups with G merges per CTA (k_live_level MODE 3), the few-merge
+    # levels above it on clusters -- bit-identical to the checker
+    n = 3_000_017
+    d, e = G.generate("sym-uniform", n)
+    ref = O.eigvals(d, e).w
+    w = live_solver.eigvals(d, e)
+    assert np.array_equal(w.view(np.int64), ref.view(np.int64)), f"max diff {np.max(np.abs(w - ref)):.3e}"
+    assert _live_ran(live_solver, d, e)
