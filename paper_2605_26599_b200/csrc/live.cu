@@ -226,6 +226,19 @@ __global__ void __launch_bounds__(kLiveInitThreads) k_live_init(Work w, LiveDev 
 // the same shared-memory operands, so the results are bitwise those of one CTA.
 // LPR < 32: the split arithmetic on groups of LPR lanes (LaneGroup, numerics.cuh;
 // bitwise the warp-per-root form), 32 / LPR roots / poles per warp.
+#ifdef BRGPU_LIVE_PROF
+// CTAs whose phase cycles are recorded: cluster rank 0 of the split-rule levels
+// and one-CTA few-merge levels (or, with -DBRGPU_LIVE_PROF_ONLY=G, only the
+// levels launched on G CTAs)
+__device__ __forceinline__ bool live_prof_cta(bool clu, int crank) {
+#ifdef BRGPU_LIVE_PROF_ONLY
+    return !clu && gridDim.x == BRGPU_LIVE_PROF_ONLY;
+#else
+    return clu ? crank == 0 : gridDim.x <= 64;
+#endif
+}
+#endif
+
 template <bool SPLIT, int NT, bool CLU = false, int LPR = 32>
 __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, const LiveDev& V, const int m0,
                                            const int cnt, const SolveParams& prm, int* __restrict__ traceOut,
@@ -248,7 +261,7 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 #define LIVE_MARK(k)                                                                          \
     do {                                                                                      \
         __syncthreads();                                                                      \
-        if (tid == 0 && (CLU ? crank == 0 : gridDim.x <= 64)) {                               \
+        if (tid == 0 && live_prof_cta(CLU, crank)) {                                          \
             const long long t_ = clock64();                                                   \
             atomicAdd(&w.counters[4 + (k)], (unsigned long long)(t_ - ph_t));                 \
             ph_t = t_;                                                                        \
@@ -915,6 +928,10 @@ __device__ __forceinline__ void live_group(const Work& w, const LevelDev& L, con
 #endif
 constexpr int kClThreads = BRGPU_CLUSTER_THREADS;
 constexpr int kClLpr = BRGPU_CLUSTER_LPR;
+#ifndef BRGPU_LIVE_M3_THREADS
+#define BRGPU_LIVE_M3_THREADS 256
+#endif
+constexpr int kLiveM3Threads = BRGPU_LIVE_M3_THREADS;  // many-merge split levels (MODE 3)
 
 // A CTA owns merges [blockIdx.x * G, +G) and processes them in batches of
 // consecutive merges whose live inputs fit kLiveMax.  MODE 0: lane arithmetic
@@ -1183,7 +1200,7 @@ void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const L
     if (L.allSplit && L.M > prm.sms) {  // many split-rule merges: lane groups, G merges per CTA
         const int per = std::max(1, std::min(kLiveGroup, L.M / (prm.sms * kLiveCtasPerSm)));
         const int G = std::min(per, kLiveGroupMax);
-        launch_pdl(k_live_level<3, kLiveThreads>, (L.M + G - 1) / G, kLiveThreads, sm, s, w, L, V, prm, traceOut, G);
+        launch_pdl(k_live_level<3, kLiveM3Threads>, (L.M + G - 1) / G, kLiveM3Threads, sm, s, w, L, V, prm, traceOut, G);
     } else if (L.allSplit) {  // few large merges: one per CTA, a warp per root
         launch_pdl(k_live_level<1, kLiveSplitThreads>, L.M, kLiveSplitThreads, sm, s, w, L, V, prm, traceOut, 1);
     } else if (L.maxSize > kSplitMinSize) {  // both sides of the split rule (unbalanced tree)
@@ -1307,7 +1324,7 @@ void init_live_attributes() {
     cudaFuncSetAttribute(k_live_level<0, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<1, kLiveSplitThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<2, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_live_level<3, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_level<3, kLiveM3Threads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_top, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -11,6 +11,6 @@ for _ in range(2):
     s.eigvals_device(td, te)
 cyc = (C.c_uint64 * 4)()
 s._lib.brgpu_phase_cycles(s._h, cyc)
-ctas = 64 + 32 + 16 + 8 + 4 + 2 + 1
-print("per-CTA avg cycles (levels with <= 64 merges):",
+ctas = int(sys.argv[1]) if len(sys.argv) > 1 else 64 + 32 + 16 + 8 + 4 + 2 + 1
+print(f"per-CTA avg cycles over {ctas} CTAs:",
       {k: round(v / ctas) for k, v in zip(["deflation", "secular", "zhat", "rows+out"], cyc)})
