@@ -138,6 +138,7 @@ class BrOptions:
     sparse: bool = False  # opt-in: grid levels with <= C non-negligible poles per merge run the sparse pipeline
     live: bool = True  # top levels of large single-block solves on live lists (live.cu); dense fallback
     live_cluster: bool = True  # split-rule live levels: one merge per thread-block cluster (live.cu)
+    live_flow: bool = True  # lane-arithmetic live levels as one dataflow launch (live.cu)
 
 
 @dataclass
@@ -236,6 +237,9 @@ class Solver:
         if not o.live_cluster or getattr(self, "_cl_off", False):  # default on: set only once turned off
             self._opt(_native.OPT_LIVE_CLUSTER, int(o.live_cluster))
             self._cl_off = not o.live_cluster
+        if not o.live_flow or getattr(self, "_lf_off", False):  # default on: set only once turned off
+            self._opt(_native.OPT_LIVE_FLOW, int(o.live_flow))
+            self._lf_off = not o.live_flow
         if self.nranks == 1:
             self._opt(_native.OPT_VIRTUAL_RANKS, int(o.virtual_ranks))
         self.options = o

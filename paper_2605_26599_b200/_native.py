@@ -25,6 +25,7 @@ OPT_ROOT_SPLIT = 8
 OPT_SPARSE = 9
 OPT_LIVE = 10
 OPT_LIVE_CLUSTER = 11
+OPT_LIVE_FLOW = 12
 
 
 class Stats(C.Structure):

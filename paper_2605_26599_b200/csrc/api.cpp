@@ -73,6 +73,9 @@ void launch_live_sort(cudaStream_t s, const LiveDev& V, int n, double* out, int 
 void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
                      int* launches, Prof* prof);
 int live_top_capacity(int sms);
+int live_lane_group(int M, int sms);
+void launch_live_flow(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
+                      int* launches, Prof* prof);
 int live_cluster_max(int device);
 int live_cluster_size(int device, int M, int cmax);
 void launch_level_live_cluster(cudaStream_t s, const Work& w, const LevelDev& L, const LiveDev& V,
@@ -110,6 +113,10 @@ constexpr int kSpMinSpan = 16;        // smallest k_sp_solve group key span (gro
 #ifndef BRGPU_SPLIT_MIN_SIZE
 #define BRGPU_SPLIT_MIN_SIZE 8192
 #endif
+#ifndef BRGPU_LIVE_FLOW_GMAX
+#define BRGPU_LIVE_FLOW_GMAX 4
+#endif
+constexpr int kLiveFlowGMax = BRGPU_LIVE_FLOW_GMAX;  // merges per dataflow work item (cap)
 constexpr int kSplitMinSizeHost = BRGPU_SPLIT_MIN_SIZE;  // == kSplitMinSize (numerics.cuh): warp-per-root merges
 constexpr int kFuseMaxMergesHost = 128;
 // A fused level with fewer merges than this many per SM x SMs gives every merge
@@ -230,6 +237,11 @@ struct Plan {
     int liveTop = -1;        // first level of the dataflow top run (k_live_top), -1: none
     int liveTopMerges = 0;
     int liveCl = 1;          // > 1: split-rule live levels run one merge per cluster of up to liveCl CTAs
+    int liveFlow = -1, liveFlowLevels = 0;  // lane-mode live levels as one dataflow launch (k_live_flow)
+    std::vector<int> liveFlowItems;         // int4 (level in run, first merge, merges, 0)
+    int liveFlowMerges = 0;
+    int* d_liveFlowItems = nullptr;
+    int* d_liveFlowDone = nullptr;          // flowMerges done words + the ticket
     int* d_liveDone = nullptr;
     cudaGraphExec_t graph = nullptr;
     bool graph_trace = false;
@@ -250,6 +262,7 @@ struct Handle {
     int sparse = 0;  // sparse grid-tier levels (BRGPU_OPT_SPARSE; opt-in)
     int live = 1;    // live-list top levels (BRGPU_OPT_LIVE)
     int liveCluster = 1;  // split-rule live levels on thread-block clusters (BRGPU_OPT_LIVE_CLUSTER)
+    int liveFlow = 1;     // lane-mode live levels as one dataflow launch (BRGPU_OPT_LIVE_FLOW)
     // live-tier fallback back-off: after a fallback at order liveVeto the next
     // liveSkip solves of that order plan densely (64, doubling per repeated fallback:
     // a failed attempt costs ~40% of a solve, so inputs that never hold pay < 1%)
@@ -496,7 +509,8 @@ void plan_fused_runs(Plan* p) {
 // subtree; smaller blocks go to ranks in contiguous chunks of the total size.
 std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstart,
                                 const std::vector<int>& segs, bool fuse, int nranks = 1, int rank = 0,
-                                int sms = 148, bool sparse = false, bool live = false, int liveCl = 1) {
+                                int sms = 148, bool sparse = false, bool live = false, int liveCl = 1,
+                                bool liveFlowOn = false) {
     auto p = std::make_unique<Plan>();
     p->n = n;
     p->sms = sms;
@@ -615,6 +629,39 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
             // a complete binary tree (merge m of level l = merges 2m, 2m+1 of l - 1)
             // whose merges are all co-resident
             p->liveCl = liveCl;
+            // lane-mode dataflow run: the live levels from the tier's first level
+            // up to the split rule, each the complete binary child level of the next
+            if (liveFlowOn) {
+                size_t t = li;
+                while (t < p->levels.size() && p->levels[t].maxSize <= kSplitMinSizeHost && t - li < (size_t)kMaxLiveTop) {
+                    if (t > li) {
+                        const LevelHost& lo = p->levels[t - 1];
+                        const LevelHost& up = p->levels[t];
+                        bool ok = lo.M == 2 * up.M;
+                        for (int q = 0; ok && q < up.M; ++q) {
+                            const size_t a = (size_t)(up.m0 + q), c0 = (size_t)(lo.m0 + 2 * q), c1 = c0 + 1;
+                            ok = p->mOff[a] == p->mOff[c0] && p->mNL[a] == p->mSize[c0] &&
+                                 p->mOff[c1] == p->mOff[a] + p->mNL[a] && p->mSize[c1] == p->mSize[a] - p->mNL[a];
+                        }
+                        if (!ok) break;
+                    }
+                    ++t;
+                }
+                if (t - li >= 2) {
+                    p->liveFlow = (int)li;
+                    p->liveFlowLevels = (int)(t - li);
+                    for (size_t l = li; l < t; ++l) {
+                        const int M = p->levels[l].M, G = std::min(live_lane_group(M, sms), kLiveFlowGMax);
+                        for (int m = 0; m < M; m += G) {
+                            p->liveFlowItems.push_back((int)(l - li));
+                            p->liveFlowItems.push_back(m);
+                            p->liveFlowItems.push_back(std::min(G, M - m));
+                            p->liveFlowItems.push_back(0);
+                        }
+                        p->liveFlowMerges += M;
+                    }
+                }
+            }
             const int cap = liveCl > 1 ? 0 : live_top_capacity(sms);  // clusters replace the dataflow run
             size_t t = p->levels.size();
             int merges = 0;
@@ -726,6 +773,8 @@ int upload_plan(Handle* h, Plan* p) {
     const size_t oLiveCtl = put(std::vector<int>(p->liveLev >= 0 ? 4 : 0, 0));
     const size_t oLiveKeys = put(std::vector<int>(p->liveLev >= 0 ? 4 : 0, 0));  // 2 u64 (16-byte aligned offsets)
     const size_t oLiveDone = put(std::vector<int>((size_t)p->liveTopMerges, 0));
+    const size_t oFlowItems = put(p->liveFlowItems);  // int4: 16-byte aligned offsets
+    const size_t oFlowDone = put(std::vector<int>(p->liveFlowMerges ? (size_t)p->liveFlowMerges + 1 : 0, 0));
     const size_t oLiveBlocks = put(p->liveBlocks);
     const size_t oLiveBctr = put(std::vector<int>(p->liveBlocks.empty() ? 0 : p->bstart.size(), 0));
     if (anySp) CUDA_TRY(h, cudaMallocHost(&p->h_ctl, sizeof(int) * (size_t)p->nctl));
@@ -748,6 +797,8 @@ int upload_plan(Handle* h, Plan* p) {
     p->d_liveCtl = p->dev + oLiveCtl;
     p->d_liveKeys = reinterpret_cast<unsigned long long*>(p->dev + oLiveKeys);
     p->d_liveDone = p->dev + oLiveDone;
+    p->d_liveFlowItems = p->dev + oFlowItems;
+    p->d_liveFlowDone = p->dev + oFlowDone;
     p->d_liveBlocks = p->dev + oLiveBlocks;
     p->d_liveBctr = p->dev + oLiveBctr;
     return BRGPU_OK;
@@ -1003,6 +1054,25 @@ void run_levels(Handle* h, Plan* p, const std::vector<LevelHost>& levels, int* l
             if ((int)li == p->liveLev)
                 launch_live_init(s, h->w, V, p->d_liveFront, (int)p->liveFront.size() / 2, prm.tol_scale,
                                  launches, prof);
+            if (phase1 && (int)li == p->liveFlow) {  // lane-mode live levels as one dataflow launch
+                LiveRun R{};
+                R.nlev = p->liveFlowLevels;
+                R.first[0] = 0;
+                for (int l = 0; l < R.nlev; ++l) {
+                    const LevelHost& ll = levels[li + (size_t)l];
+                    R.L[l] = level_dev(h, p, ll, l ? &levels[li + (size_t)l - 1] : prev);
+                    R.trace[l] = h->trace ? h->traceBuf + 2 * ll.m0 : nullptr;
+                    R.first[l + 1] = R.first[l] + ll.M;
+                }
+                R.done = p->d_liveFlowDone;
+                R.ticket = p->d_liveFlowDone + p->liveFlowMerges;
+                R.items = reinterpret_cast<const int4*>(p->d_liveFlowItems);
+                R.nitems = (int)p->liveFlowItems.size() / 4;
+                launch_live_flow(s, h->w, R, V, prm, launches, prof);
+                li += (size_t)R.nlev - 1;
+                if (li + 1 == levels.size()) live_final_sort(h, p, V, launches, prof);
+                continue;
+            }
             if (phase1 && (int)li == p->liveTop) {  // the rest of the tree as one dataflow launch
                 LiveRun R{};
                 R.nlev = (int)(levels.size() - li);
@@ -1065,6 +1135,8 @@ void run_stage_a(Handle* h, Plan* p, int* launches, Prof* prof) {
     if (p->anySp) cudaMemsetAsync(p->d_ctl, 0, sizeof(int) * (size_t)p->nctl, s);  // level words (barrier counters)
     if (p->liveLev >= 0) cudaMemsetAsync(p->d_liveCtl, 0, sizeof(int) * 8, s);   // live words + key words
     if (p->liveTopMerges) cudaMemsetAsync(p->d_liveDone, 0, sizeof(int) * (size_t)p->liveTopMerges, s);
+    if (p->liveFlowMerges)
+        cudaMemsetAsync(p->d_liveFlowDone, 0, sizeof(int) * ((size_t)p->liveFlowMerges + 1), s);
     if (!p->liveBlocks.empty()) cudaMemsetAsync(p->d_liveBctr, 0, sizeof(int) * p->bstart.size(), s);
     launch_prepare(s, n, p->d_bstart, nblk, h->sbits, h->w.dw, h->w.ew, (int)p->cutPos.size(),
                    p->d_cut, launches, prof);
@@ -1355,7 +1427,7 @@ int solve_prepared(Handle* h, int n, const std::vector<int>& segs) {
         if (h->plan) free_plan(h->plan.get());
         h->plan = make_plan(n, h->leaf_cutoff, bstart, segs, !sig && h->subtree != 0 && !h->strace, h->nranks,
                             h->rank, h->sms, !sig && h->sparse != 0 && !h->strace, wantLive,
-                            h->liveCluster ? live_cluster_max(h->device) : 1);
+                            h->liveCluster ? live_cluster_max(h->device) : 1, h->liveFlow != 0);
         p = h->plan.get();
         if (sig) {  // every merge propagates the requested rows: no root-only mode
             p->sigma = true;
@@ -1702,6 +1774,7 @@ int brgpu_set_option(brgpu_handle* hh, int opt, int64_t v) {
         case BRGPU_OPT_SPARSE: set_plan_opt(h, h->sparse, v != 0); return BRGPU_OK;
         case BRGPU_OPT_LIVE: set_plan_opt(h, h->live, v != 0); h->liveVeto = h->liveSkip = 0; return BRGPU_OK;
         case BRGPU_OPT_LIVE_CLUSTER: set_plan_opt(h, h->liveCluster, v != 0); return BRGPU_OK;
+        case BRGPU_OPT_LIVE_FLOW: set_plan_opt(h, h->liveFlow, v != 0); return BRGPU_OK;
         case BRGPU_OPT_VIRTUAL_RANKS:
             if (v < 1 || v > 64) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks must be in [1, 64]");
             if (h->nranks > 1) return fail(h, BRGPU_ERR_INVALID_ARGUMENT, "virtual ranks on a distributed handle");
@@ -1726,6 +1799,7 @@ int brgpu_get_option(const brgpu_handle* hh, int opt, int64_t* v) {
         case BRGPU_OPT_SPARSE: *v = h->sparse; return BRGPU_OK;
         case BRGPU_OPT_LIVE: *v = h->live; return BRGPU_OK;
         case BRGPU_OPT_LIVE_CLUSTER: *v = h->liveCluster; return BRGPU_OK;
+        case BRGPU_OPT_LIVE_FLOW: *v = h->liveFlow; return BRGPU_OK;
         default: return BRGPU_ERR_INVALID_ARGUMENT;
     }
 }

@@ -136,6 +136,11 @@ struct LiveRun {
     int first[kMaxLiveTop + 1];  // CTA offset of each level
     int nlev;
     int* done;                   // one word per merge of the run (zeroed per solve)
+    // lane-mode dataflow run (k_live_flow): work items (level, first merge, merges)
+    // in level order, taken by ticket, so an item only waits on lower tickets
+    const int4* items = nullptr;
+    int nitems = 0;
+    int* ticket = nullptr;       // zeroed per solve
 };
 
 // A run of consecutive fused levels launched as one kernel (k_levels_fused).

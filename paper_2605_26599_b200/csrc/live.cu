@@ -1014,6 +1014,59 @@ __global__ void __launch_bounds__(NT, 1) k_live_cluster(Work w, LevelDev L, Live
     live_group<true, NT, true, LPR>(w, L, V, m, 1, prm, traceOut, S);
 }
 
+// Lane-mode live levels as one dataflow launch: persistent CTAs take work items
+// (G consecutive merges of one level, the per-level launch's CTA share) by
+// ticket, in level order; an item waits until its merges' children (level l - 1
+// merges 2m, 2m + 1 -- api.cpp checks the run is that complete binary tree) have
+// set their done words, so each merge starts when its own inputs are ready and
+// the levels' root tails overlap instead of adding up.  Tickets hand out items
+// children-first, so every awaited item is held by a running CTA.
+__global__ void __launch_bounds__(kLiveThreads, kLiveCtasPerSm) k_live_flow(Work w, LiveRun R, LiveDev V,
+                                                                            SolveParams prm) {
+    pdl_entry();
+    extern __shared__ __align__(16) unsigned char live_raw[];
+    LiveSmem& S = *reinterpret_cast<LiveSmem*>(live_raw);
+    __shared__ int s_item;
+    const int tid = threadIdx.x;
+    for (;;) {
+        if (tid == 0) s_item = atomicAdd(R.ticket, 1);
+        __syncthreads();
+        const int it = s_item;
+        if (it >= R.nitems) return;
+        const int4 I = R.items[it];
+        const int l = I.x, m0 = I.y, cnt = I.z;
+        if (l > 0) {
+            if (tid < 2 * cnt) {
+                const volatile int* f = R.done + R.first[l - 1] + 2 * m0 + tid;
+                while (*f == 0) __nanosleep(128);
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        for (int m = m0; m < m0 + cnt;) {  // batches of the item's merges (k_live_level, MODE 0)
+            if (tid == 0) {
+                int c = 0, sum = 0;
+                while (m + c < m0 + cnt && c < kLiveGroup) {
+                    const int base = R.L[l].mOff[m + c];
+                    const int e = V.cnt[base] + V.cnt[base + R.L[l].mNL[m + c]];
+                    if (c > 0 && sum + e > kLiveMax) break;
+                    sum += e;
+                    ++c;
+                }
+                S.batch = c;
+            }
+            __syncthreads();
+            const int c = S.batch;
+            live_group<false, kLiveThreads>(w, R.L[l], V, m, c, prm, R.trace[l], S);
+            __syncthreads();
+            m += c;
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid < cnt) atomicExch(R.done + R.first[l] + m0 + tid, 1);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Final order: bucket sort of the pool (n values).  Buckets split the value
 // range uniformly (a monotone bucket function, so concatenated buckets are in
@@ -1216,6 +1269,21 @@ void launch_level_live(cudaStream_t s, const Work& w, const LevelDev& L, const L
     if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
 }
 
+// merges per work item of a lane-mode live level of M merges (the per-level
+// launch's CTA share, launch_level_live)
+int live_lane_group(int M, int sms) {
+    const int per = std::max(1, std::min(kLiveGroup, M / (sms * kLiveCtasPerSm)));
+    return std::min(per, kLiveGroupMax);
+}
+
+void launch_live_flow(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
+                      int* launches, Prof* prof) {
+    launch_pdl(k_live_flow, std::min(R.nitems, prm.sms * kLiveCtasPerSm), kLiveThreads, sizeof(LiveSmem), s, w, R,
+               V, prm);
+    *launches += 1;
+    if (prof) prof_mark(prof, (void*)s, BRGPU_K_LIVE);
+}
+
 void launch_live_top(cudaStream_t s, const Work& w, const LiveRun& R, const LiveDev& V, const SolveParams& prm,
                      int* launches, Prof* prof) {
     launch_pdl(k_live_top, R.first[R.nlev], kLiveSplitThreads, sizeof(LiveSmem), s, w, R, V, prm);
@@ -1326,6 +1394,7 @@ void init_live_attributes() {
     cudaFuncSetAttribute(k_live_level<2, kLiveThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_level<3, kLiveM3Threads>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_top, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_live_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_live_cluster<kClThreads, kClLpr>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }

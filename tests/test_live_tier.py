@@ -209,3 +209,28 @@ def test_live_many_split_merges_vs_checker(live_solver):
     w = live_solver.eigvals(d, e)
     assert np.array_equal(w.view(np.int64), ref.view(np.int64)), f"max diff {np.max(np.abs(w - ref)):.3e}"
     assert _live_ran(live_solver, d, e)
+
+
+@pytest.mark.parametrize("fam,n", [("sym-uniform", 1 << 20), ("uniform", 1 << 18), ("normal", 1 << 17)])
+def test_live_flow_matches_per_level(live_solver, fam, n):
+    # the lane-arithmetic live levels as one dataflow launch (k_live_flow: ticketed
+    # work items, a batch starts when its children are done) against one launch per
+    # level: bit-identical eigenvalues and per-merge (nn, K) traces
+    d, e = G.generate(fam, n)
+    s = br.Solver(0, br.BrOptions(live_flow=False))
+    live_solver.set_trace(True)
+    s.set_trace(True)
+    try:
+        w1 = live_solver.eigvals(d, e)
+        t1 = live_solver.trace()
+        w0 = s.eigvals(d, e)
+        t0 = s.trace()
+        import ctypes
+        v = ctypes.c_int64(-1)
+        assert s._lib.brgpu_get_option(s._h, 12, ctypes.byref(v)) == 0 and v.value == 0
+    finally:
+        live_solver.set_trace(False)
+        s.close()
+    assert np.array_equal(w1.view(np.int64), w0.view(np.int64))
+    assert t1 == t0
+    assert np.array_equal(w1, O.eigvals(d, e).w)
