@@ -15,5 +15,5 @@ $NCU --metrics $M -c 900 --csv --log-file $O/launches_c3.csv python tools/ncu_so
 $NCU --metrics $M -c 900 --csv --log-file $O/launches_c4.csv python tools/ncu_solve.py --family wilkinson --n 262144 --reps 2 > $O/launches_c4.log 2>&1
 F="$NCU --set full --import-source on"
 $F -k regex:"k_live_cluster" -s 2 -c 1 -o $O/k_live_cluster python tools/ncu_solve.py --reps 1 > $O/cl.log 2>&1
-$F -k regex:"k_levels_fused" -c 1 -o $O/k_levels_fused_run python tools/ncu_solve.py --reps 1 > $O/fu.log 2>&1
+$F -k regex:"k_live_flow" -c 1 -o $O/k_live_flow python tools/ncu_solve.py --reps 1 > $O/fl.log 2>&1
 ls -la $O

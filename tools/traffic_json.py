@@ -14,7 +14,7 @@ CLASSES = {
     "merge_scatter": ["k_merge_prep", "k_merge_nn"], "segment_walk": ["k_segment_walk"],
     "surv_write": ["k_surv_scan"], "secular": ["k_secular", "k_secular_tiled", "k_secular_warp"],
     "zhat": ["k_zhat", "k_zhat_warp"], "rows": ["k_rows", "k_rows_warp"], "deflated_out": ["k_deflated_out"],
-    "live_level": ["k_live_init", "k_live_level", "k_live_top", "k_live_cluster"],
+    "live_level": ["k_live_init", "k_live_level", "k_live_top", "k_live_cluster", "k_live_flow"],
     "live_sort": ["k_live_bounds", "k_live_hist", "k_live_scan", "k_live_scatter", "k_live_bucket"],
 }
 
