@@ -625,9 +625,6 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
             std::sort(front.begin(), front.end());
             for (auto& f : front) { p->liveFront.push_back(f.first); p->liveFront.push_back(f.second); }
             p->liveNb = live_buckets(n);
-            // dataflow top run: the longest tail of split-arithmetic levels that form
-            // a complete binary tree (merge m of level l = merges 2m, 2m+1 of l - 1)
-            // whose merges are all co-resident
             p->liveCl = liveCl;
             // lane-mode dataflow run: the live levels from the tier's first level
             // up to the split rule, each the complete binary child level of the next
@@ -662,6 +659,9 @@ std::unique_ptr<Plan> make_plan(int n, int cutoff, const std::vector<int>& bstar
                     }
                 }
             }
+            // dataflow top run (clusters off): the longest tail of split-arithmetic
+            // levels that form a complete binary tree (merge m of level l = merges
+            // 2m, 2m+1 of l - 1) whose merges are all co-resident
             const int cap = liveCl > 1 ? 0 : live_top_capacity(sms);  // clusters replace the dataflow run
             size_t t = p->levels.size();
             int merges = 0;
