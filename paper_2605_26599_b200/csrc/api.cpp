@@ -87,9 +87,10 @@ int live_buckets(int n);
 void init_live_attributes();
 // Live-list tier (live.cu): single-block solves of at least kLiveMinN elements
 // run every level above the last fused / small one on live lists when all those
-// levels' merges are >= kLiveMinSize (random 2^20: levels 4..16)
+// levels' merges are >= kLiveMinSize (random 2^20: levels 5..16).  512 since the
+// lane levels run as one dataflow launch (C5 -0.015 ms against 1024; 256 +0.03 ms)
 #ifndef BRGPU_LIVE_MIN_SIZE
-#define BRGPU_LIVE_MIN_SIZE 1024
+#define BRGPU_LIVE_MIN_SIZE 512
 #endif
 constexpr int kLiveMinSize = BRGPU_LIVE_MIN_SIZE;
 constexpr int kLiveMinN = 1 << 15;
